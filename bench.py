@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark of the decomposed multi-frontal SOR sweep (arXiv 1008.3699) on B200.
+
+Metric (BASELINE.json): lattice-point sweep updates per second (GLUP/s) and the
+fraction of the HBM roofline.  Workload at N=1 (config 4 of BASELINE.json, the
+1/2/4/8-GPU scaling config): 2D 5-point Poisson on 16384 x 16384 fp64, Dirichlet 0,
+b = h^2 f with f ~ U[-1,1) (seeded, gen.py), 64 x 64 boxes, omega = 2/(1+sin(pi h)).
+One step = one decomposed SOR sweep over the whole grid (schedule, ghost refresh,
+corner/edge coupled solves, interior wavefront, write-back: SURVEY §8(a) a2-a8).
+For N > 1 (torchrun): weak scaling, 16384 x (16384 N), row slabs of 256 tile rows per
+rank, ghost layers exchanged with NCCL before every sweep.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_PER_LUP_POISSON = 24          # x_old read, x_new write, b read
+NX = 16384
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def rhs_slab(seed, rows, row0, nx, h):
+    from paper_1008_3699_b200 import gen
+    f = gen.uniform(seed, gen.STREAM_RHS, rows * nx, start=row0 * nx)
+    return (f * (h * h)).reshape(rows, nx)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1008_3699_b200 import binding, parallel
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    binding.load()
+    T = 64
+    ny = NX * world                        # weak scaling: 16384 x 16384 per GPU
+    n = (NX, ny)
+    h = 1.0 / (NX + 1)
+    omega = 2.0 / (1.0 + np.sin(np.pi * h))
+    g = binding.Grid(2, n, binding.COEF_POISSON, 0.0, local).decompose((T, T), rank, world)
+    nl_y = g.n_local[1]
+    row0 = g.slab_offset
+    b = rhs_slab(args.seed, nl_y, row0, NX, h)
+    g.set_vector(binding.B, b)
+    g.set_vector(binding.X, np.zeros((nl_y, NX)))
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        # b's ghost rows (partner nodes' right-hand sides) once; x's every sweep
+        parallel.exchange_ghosts(g.view(binding.B), nl_y, rank, world)
+    bufs = {}
+
+    def step(phase):
+        if world > 1:
+            parallel.exchange_ghosts(g.view(binding.X), nl_y, rank, world, bufs=bufs)
+        return g.sor_sweep([omega], 1, phase)
+
+    phase = 0
+    for _ in range(args.warmup):
+        phase = step(phase)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = g.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            phase = step(phase)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = g.launch_count() - l0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nodes_total = NX * ny
+    glups = nodes_total * args.steps / (ms * 1e-3) / 1e9
+    ms_per_step = ms / args.steps
+
+    # dominant kernel = the sweep kernel (the only kernel of a single-GPU step); its per-launch
+    # duration from CUDA events on the launching stream, one launch per event pair
+    kern_ms = []
+    if world == 1:
+        for _ in range(min(args.steps, 10)):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            phase = g.sor_sweep([omega], 1, phase)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            kern_ms.append(e0.elapsed_time(e1))
+    else:
+        kern_ms = [ms_per_step]
+    peak, peak_src = peaks()
+    per_launch_bytes = B_PER_LUP_POISSON * (NX * nl_y)
+    kavg = float(np.mean(kern_ms))
+    achieved = per_launch_bytes / (kavg * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "sweep2d_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+
+    # end-to-end through the public API with HOST buffers: one user job = upload b and x0 from
+    # pinned host memory, 200 sweeps (config 4's count), download x; time with events
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        hb = torch.from_numpy(b).pin_memory()
+        hx = torch.zeros((nl_y, NX), dtype=torch.float64).pin_memory()
+        hout = torch.empty((nl_y, NX), dtype=torch.float64).pin_memory()
+        nsw = 200
+        times = []
+        for rep in range(2):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.set_vector(binding.B, hb)
+            g.set_vector(binding.X, hx)
+            g.sor_sweep([omega], nsw, 0)
+            g.get_vector(binding.X, hout)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        t = min(times)
+        e2e = {"value": round(NX * nl_y * nsw / (t * 1e-3) / 1e9, 3), "unit": "GLUP/s",
+               "h2d_bytes_per_step": int(2 * NX * nl_y * 8), "d2h_bytes_per_step": int(NX * nl_y * 8),
+               "step": f"one job: b,x0 H2D from pinned host + {nsw} sweeps + x D2H", "ms_per_job": round(t, 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.seed, args.cpu_n, args.cpu_sweeps)
+
+    if rank == 0:
+        line = {
+            "metric": "lattice-point sweep updates/sec (GLUP/s), decomposed SOR sweep",
+            "value": round(glups, 3), "unit": "GLUP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1) rhs, gen.py)",
+            "config": {"workload": "BASELINE config 4: 2D 5-point Poisson 16384 x 16384*N fp64, 64x64 boxes, "
+                                   "SOR omega_opt, row slabs per GPU",
+                       "n": [NX, ny], "tile": [T, T], "omega": omega, "parallelism": f"slab{world}",
+                       "l2": "inputs (2.1 GB per array) exceed the 126 MB L2; no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "sweep (decomposed SOR, 24 algorithmic B/LUP)", "peak_source": peak_src,
+                         "kernel_ms": round(kavg, 4)},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "cpu_baseline": cpu,
+        }
+        line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(seed, n, sweeps):
+    """The oracle as it stands, single-threaded, on an n x n sample of the same workload."""
+    import oracle as O
+    pb = O.tiled((n, n), (64, 64))
+    h = 1.0 / (NX + 1)
+    b = rhs_slab(seed, n, 0, n, h)
+    x = np.zeros(pb.shape)
+    t0 = time.perf_counter()
+    for k in range(sweeps):
+        x = O.sweep(pb, [2.0 / (1.0 + np.sin(np.pi * h))], x, b, phase=k)
+    dt = time.perf_counter() - t0
+    return {"value": round(n * n * sweeps / dt / 1e9, 6), "unit": "GLUP/s", "cores": 1, "kind": "oracle",
+            "sample": f"{sweeps} decomposed SOR sweeps on a {n}x{n} sub-grid (64x64 boxes), same per-node work",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    n = args.ref_n
+    pb = O.tiled((n, n), (64, 64))
+    h = 1.0 / (NX + 1)
+    b = rhs_slab(args.seed, n, 0, n, h)
+    w = [2.0 / (1.0 + np.sin(np.pi * h))]
+    x = np.zeros(pb.shape)
+    for k in range(args.warmup):
+        x = O.sweep(pb, w, x, b, phase=k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        x = O.sweep(pb, w, x, b, phase=k)
+    dt = time.perf_counter() - t0
+    v = n * n * args.steps / dt / 1e9
+    line = {"impl": "reference", "metric": "lattice-point sweep updates/sec (GLUP/s), decomposed SOR sweep",
+            "value": round(v, 6), "unit": "GLUP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1) rhs, gen.py)",
+            "config": {"workload": "BASELINE config 4 sweep, bounded CPU sample", "n": [n, n], "tile": [64, 64]},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GLUP/s", "cores": 1, "kind": "oracle",
+                             "sample": f"each step = 1 sweep of a {n}x{n} sub-grid of config 4"},
+            "e2e": {"value": round(v, 6), "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-n", type=int, default=4096)
+    ap.add_argument("--cpu-sweeps", type=int, default=2)
+    ap.add_argument("--ref-n", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

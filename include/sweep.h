@@ -1,0 +1,156 @@
+/*
+ * sweep.h -- C ABI of the B200 (sm_100a) implementation of the decomposed multi-frontal
+ * SOR / SSOR / ILU(0) sweeps of arXiv 1008.3699 (Tavakoli, "Parallelizing sequential
+ * sweeping on structured grids").  Citations "PAPER:n" are line numbers of the paper's
+ * text; "R-n" are the readings listed in DESIGN.md §3.
+ *
+ * Problem (PAPER:163-216 1D, 394-459 2D, 860-895 3D):  A u = b on a structured grid of
+ * n_0 x n_1 x n_2 interior nodes (x fastest), 2d+1-point stencil
+ *     (A u)_p = a_P,p u_p - sum_{q nbr of p} c_pq u_q,   a_P,p = sum_q c_pq + beta,
+ * Dirichlet data folded into b (so every node outside the domain has value 0).
+ * c_pq is the coefficient of the face between p and q (all 1 for SW_COEF_POISSON).
+ *
+ * Decomposition: the grid is cut into boxes of
+ * tile[0] x tile[1] x tile[2] nodes (tile must divide n).  In sweep k box r starts at
+ * the corner with start bits s_a = c_a(k mod 2^d) XOR (r_a mod 2) (bit a set = starts at
+ * the max end of axis a), c = [LR, RL] (1D), [NE, SW, NW, SE] (2D), the 8-cycle
+ * [(111),(000),(011),(100),(101),(010),(110),(001)] (3D) (R-4, R-5).  Direction index
+ * of a box = sum_a s_a << a; omega arrays are indexed by it (1D: 0 = LR, 1 = RL;
+ * 2D: 0 = SW, 1 = SE, 2 = NW, 3 = NE).
+ *
+ * Multi-GPU: the slowest used axis (y in 2D, z in 3D) is split into contiguous slabs of
+ * whole tile rows, one per rank.  Every per-node array on the device carries 2 ghost
+ * layers on each side of every axis; the ghost layers of the slab axis hold the
+ * neighbouring ranks' values and are refreshed by the caller through sw_ghost_view()
+ * (the Python binding does this with torch.distributed / NCCL).
+ *
+ * Conventions.  Every call returns sw_status; nothing aborts the process; on error
+ * sw_last_error() returns a thread-local message.  The library owns all device memory
+ * it allocates; host inputs are copied.  All work is ordered on the cudaStream_t given
+ * (NULL = legacy default stream); only sw_residual_norm, sw_pcg_solve and
+ * sw_check_status synchronise.  Arrays passed in are fp64, x fastest ("numpy C order
+ * with shape (n2, n1, n0)").
+ */
+#ifndef SWEEP_H
+#define SWEEP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sw_grid sw_grid; /* opaque */
+typedef struct CUstream_st *sw_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    SW_OK = 0,
+    SW_EINVAL = 1,     /* bad argument (sizes, tile, omega outside (0,2), coefficient <= 0, ...) */
+    SW_ESINGULAR = 2,  /* a coupled system had |pivot| < 1e-14 or an ILU pivot D~ <= 0 */
+    SW_ENOCONV = 3,    /* PCG hit maxit (outputs still valid) */
+    SW_ECUDA = 4,      /* CUDA runtime error */
+    SW_ENOMEM = 6,     /* device allocation failed */
+    SW_ESTATE = 7      /* call out of order (e.g. ilu_apply before ilu0_factor) */
+} sw_status;
+
+typedef enum { SW_COEF_POISSON = 0, SW_COEF_FACES = 1 } sw_coef;
+typedef enum { SW_PC_NONE = 0, SW_PC_SSOR = 1, SW_PC_ILU0 = 2 } sw_precond;
+/* SYMMETRIC: P = (D~+L) D~^-1 (D~+L)^T;  PAPER: P = (D~+L) D~^-1 (D~+U), U = A_E(k0) (R-C) */
+typedef enum { SW_PAIR_SYMMETRIC = 0, SW_PAIR_PAPER = 1 } sw_pairing;
+typedef enum { SW_X = 0, SW_B = 1, SW_R = 2, SW_Z = 3, SW_P = 4, SW_Q = 5, SW_INVD = 6, SW_Y = 7 } sw_vector;
+
+/* Create a grid of n[0..dim-1] GLOBAL interior nodes.  kind = SW_COEF_POISSON (unit
+ * faces) or SW_COEF_FACES (coefficients supplied by sw_set_faces / sw_set_coefficients_k
+ * after sw_decompose).  beta >= 0.  Selects cuda_device.  No device memory is allocated
+ * until sw_decompose.  *out is NULL on error. */
+sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, double beta, int cuda_device, sw_grid **out);
+
+/* Fix the box shape (tile[a] must divide n[a]) and this rank's slab: rank r of nranks
+ * owns tile rows [r*R/nranks, (r+1)*R/nranks) of the slowest axis (R = n_slow/tile_slow,
+ * nranks must divide R).  Allocates the device arrays (2 iterate buffers, b, faces, ILU
+ * and PCG work vectors) for the local slab plus 2 ghost layers per side of every axis,
+ * all zero. */
+sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int nranks);
+
+/* Local slab geometry: n_local[3] (x,y,z), slab offset (global index of the first local
+ * node along the slab axis), padded dims pad[3] of every device array and the element
+ * offset of local node (0,0,0) in it.  Device arrays are x-fastest with strides
+ * (1, pad[0], pad[0]*pad[1]). */
+sw_status sw_local_shape(const sw_grid *g, int64_t n_local[3], int64_t *slab_offset, int64_t pad[3],
+                         int64_t *origin);
+
+/* Copy a per-node vector in / out.  src/dst hold the LOCAL slab interior (n_local
+ * nodes, x fastest); *_is_device selects host or device memory.  sw_set_vector(SW_X)
+ * sets the current iterate; SW_B the right-hand side.  Ghost layers are not touched
+ * (refresh them with sw_ghost_view after setting, when nranks > 1). */
+sw_status sw_set_vector(sw_grid *g, sw_vector which, const double *src, int src_is_device, sw_stream_t s);
+sw_status sw_get_vector(const sw_grid *g, sw_vector which, double *dst, int dst_is_device, sw_stream_t s);
+
+/* Device pointer of the padded array `which` (the current iterate for SW_X) so callers
+ * can exchange ghost layers.  Borrowed; valid until sw_destroy / the next sweep swaps
+ * the iterate buffers. */
+sw_status sw_ghost_view(sw_grid *g, sw_vector which, double **dev_ptr);
+
+/* Face coefficients.  face_host[a] is the array of faces normal to axis a for the
+ * local slab extended by 2 node layers on each side of the slab axis: shape n_local
+ * with n_a + 1 along axis a, and n_slow_local + 4 (+1 if a is the slab axis) along the
+ * slab axis; entry [c] is the face between node c - e_a and node c (c in slab-local
+ * coordinates, slab axis shifted by 2).  Every face must be > 0 except those outside the
+ * physical domain, which are ignored.  (PAPER:189-197, 429-448.) */
+sw_status sw_set_faces(sw_grid *g, const double *const face_host[3], sw_stream_t s);
+
+/* Assemble faces on the device from node diffusivities:
+ *   face_a(p,q) = scale[a] * ((2 k_p) k_q) / (k_p + k_q).
+ * k_host covers the local slab with a one-node ring on the non-slab axes (n_a + 2 nodes,
+ * index 0 = coordinate -1) and two extra layers on each side of the slab axis
+ * (n_slow_local + 4 layers, index 0 = coordinate -2); entries outside the physical
+ * domain's node ring are ignored.  k > 0. */
+sw_status sw_set_coefficients_k(sw_grid *g, const double *k_host, const double scale[3], sw_stream_t s);
+
+/* nsweeps decomposed SOR sweeps (PAPER:326-346 1D, 524-693 2D, 860-895 3D) starting at
+ * phase *phase_inout; on return *phase_inout += nsweeps.  omega holds 1 value (all
+ * directions) or 2^dim values indexed by direction bits, each in (0, 2).  Each sweep
+ * solves (D/Omega + A_I(k)) u+ = b + (D/Omega - D) u - A_E(k) u exactly, i.e. every box
+ * is relaxed from its start corner with the coupled 2x2 / 4x4 / 8x8 systems at faces
+ * where two boxes start.  Single rank only for nsweeps > 1; with
+ * nranks > 1 call with nsweeps = 1 and refresh the SW_X ghost layers before each call. */
+sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, int nsweeps, int64_t *phase_inout,
+                       sw_stream_t s);
+
+/* ||b - A x||_2 / ||b||_2 of the current iterate (single rank; synchronises). */
+sw_status sw_residual_norm(sw_grid *g, double *rel_out, sw_stream_t s);
+
+/* D-ILU(0) factor at phase k0 (R-C): D~_p = a_P,p - sum_{q implicit for p, same box}
+ * c_pq^2 / D~_q, stored as 1/D~ in SW_INVD.  Tile-local.  SW_ESINGULAR (reported at the
+ * next synchronising call or sw_check_status) if some D~ <= 0. */
+sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s);
+
+/* z = P^-1 r for the D-ILU(0) of sw_ilu0_factor.  r_dev / z_dev are device pointers to
+ * PADDED arrays of the layout reported by sw_local_shape (e.g. from sw_ghost_view);
+ * r's ghost layers must be current.  Borrowed.  Single rank. */
+sw_status sw_ilu_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_pairing pairing, sw_stream_t s);
+
+/* Same for the SSOR / SGS preconditioner z = w(2-w)(D + w L^T)^-1 D (D + w L)^-1 r at the
+ * factor phase. */
+sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev, double *z_dev, sw_pairing pairing,
+                        sw_stream_t s);
+
+/* Preconditioned CG from x0 = 0 on the right-hand side SW_B until ||r||/||b|| < rtol
+ * (recursive residual) or maxit; result in SW_X.  precond SW_PC_ILU0 factors at phase 0
+ * first.  SW_ENOCONV: iters/relres still valid.  Single rank. */
+sw_status sw_pcg_solve(sw_grid *g, sw_precond precond, double omega, sw_pairing pairing, double rtol, int maxit,
+                       int *iters_out, double *relres_out, sw_stream_t s);
+
+/* Synchronise `s` and report a deferred device-side error (singular coupled system). */
+sw_status sw_check_status(sw_grid *g, sw_stream_t s);
+
+/* Number of kernel launches this grid has issued (for the bench's gpu_launches). */
+int64_t sw_launch_count(const sw_grid *g);
+
+sw_status sw_destroy(sw_grid *g);
+const char *sw_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -382,7 +382,8 @@ int or_sor_lex(const or_grid *g, double omega, int corner_bits, double *x, const
     return OR_OK;
 }
 
-/* y = A x  (PAPER eq d2d, 426-428; 1D eq d1d, 184) */
+/* y = A x  (PAPER eq d2d, 426-428; 1D eq d1d, 184), evaluated as
+ *   s = a_P x_p;  s = fma(-c_pq, x_q, s) over neighbours in axis order (-, +)   (R-7) */
 void or_apply_A(const or_grid *g, const double *xv, double *y) {
     int64_t N = n_nodes(g);
     for (int64_t i = 0; i < N; ++i) {
@@ -393,10 +394,34 @@ void or_apply_A(const or_grid *g, const double *xv, double *y) {
             for (int sd = -1; sd <= 1; sd += 2) {
                 int64_t q[3] = {c[0], c[1], c[2]};
                 q[a] += sd;
-                if (inside(g, q)) s -= face_between(g, c, a, sd) * xv[lin(g, q)];
+                if (inside(g, q)) s = fma(-face_between(g, c, a, sd), xv[lin(g, q)], s);
             }
         y[i] = s;
     }
+}
+
+/* Accurate dot product: error-free transformations (TwoProd by fma, TwoSum) accumulate
+ * sum a_i b_i in double-double (~106 bits) before the final rounding, so the value is the
+ * correctly rounded exact sum except in pathological near-tie cases. */
+typedef struct { double hi, lo; } dd_t;
+
+static void dd_add(dd_t *s, double p) {
+    double t = s->hi + p;
+    double bp = t - s->hi;
+    double err = (s->hi - (t - bp)) + (p - bp);
+    s->hi = t;
+    s->lo += err;
+}
+
+static double dot_dd(int64_t N, const double *a, const double *b) {
+    dd_t s = {0.0, 0.0};
+    for (int64_t i = 0; i < N; ++i) {
+        double p = a[i] * b[i];
+        double e = fma(a[i], b[i], -p);
+        dd_add(&s, p);
+        s.lo += e;
+    }
+    return s.hi + s.lo;
 }
 
 /* ||b - A x||_2 / ||b||_2 (stop test of the configs; replaces the paper's L1 error) */
@@ -405,12 +430,8 @@ double or_relres(const or_grid *g, const double *xv, const double *b) {
     double *y = (double *)malloc(sizeof(double) * (size_t)N);
     if (!y) return -1.0;
     or_apply_A(g, xv, y);
-    double rr = 0.0, bb = 0.0;
-    for (int64_t i = 0; i < N; ++i) {
-        double r = b[i] - y[i];
-        rr += r * r;
-        bb += b[i] * b[i];
-    }
+    for (int64_t i = 0; i < N; ++i) y[i] = b[i] - y[i];
+    double rr = dot_dd(N, y, y), bb = dot_dd(N, b, b);
     free(y);
     return bb > 0.0 ? sqrt(rr) / sqrt(bb) : sqrt(rr);
 }
@@ -530,12 +551,9 @@ out:
  * preconditioners).  x0 = 0, r0 = b; stop when ||r||/||b|| < rtol on
  * the recursively updated residual.  precond: 0 none, 1 SSOR(omega), 2 D-ILU(0).
  * flexible != 0 uses the Polak-Ribiere beta = z+.(r+ - r)/(r.z) (needed for the
- * nonsymmetric PAPER pairing).  Dot products are plain sequential sums. */
-static double dot(int64_t N, const double *a, const double *b) {
-    double s = 0.0;
-    for (int64_t i = 0; i < N; ++i) s += a[i] * b[i];
-    return s;
-}
+ * nonsymmetric PAPER pairing).  Dot products are accurate (dot_dd); updates are
+ * x = fma(alpha, p, x), r = fma(-alpha, q, r), p = fma(beta, p, z). */
+static double dot(int64_t N, const double *a, const double *b) { return dot_dd(N, a, b); }
 
 int or_pcg(const or_grid *g, int precond, double omega, int pairing, int flexible, int64_t phase, int ov,
            double rtol, int maxit, const double *b, double *xo, int *iters, double *relres) {
@@ -575,8 +593,8 @@ int or_pcg(const or_grid *g, int precond, double omega, int pairing, int flexibl
         double al = rz / pq;
         if (flexible) memcpy(rold, r, sizeof(double) * (size_t)N);
         for (int64_t i = 0; i < N; ++i) {
-            xo[i] += al * p[i];
-            r[i] -= al * q[i];
+            xo[i] = fma(al, p[i], xo[i]);
+            r[i] = fma(-al, q[i], r[i]);
         }
         double rr = dot(N, r, r);
         *iters = it;
@@ -585,14 +603,13 @@ int or_pcg(const or_grid *g, int precond, double omega, int pairing, int flexibl
         APPLY_M(r, z);
         double rzn = dot(N, r, z), be;
         if (flexible) {
-            double s = 0.0;
-            for (int64_t i = 0; i < N; ++i) s += z[i] * (r[i] - rold[i]);
-            be = s / rz;
+            for (int64_t i = 0; i < N; ++i) rold[i] = r[i] - rold[i];
+            be = dot(N, z, rold) / rz;
         } else {
             be = rzn / rz;
         }
         rz = rzn;
-        for (int64_t i = 0; i < N; ++i) p[i] = z[i] + be * p[i];
+        for (int64_t i = 0; i < N; ++i) p[i] = fma(be, p[i], z[i]);
     }
 #undef APPLY_M
 out:

@@ -1,0 +1,250 @@
+"""Thin Python binding of the C ABI in include/sweep.h (argument marshalling only).
+
+Every step of the method runs in the CUDA library ``libsweep.so`` (built in-tree for
+sm_100a by ``paper_1008_3699_b200.build``).  There is no CPU fallback: ``load()``
+raises if the library or a GPU is missing.  PyTorch is used only for device memory
+views, streams and (in ``parallel.py``) process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsweep.so")
+
+SW_OK, SW_EINVAL, SW_ESINGULAR, SW_ENOCONV, SW_ECUDA, SW_ENOMEM, SW_ESTATE = 0, 1, 2, 3, 4, 6, 7
+COEF_POISSON, COEF_FACES = 0, 1
+PC_NONE, PC_SSOR, PC_ILU0 = 0, 1, 2
+PAIR_SYMMETRIC, PAIR_PAPER = 0, 1
+X, B, R, Z, P, Q, INVD, Y = range(8)
+
+_lib = None
+
+
+class SweepError(RuntimeError):
+    def __init__(self, code: int, what: str, msg: str):
+        super().__init__(f"{what} failed: status {code}: {msg}")
+        self.code = code
+
+
+def load():
+    """Load libsweep.so (the CUDA path).  Fails loudly if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA extension {LIB_PATH} is missing: run paper_1008_3699_b200.build.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P_ = ctypes.c_void_p
+    I64 = ctypes.c_int64
+    I = ctypes.c_int
+    D = ctypes.c_double
+    L.sw_create_grid.argtypes = [I, P_, I, D, I, ctypes.POINTER(P_)]
+    L.sw_decompose.argtypes = [P_, P_, I, I]
+    L.sw_local_shape.argtypes = [P_, P_, P_, P_, P_]
+    L.sw_set_vector.argtypes = [P_, I, P_, I, P_]
+    L.sw_get_vector.argtypes = [P_, I, P_, I, P_]
+    L.sw_ghost_view.argtypes = [P_, I, ctypes.POINTER(P_)]
+    L.sw_set_faces.argtypes = [P_, P_, P_]
+    L.sw_set_coefficients_k.argtypes = [P_, P_, P_, P_]
+    L.sw_sor_sweep.argtypes = [P_, P_, I, I, ctypes.POINTER(I64), P_]
+    L.sw_residual_norm.argtypes = [P_, ctypes.POINTER(D), P_]
+    L.sw_ilu0_factor.argtypes = [P_, I64, P_]
+    L.sw_ilu_apply.argtypes = [P_, P_, P_, I, P_]
+    L.sw_ssor_apply.argtypes = [P_, D, P_, P_, I, P_]
+    L.sw_pcg_solve.argtypes = [P_, I, D, I, D, I, ctypes.POINTER(I), ctypes.POINTER(D), P_]
+    L.sw_check_status.argtypes = [P_, P_]
+    L.sw_launch_count.argtypes = [P_]
+    L.sw_launch_count.restype = I64
+    L.sw_destroy.argtypes = [P_]
+    L.sw_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(st: int, what: str, allow=()):
+    if st != SW_OK and st not in allow:
+        raise SweepError(st, what, load().sw_last_error().decode())
+    return st
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return int(stream)
+
+
+class _CAI:
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _host_ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Grid:
+    """A structured grid with its decomposition, owned device arrays and operations."""
+
+    def __init__(self, dim: int, n: Sequence[int], kind: int = COEF_POISSON, beta: float = 0.0, device: int = 0):
+        L = load()
+        self.dim = dim
+        self.n = tuple(int(v) for v in n)
+        nn = (ctypes.c_int64 * 3)(*(list(self.n) + [1] * (3 - dim)))
+        h = ctypes.c_void_p()
+        _check(L.sw_create_grid(dim, nn, kind, float(beta), int(device), ctypes.byref(h)), "sw_create_grid")
+        self.h = h
+        self.kind = kind
+        self.device = device
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                load().sw_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- geometry
+    def decompose(self, tile: Sequence[int], rank: int = 0, nranks: int = 1):
+        t = (ctypes.c_int * 3)(*(list(tile) + [1] * (3 - self.dim)))
+        _check(load().sw_decompose(self.h, t, int(rank), int(nranks)), "sw_decompose")
+        nl = (ctypes.c_int64 * 3)()
+        pad = (ctypes.c_int64 * 3)()
+        off = ctypes.c_int64()
+        org = ctypes.c_int64()
+        _check(load().sw_local_shape(self.h, nl, ctypes.byref(off), pad, ctypes.byref(org)), "sw_local_shape")
+        self.n_local = tuple(nl[a] for a in range(self.dim))
+        self.slab_offset = off.value
+        self.pad = tuple(pad[a] for a in range(3))
+        self.origin = org.value
+        self.tile = tuple(tile)
+        self.rank, self.nranks = rank, nranks
+        return self
+
+    @property
+    def local_shape(self):
+        """numpy shape of the local slab interior (slow axis first)."""
+        return tuple(reversed(self.n_local))
+
+    @property
+    def padded_shape(self):
+        return tuple(reversed(self.pad[: self.dim]))
+
+    # -------------------------------------------------------------- vectors
+    def set_vector(self, which: int, src, stream=None):
+        """src: local-slab interior values (numpy array, or torch tensor on host/device)."""
+        try:
+            import torch
+            if isinstance(src, torch.Tensor):
+                assert src.dtype == torch.float64 and src.is_contiguous()
+                assert src.numel() == int(np.prod(self.n_local))
+                _check(load().sw_set_vector(self.h, which, ctypes.c_void_p(src.data_ptr()), int(src.is_cuda),
+                                            _stream(stream)), "sw_set_vector")
+                return
+        except ImportError:
+            pass
+        a = np.ascontiguousarray(np.asarray(src, dtype=np.float64))
+        assert a.size == int(np.prod(self.n_local)), (a.shape, self.n_local)
+        _check(load().sw_set_vector(self.h, which, _host_ptr(a), 0, _stream(stream)), "sw_set_vector")
+        self.sync(stream)
+
+    def get_vector(self, which: int, out=None, stream=None):
+        if out is None:
+            out = np.empty(self.local_shape)
+        try:
+            import torch
+            if isinstance(out, torch.Tensor):
+                _check(load().sw_get_vector(self.h, which, ctypes.c_void_p(out.data_ptr()), int(out.is_cuda),
+                                            _stream(stream)), "sw_get_vector")
+                return out
+        except ImportError:
+            pass
+        _check(load().sw_get_vector(self.h, which, _host_ptr(out), 0, _stream(stream)), "sw_get_vector")
+        self.sync(stream)
+        return out
+
+    def view(self, which: int):
+        """torch tensor (padded shape) aliasing the library's device array (borrowed)."""
+        import torch
+        p = ctypes.c_void_p()
+        _check(load().sw_ghost_view(self.h, which, ctypes.byref(p)), "sw_ghost_view")
+        return torch.as_tensor(_CAI(p.value, self.padded_shape), device=f"cuda:{self.device}")
+
+    def ptr(self, which: int) -> int:
+        p = ctypes.c_void_p()
+        _check(load().sw_ghost_view(self.h, which, ctypes.byref(p)), "sw_ghost_view")
+        return p.value
+
+    # -------------------------------------------------------------- coefficients
+    def set_faces_slab(self, faces_ext, stream=None):
+        """faces_ext[a]: slab-extended face arrays (see sw_set_faces)."""
+        arrs = [np.ascontiguousarray(f, dtype=np.float64) for f in faces_ext]
+        ptrs = (ctypes.c_void_p * 3)(*([a.ctypes.data for a in arrs] + [None] * (3 - self.dim)))
+        _check(load().sw_set_faces(self.h, ptrs, _stream(stream)), "sw_set_faces")
+
+    def set_faces_global(self, faces, stream=None):
+        """Single rank convenience: faces in the oracle layout (face[a] has n_a+1 along axis a)."""
+        ext = []
+        for a, f in enumerate(faces):
+            f = np.asarray(f, dtype=np.float64)
+            pad = [(0, 0)] * self.dim
+            pad[0] = (2, 2)                                     # numpy axis 0 = slab (slowest) axis
+            ext.append(np.pad(f, pad))
+        self.set_faces_slab(ext, stream)
+
+    def set_coefficients_k(self, k_ext, scale=(1.0, 1.0, 1.0), stream=None):
+        k = np.ascontiguousarray(np.asarray(k_ext, dtype=np.float64))
+        sc = np.ascontiguousarray(np.asarray(list(scale) + [1.0] * (3 - len(scale)), dtype=np.float64)[:3])
+        _check(load().sw_set_coefficients_k(self.h, _host_ptr(k), _host_ptr(sc), _stream(stream)),
+               "sw_set_coefficients_k")
+
+    # -------------------------------------------------------------- operations
+    def sor_sweep(self, omega, nsweeps: int = 1, phase: int = 0, stream=None) -> int:
+        w = np.ascontiguousarray(np.atleast_1d(np.asarray(omega, dtype=np.float64)))
+        ph = ctypes.c_int64(int(phase))
+        _check(load().sw_sor_sweep(self.h, _host_ptr(w), len(w), int(nsweeps), ctypes.byref(ph), _stream(stream)),
+               "sw_sor_sweep")
+        self._w = w
+        return ph.value
+
+    def residual_norm(self, stream=None) -> float:
+        r = ctypes.c_double()
+        _check(load().sw_residual_norm(self.h, ctypes.byref(r), _stream(stream)), "sw_residual_norm")
+        return r.value
+
+    def ilu0_factor(self, phase: int = 0, stream=None):
+        _check(load().sw_ilu0_factor(self.h, int(phase), _stream(stream)), "sw_ilu0_factor")
+
+    def ilu_apply(self, r_ptr: int, z_ptr: int, pairing: int = PAIR_SYMMETRIC, stream=None):
+        _check(load().sw_ilu_apply(self.h, ctypes.c_void_p(r_ptr), ctypes.c_void_p(z_ptr), int(pairing),
+                                   _stream(stream)), "sw_ilu_apply")
+
+    def ssor_apply(self, omega: float, r_ptr: int, z_ptr: int, pairing: int = PAIR_SYMMETRIC, stream=None):
+        _check(load().sw_ssor_apply(self.h, float(omega), ctypes.c_void_p(r_ptr), ctypes.c_void_p(z_ptr),
+                                    int(pairing), _stream(stream)), "sw_ssor_apply")
+
+    def pcg_solve(self, precond: int = PC_ILU0, omega: float = 1.0, pairing: int = PAIR_SYMMETRIC,
+                  rtol: float = 1e-8, maxit: int = 10000, stream=None):
+        it = ctypes.c_int()
+        rr = ctypes.c_double()
+        st = _check(load().sw_pcg_solve(self.h, int(precond), float(omega), int(pairing), float(rtol), int(maxit),
+                                        ctypes.byref(it), ctypes.byref(rr), _stream(stream)), "sw_pcg_solve",
+                    allow=(SW_ENOCONV,))
+        return it.value, rr.value, st == SW_OK
+
+    def check(self, stream=None):
+        _check(load().sw_check_status(self.h, _stream(stream)), "sw_check_status")
+
+    def sync(self, stream=None):
+        import torch
+        torch.cuda.synchronize(self.device)
+
+    def launch_count(self) -> int:
+        return int(load().sw_launch_count(self.h))

@@ -1,0 +1,242 @@
+// blas.cuh -- PCG vector kernels with fused, deterministic reductions (north_star
+// "PCG driver with fused dot-product/axpy reductions").
+//
+// Every reduction writes one partial per CTA (fixed thread order inside the CTA) and a
+// single-CTA finisher sums the partials in CTA order, so results are bitwise
+// reproducible run to run.  Interior nodes are addressed by a flattened local index;
+// ghost layers of the padded arrays are never written here.
+#pragma once
+#include "common.cuh"
+
+namespace sw {
+
+constexpr int RED_THREADS = 256;
+constexpr int RED_BLOCKS = 1184;   // 8 x 148 SMs
+
+// Accurate reductions: every dot product is accumulated in double-double (TwoProd by fma,
+// TwoSum), per thread, then per CTA in fixed warp-shuffle order, then across CTAs in CTA
+// order; the final hi + lo is the correctly rounded exact sum except in near-tie cases,
+// which makes PCG iterates independent of the reduction tree (PCG parity).
+struct DD {
+    double hi, lo;
+};
+
+__device__ inline void dd_add(DD &s, double p) {
+    double t = s.hi + p;
+    double bp = t - s.hi;
+    double err = (s.hi - (t - bp)) + (p - bp);
+    s.hi = t;
+    s.lo += err;
+}
+
+__device__ inline void dd_add_prod(DD &s, double a, double b) {
+    double p = a * b;
+    double e = fma(a, b, -p);
+    dd_add(s, p);
+    s.lo += e;
+}
+
+__device__ inline DD dd_merge(DD a, DD b) {
+    DD r = a;
+    dd_add(r, b.hi);
+    r.lo += b.lo;
+    double t = r.hi + r.lo;          // renormalise
+    r.lo = r.lo - (t - r.hi);
+    r.hi = t;
+    return r;
+}
+
+__device__ inline DD block_sum_dd(DD v, DD *sh) {
+    for (int o = 16; o > 0; o >>= 1) {
+        DD w;
+        w.hi = __shfl_down_sync(0xffffffffu, v.hi, o);
+        w.lo = __shfl_down_sync(0xffffffffu, v.lo, o);
+        v = dd_merge(v, w);
+    }
+    int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[wi] = v;
+    __syncthreads();
+    DD s = {0.0, 0.0};
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = dd_merge(s, sh[i]);
+    __syncthreads();
+    return s;
+}
+
+__device__ inline int64_t interior_index(const Geo &G, int64_t t) {
+    int64_t i0 = t % G.n[0];
+    int64_t r = t / G.n[0];
+    int64_t i1 = r % G.n[1];
+    int64_t i2 = r / G.n[1];
+    return G.origin + i0 + G.P0 * i1 + G.P01 * i2;
+}
+
+// (A x)_p = a_P x_p - sum_q c_pq x_q, evaluated s = a_P x_p; s = fma(-c, x_q, s) in axis
+// order (-, +) (DESIGN R-7, same as the oracle).  Ghost neighbours read 0.
+__device__ inline double apply_A_at(const Geo &G, const double *const F[3], const double *x, int64_t idx,
+                                    const int64_t g[3]) {
+    double s = a_p(G, F, g) * x[idx];
+    const int64_t st[3] = {1, G.P0, G.P01};
+    for (int a = 0; a < G.dim; ++a) {
+        s = fma(-face(G, F, g, a, -1), x[idx - st[a]], s);
+        s = fma(-face(G, F, g, a, +1), x[idx + st[a]], s);
+    }
+    return s;
+}
+
+__device__ inline void local_to_global(const Geo &G, int64_t t, int64_t g[3]) {
+    g[0] = t % G.n[0];
+    int64_t r = t / G.n[0];
+    g[1] = r % G.n[1];
+    g[2] = r / G.n[1];
+    for (int a = 0; a < 3; ++a) g[a] += G.off[a];
+}
+
+// q = A p ; partial[blk] = sum p.q
+__global__ void k_spmv_dot(Geo G, const double *F0, const double *F1, const double *F2, const double *p, double *q,
+                           DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    const double *F[3] = {F0, F1, F2};
+    int64_t N = G.n[0] * G.n[1] * G.n[2];
+    DD acc = {0.0, 0.0};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t g[3];
+        local_to_global(G, t, g);
+        int64_t i = interior_index(G, t);
+        double v = apply_A_at(G, F, p, i, g);
+        q[i] = v;
+        dd_add_prod(acc, p[i], v);
+    }
+    DD s = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// r = b - A x ; partial[2*blk] = sum r.r, partial[2*blk+1] = sum b.b
+__global__ void k_residual(Geo G, const double *F0, const double *F1, const double *F2, const double *x,
+                           const double *b, double *r, DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    const double *F[3] = {F0, F1, F2};
+    int64_t N = G.n[0] * G.n[1] * G.n[2];
+    DD rr = {0.0, 0.0}, bb = {0.0, 0.0};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t g[3];
+        local_to_global(G, t, g);
+        int64_t i = interior_index(G, t);
+        double v = b[i] - apply_A_at(G, F, x, i, g);
+        if (r) r[i] = v;
+        dd_add_prod(rr, v, v);
+        dd_add_prod(bb, b[i], b[i]);
+    }
+    DD s1 = block_sum_dd(rr, sh);
+    DD s2 = block_sum_dd(bb, sh);
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = s1;
+        partial[2 * blockIdx.x + 1] = s2;
+    }
+}
+
+// generic dot: partial[blk] = sum a.b
+__global__ void k_dot(Geo G, const double *a, const double *b, DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    int64_t N = G.n[0] * G.n[1] * G.n[2];
+    DD acc = {0.0, 0.0};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = interior_index(G, t);
+        dd_add_prod(acc, a[i], b[i]);
+    }
+    DD s = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// PCG scalars kept on the device
+struct CgScalars {
+    double rz, pq, alpha, beta, rr, bb, rz_new;
+};
+
+// sum `nparts` partials (stride `stride`, offset `off`) in fixed order into *dst = hi + lo
+__global__ void k_finish_sum(const DD *partial, int nparts, int stride, int off, double *dst) {
+    __shared__ DD sh[RED_THREADS / 32];
+    DD acc = {0.0, 0.0};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc = dd_merge(acc, partial[(int64_t)i * stride + off]);
+    DD s = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) *dst = s.hi + s.lo;
+}
+
+// alpha = rz / pq
+__global__ void k_cg_alpha(CgScalars *c) { c->alpha = c->rz / c->pq; }
+// beta = rz_new / rz ; rz = rz_new
+__global__ void k_cg_beta(CgScalars *c) {
+    c->beta = c->rz_new / c->rz;
+    c->rz = c->rz_new;
+}
+
+// x = fma(alpha, p, x) ; r = fma(-alpha, q, r) ; partial = sum r.r
+__global__ void k_axpy2_dot(Geo G, const CgScalars *c, double *x, double *r, const double *p, const double *q,
+                            DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    int64_t N = G.n[0] * G.n[1] * G.n[2];
+    double al = c->alpha;
+    DD acc = {0.0, 0.0};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = interior_index(G, t);
+        x[i] = fma(al, p[i], x[i]);
+        double rv = fma(-al, q[i], r[i]);
+        r[i] = rv;
+        dd_add_prod(acc, rv, rv);
+    }
+    DD s = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// p = fma(beta, p, z)   (first: p = z)
+__global__ void k_pupdate(Geo G, const CgScalars *c, int first, const double *z, double *p) {
+    int64_t N = G.n[0] * G.n[1] * G.n[2];
+    double be = first ? 0.0 : c->beta;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = interior_index(G, t);
+        p[i] = first ? z[i] : fma(be, p[i], z[i]);
+    }
+}
+
+// faces from node diffusivities (DESIGN R-12):
+//   F[a] at node g = scale_a * ((2 k(g-e_a)) k(g)) / (k(g-e_a) + k(g))
+// k layout: per used axis kd[a] nodes, local coordinate c stored at c + kor[a]
+// (kor = 1 with a one-node ring, 2 on the slab axis with two extra layers).
+struct KLayout {
+    int64_t kd[3];
+    int64_t kor[3];
+    double scale[3];
+};
+
+__global__ void k_faces_from_k(Geo G, KLayout K, const double *kk, double *F0, double *F1, double *F2) {
+    int64_t w[3] = {1, 1, 1};
+    for (int a = 0; a < G.dim; ++a) w[a] = G.n[a] + 4;
+    int64_t N = w[0] * w[1] * w[2];
+    double *F[3] = {F0, F1, F2};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t l[3] = {t % w[0], (t / w[0]) % w[1], t / (w[0] * w[1])};
+        for (int a = 0; a < G.dim; ++a) l[a] -= 2;           // local coordinates in [-2, n+2)
+        int64_t g[3] = {l[0] + G.off[0], l[1] + G.off[1], l[2] + G.off[2]};
+        int64_t pi = gidx(G, g[0], g[1], g[2]);
+        for (int a = 0; a < G.dim; ++a) {
+            bool ok = (g[a] >= 0 && g[a] <= G.ng[a]);       // faces 0..ng along a
+            for (int b = 0; b < G.dim; ++b)
+                if (b != a && (g[b] < -1 || g[b] > G.ng[b])) ok = false;
+            int64_t cq[3], cp[3];
+            for (int b = 0; b < 3; ++b) {
+                cq[b] = (b < G.dim) ? l[b] + K.kor[b] : 0;
+                cp[b] = cq[b] - (b == a ? 1 : 0);
+                if (b < G.dim && (cq[b] < 0 || cp[b] < 0 || cq[b] >= K.kd[b] || cp[b] >= K.kd[b])) ok = false;
+            }
+            double v = 0.0;
+            if (ok) {
+                double kp = kk[cp[0] + K.kd[0] * (cp[1] + K.kd[1] * cp[2])];
+                double kq = kk[cq[0] + K.kd[0] * (cq[1] + K.kd[1] * cq[2])];
+                v = K.scale[a] * ((2.0 * kp) * kq / (kp + kq));
+            }
+            F[a][pi] = v;
+        }
+    }
+}
+
+}  // namespace sw

@@ -1,0 +1,607 @@
+// sweep.cu -- host runtime of the C ABI (include/sweep.h): grid/slab geometry, device
+// memory, kernel dispatch for the decomposed SOR sweep, D-ILU(0)/SSOR application and
+// the PCG driver.  Kernels: generic.cuh (all dims/modes), sweep2d.cuh (fast 2D SOR),
+// blas.cuh (PCG vector work).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sweep.h"
+#include "blas.cuh"
+#include "generic.cuh"
+#include "sweep2d.cuh"
+
+using namespace sw;
+
+static thread_local std::string g_err;
+
+static sw_status fail(sw_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(SW_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));           \
+    } while (0)
+
+struct sw_grid {
+    int dim = 0;
+    int64_t ng[3] = {1, 1, 1};
+    sw_coef kind = SW_COEF_POISSON;
+    double beta = 0.0;
+    int dev = 0;
+    bool decomposed = false;
+    int tile[3] = {1, 1, 1};
+    int rank = 0, nranks = 1;
+    Geo G{};
+    int64_t pad[3] = {1, 1, 1};
+    int64_t nelem = 0;
+    double *X[2] = {nullptr, nullptr};
+    int cur = 0;
+    double *B = nullptr;
+    double *F[3] = {nullptr, nullptr, nullptr};
+    double *invD = nullptr, *R = nullptr, *Z = nullptr, *Pv = nullptr, *Q = nullptr, *Y = nullptr;
+    DD *partial = nullptr;
+    CgScalars *cg = nullptr;
+    int *flag = nullptr;
+    bool factored = false;
+    int64_t factor_phase = 0;
+    int64_t launches = 0;
+    int fast2d = 1;
+    Maps2d maps;
+};
+
+extern "C" const char *sw_last_error(void) { return g_err.c_str(); }
+
+extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, double beta, int cuda_device,
+                                    sw_grid **out) {
+    if (!out) return fail(SW_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (dim < 1 || dim > 3) return fail(SW_EINVAL, "dim must be 1, 2 or 3");
+    if (!n) return fail(SW_EINVAL, "n is NULL");
+    for (int a = 0; a < dim; ++a)
+        if (n[a] < 1) return fail(SW_EINVAL, "n[a] must be >= 1");
+    if (!(beta >= 0.0)) return fail(SW_EINVAL, "beta must be >= 0");
+    if (kind != SW_COEF_POISSON && kind != SW_COEF_FACES) return fail(SW_EINVAL, "bad coefficient kind");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (cuda_device < 0 || cuda_device >= ndev) return fail(SW_EINVAL, "bad cuda_device");
+    CK(cudaSetDevice(cuda_device));
+    sw_grid *g = new sw_grid();
+    g->dim = dim;
+    for (int a = 0; a < dim; ++a) g->ng[a] = n[a];
+    g->kind = kind;
+    g->beta = beta;
+    g->dev = cuda_device;
+    const char *env = getenv("SW_DISABLE_FAST2D");
+    if (env && env[0] == '1') g->fast2d = 0;
+    *out = g;
+    return SW_OK;
+}
+
+static void free_all(sw_grid *g) {
+    double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
+                       &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y};
+    for (double **p : ptrs)
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    if (g->partial) cudaFree(g->partial);
+    if (g->cg) cudaFree(g->cg);
+    if (g->flag) cudaFree(g->flag);
+    g->partial = nullptr;
+    g->cg = nullptr;
+    g->flag = nullptr;
+}
+
+static sw_status alloc_arr(sw_grid *g, double **p) {
+    if (*p) return SW_OK;
+    cudaError_t e = cudaMalloc(p, sizeof(double) * (size_t)g->nelem);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(SW_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    CK(cudaMemset(*p, 0, sizeof(double) * (size_t)g->nelem));
+    return SW_OK;
+}
+
+extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int nranks) {
+    if (!g || !tile) return fail(SW_EINVAL, "NULL argument");
+    if (g->decomposed) return fail(SW_ESTATE, "grid already decomposed");
+    const int d = g->dim, sa = d - 1;
+    for (int a = 0; a < d; ++a) {
+        if (tile[a] < 1 || g->ng[a] % tile[a] != 0)
+            return fail(SW_EINVAL, "tile must be >= 1 and divide n along every axis");
+    }
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SW_EINVAL, "bad rank / nranks");
+    int64_t rows = g->ng[sa] / tile[sa];
+    if (rows % nranks != 0) return fail(SW_EINVAL, "nranks must divide the number of tile rows of the slab axis");
+    CK(cudaSetDevice(g->dev));
+    Geo &G = g->G;
+    memset(&G, 0, sizeof(G));
+    G.dim = d;
+    G.poisson = (g->kind == SW_COEF_POISSON);
+    G.beta = g->beta;
+    for (int a = 0; a < 3; ++a) {
+        G.n[a] = G.ng[a] = 1;
+        G.T[a] = 1;
+        G.nt[a] = 1;
+        G.ntg[a] = 1;
+        G.off[a] = 0;
+        G.toff[a] = 0;
+        g->pad[a] = 1;
+        g->tile[a] = 1;
+    }
+    for (int a = 0; a < d; ++a) {
+        g->tile[a] = tile[a];
+        G.T[a] = tile[a];
+        G.ng[a] = g->ng[a];
+        G.ntg[a] = g->ng[a] / tile[a];
+        G.n[a] = g->ng[a];
+        G.nt[a] = (int)G.ntg[a];
+    }
+    int64_t my_rows = rows / nranks;
+    G.n[sa] = my_rows * tile[sa];
+    G.nt[sa] = (int)my_rows;
+    G.toff[sa] = my_rows * rank;
+    G.off[sa] = G.toff[sa] * tile[sa];
+    for (int a = 0; a < d; ++a) g->pad[a] = G.n[a] + 4;
+    g->pad[0] = (g->pad[0] + 7) / 8 * 8;
+    G.P0 = g->pad[0];
+    G.P01 = g->pad[0] * g->pad[1];
+    G.origin = 2 + (d > 1 ? 2 * G.P0 : 0) + (d > 2 ? 2 * G.P01 : 0);
+    g->nelem = g->pad[0] * g->pad[1] * g->pad[2];
+    g->rank = rank;
+    g->nranks = nranks;
+    sw_status st;
+    if ((st = alloc_arr(g, &g->X[0])) != SW_OK || (st = alloc_arr(g, &g->X[1])) != SW_OK ||
+        (st = alloc_arr(g, &g->B)) != SW_OK) {
+        free_all(g);
+        return st;
+    }
+    if (!G.poisson)
+        for (int a = 0; a < d; ++a)
+            if ((st = alloc_arr(g, &g->F[a])) != SW_OK) { free_all(g); return st; }
+    if (cudaMalloc(&g->partial, sizeof(DD) * 2 * RED_BLOCKS) != cudaSuccess ||
+        cudaMalloc(&g->cg, sizeof(CgScalars)) != cudaSuccess || cudaMalloc(&g->flag, sizeof(int)) != cudaSuccess) {
+        free_all(g);
+        return fail(SW_ENOMEM, "cudaMalloc of scratch failed");
+    }
+    CK(cudaMemset(g->flag, 0, sizeof(int)));
+    CK(cudaMemset(g->cg, 0, sizeof(CgScalars)));
+    if (d == 2 && sweep2d_supported(G))
+        make_maps2d(g->maps, g->X[0], g->X[1], g->B, g->F[0], g->F[1], g->pad[0], g->pad[1]);
+    g->decomposed = true;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_local_shape(const sw_grid *g, int64_t n_local[3], int64_t *slab_offset, int64_t pad[3],
+                                    int64_t *origin) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    for (int a = 0; a < 3; ++a) {
+        if (n_local) n_local[a] = g->G.n[a];
+        if (pad) pad[a] = g->pad[a];
+    }
+    if (slab_offset) *slab_offset = g->G.off[g->dim - 1];
+    if (origin) *origin = g->G.origin;
+    return SW_OK;
+}
+
+static double *vec_ptr(sw_grid *g, sw_vector which) {
+    switch (which) {
+        case SW_X: return g->X[g->cur];
+        case SW_B: return g->B;
+        case SW_R: return g->R;
+        case SW_Z: return g->Z;
+        case SW_P: return g->Pv;
+        case SW_Q: return g->Q;
+        case SW_INVD: return g->invD;
+        case SW_Y: return g->Y;
+    }
+    return nullptr;
+}
+
+static sw_status ensure_work(sw_grid *g) {
+    sw_status st;
+    double **ps[] = {&g->invD, &g->R, &g->Z, &g->Pv, &g->Q, &g->Y};
+    for (double **p : ps)
+        if ((st = alloc_arr(g, p)) != SW_OK) return st;
+    return SW_OK;
+}
+
+static sw_status copy_interior(sw_grid *g, double *dev, const double *src_host_or_dev, double *dst, bool to_dev,
+                               cudaStream_t s) {
+    cudaMemcpy3DParms p = {};
+    const Geo &G = g->G;
+    cudaPitchedPtr lin = make_cudaPitchedPtr(to_dev ? (void *)src_host_or_dev : (void *)dst,
+                                             sizeof(double) * G.n[0], G.n[0], G.n[1]);
+    cudaPitchedPtr padp = make_cudaPitchedPtr(dev, sizeof(double) * g->pad[0], g->pad[0], g->pad[1]);
+    cudaPos pos = make_cudaPos(sizeof(double) * 2, g->dim > 1 ? 2 : 0, g->dim > 2 ? 2 : 0);
+    if (to_dev) {
+        p.srcPtr = lin;
+        p.dstPtr = padp;
+        p.dstPos = pos;
+    } else {
+        p.srcPtr = padp;
+        p.srcPos = pos;
+        p.dstPtr = lin;
+    }
+    p.extent = make_cudaExtent(sizeof(double) * G.n[0], G.n[1], G.n[2]);
+    p.kind = cudaMemcpyDefault;
+    CK(cudaMemcpy3DAsync(&p, s));
+    return SW_OK;
+}
+
+extern "C" sw_status sw_set_vector(sw_grid *g, sw_vector which, const double *src, int src_is_device,
+                                   sw_stream_t s) {
+    (void)src_is_device;
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!src) return fail(SW_EINVAL, "src is NULL");
+    if (which != SW_X && which != SW_B) {
+        sw_status st = ensure_work(g);
+        if (st != SW_OK) return st;
+    }
+    double *d = vec_ptr(g, which);
+    if (!d) return fail(SW_EINVAL, "bad vector id");
+    if (which == SW_INVD) g->factored = true;
+    return copy_interior(g, d, src, nullptr, true, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_get_vector(const sw_grid *gc, sw_vector which, double *dst, int dst_is_device,
+                                   sw_stream_t s) {
+    (void)dst_is_device;
+    sw_grid *g = const_cast<sw_grid *>(gc);
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!dst) return fail(SW_EINVAL, "dst is NULL");
+    double *d = vec_ptr(g, which);
+    if (!d) return fail(SW_ESTATE, "vector not allocated");
+    return copy_interior(g, d, nullptr, dst, false, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_ghost_view(sw_grid *g, sw_vector which, double **dev_ptr) {
+    if (!g || !g->decomposed || !dev_ptr) return fail(SW_ESTATE, "grid not decomposed / NULL");
+    if (which != SW_X && which != SW_B) {
+        sw_status st = ensure_work(g);
+        if (st != SW_OK) return st;
+    }
+    *dev_ptr = vec_ptr(g, which);
+    return *dev_ptr ? SW_OK : fail(SW_EINVAL, "bad vector id");
+}
+
+extern "C" sw_status sw_set_faces(sw_grid *g, const double *const face_host[3], sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->kind != SW_COEF_FACES) return fail(SW_ESTATE, "grid was created with Poisson coefficients");
+    const Geo &G = g->G;
+    const int d = g->dim, sa = d - 1;
+    std::vector<double> hb((size_t)g->nelem);
+    for (int a = 0; a < d; ++a) {
+        if (!face_host[a]) return fail(SW_EINVAL, "face array is NULL");
+        int64_t m[3] = {1, 1, 1};
+        for (int b = 0; b < d; ++b) m[b] = G.n[b] + (b == a ? 1 : 0) + (b == sa ? 4 : 0);
+        std::fill(hb.begin(), hb.end(), 0.0);
+        for (int64_t k = 0; k < m[2]; ++k)
+            for (int64_t j = 0; j < m[1]; ++j)
+                for (int64_t i = 0; i < m[0]; ++i) {
+                    int64_t c[3] = {i, j, k};
+                    c[sa] -= 2;                       // slab axis: entry 0 = coordinate -2
+                    int64_t gg[3] = {c[0] + G.off[0], c[1] + G.off[1], c[2] + G.off[2]};
+                    double v = face_host[a][i + m[0] * (j + m[1] * k)];
+                    bool phys = true;                 // face between g - e_a and g inside the domain's ring
+                    for (int b = 0; b < d; ++b) {
+                        if (b == a && (gg[b] < 0 || gg[b] > G.ng[b])) phys = false;
+                        if (b != a && (gg[b] < 0 || gg[b] >= G.ng[b])) phys = false;
+                    }
+                    if (!phys) continue;
+                    if (!(v > 0.0)) return fail(SW_EINVAL, "face coefficients must be > 0");
+                    hb[(size_t)(G.origin + c[0] + G.P0 * c[1] + G.P01 * c[2])] = v;
+                }
+        CK(cudaMemcpyAsync(g->F[a], hb.data(), sizeof(double) * (size_t)g->nelem, cudaMemcpyHostToDevice,
+                           (cudaStream_t)s));
+        CK(cudaStreamSynchronize((cudaStream_t)s));
+    }
+    g->factored = false;
+    return SW_OK;
+}
+
+static int grid_blocks(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b > RED_BLOCKS) b = RED_BLOCKS;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+extern "C" sw_status sw_set_coefficients_k(sw_grid *g, const double *k_host, const double scale[3], sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->kind != SW_COEF_FACES) return fail(SW_ESTATE, "grid was created with Poisson coefficients");
+    if (!k_host || !scale) return fail(SW_EINVAL, "NULL argument");
+    const Geo &G = g->G;
+    const int d = g->dim, sa = d - 1;
+    KLayout K{};
+    int64_t cnt = 1;
+    for (int a = 0; a < 3; ++a) {
+        K.kd[a] = 1;
+        K.kor[a] = 0;
+        K.scale[a] = (a < d) ? scale[a] : 1.0;
+        if (a < d) {
+            K.kd[a] = G.n[a] + (a == sa ? 4 : 2);
+            K.kor[a] = (a == sa) ? 2 : 1;
+            if (!(scale[a] > 0.0)) return fail(SW_EINVAL, "scale must be > 0");
+        }
+        cnt *= K.kd[a];
+    }
+    double *kd = nullptr;
+    CK(cudaMalloc(&kd, sizeof(double) * (size_t)cnt));
+    cudaError_t e = cudaMemcpyAsync(kd, k_host, sizeof(double) * (size_t)cnt, cudaMemcpyDefault, (cudaStream_t)s);
+    if (e == cudaSuccess) {
+        int64_t npos = 1;
+        for (int a = 0; a < d; ++a) npos *= G.n[a] + 4;
+        k_faces_from_k<<<grid_blocks(npos, 256), 256, 0, (cudaStream_t)s>>>(G, K, kd, g->F[0], g->F[1], g->F[2]);
+        g->launches++;
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)s);
+    cudaFree(kd);
+    if (e != cudaSuccess) return fail(SW_ECUDA, std::string("faces_from_k: ") + cudaGetErrorString(e));
+    g->factored = false;
+    return SW_OK;
+}
+
+static sw_status launch_generic(sw_grid *g, const KParams &P, cudaStream_t s) {
+    int64_t tiles = (int64_t)g->G.nt[0] * g->G.nt[1] * g->G.nt[2];
+    switch (g->dim) {
+        case 1: k_generic<1><<<(unsigned)tiles, 32, 0, s>>>(P); break;
+        case 2: k_generic<2><<<(unsigned)tiles, 96, 0, s>>>(P); break;
+        default: k_generic<3><<<(unsigned)tiles, 128, 0, s>>>(P); break;
+    }
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+static KParams base_params(sw_grid *g) {
+    KParams P;
+    memset(&P, 0, sizeof(P));
+    P.G = g->G;
+    for (int a = 0; a < 3; ++a) P.F[a] = g->F[a];
+    P.flag = g->flag;
+    P.coef = 1.0;
+    return P;
+}
+
+static sw_status check_omega(const double *omega, int n_omega, int dim, double w8[8]) {
+    if (!omega || (n_omega != 1 && n_omega != (1 << dim))) return fail(SW_EINVAL, "omega must have 1 or 2^dim values");
+    for (int i = 0; i < 8; ++i) {
+        double w = omega[n_omega == 1 ? 0 : (i < n_omega ? i : 0)];
+        if (!(w > 0.0 && w < 2.0)) return fail(SW_EINVAL, "omega must lie in (0, 2)");
+        w8[i] = w;
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, int nsweeps, int64_t *phase_inout,
+                                  sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!phase_inout || nsweeps < 0) return fail(SW_EINVAL, "bad phase / nsweeps");
+    if (g->nranks > 1 && nsweeps > 1) return fail(SW_EINVAL, "multi-rank: one sweep per call (exchange ghosts between)");
+    double w8[8];
+    sw_status st = check_omega(omega, n_omega, g->dim, w8);
+    if (st != SW_OK) return st;
+    CK(cudaSetDevice(g->dev));
+    cudaStream_t cs = (cudaStream_t)s;
+    for (int it = 0; it < nsweeps; ++it) {
+        int64_t k = *phase_inout;
+        int base = base_bits(g->dim, k);
+        const double *xo = g->X[g->cur];
+        double *xn = g->X[1 - g->cur];
+        if (g->dim == 2 && g->fast2d && g->maps.ok) {
+            cudaError_t e = launch_sweep2d(g->maps, g->cur, g->G, base, w8, g->B, xn, g->flag, !g->G.poisson, cs);
+            g->launches++;
+            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2d launch: ") + cudaGetErrorString(e));
+        } else {
+            KParams P = base_params(g);
+            P.mode = M_FWD;
+            P.rhs = R_SOR;
+            P.alpha_mode = A_OMEGA_AP;
+            P.base = base;
+            for (int i = 0; i < 8; ++i) P.omega[i] = w8[i];
+            P.xold = xo;
+            P.b = g->B;
+            P.out = xn;
+            st = launch_generic(g, P, cs);
+        }
+        if (st != SW_OK) return st;
+        CK(cudaGetLastError());
+        g->cur = 1 - g->cur;
+        *phase_inout = k + 1;
+    }
+    return SW_OK;
+}
+
+static sw_status finish(sw_grid *g, int nparts, int stride, int off, double *dst, cudaStream_t s) {
+    k_finish_sum<<<1, RED_THREADS, 0, s>>>(g->partial, nparts, stride, off, dst);
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+extern "C" sw_status sw_check_status(sw_grid *g, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    CK(cudaStreamSynchronize((cudaStream_t)s));
+    int f = 0;
+    CK(cudaMemcpy(&f, g->flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (f) {
+        CK(cudaMemset(g->flag, 0, sizeof(int)));
+        return fail(SW_ESINGULAR, "singular coupled system or non-positive ILU pivot");
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_residual_norm(sw_grid *g, double *rel_out, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!rel_out) return fail(SW_EINVAL, "rel_out is NULL");
+    if (g->nranks > 1) return fail(SW_EINVAL, "sw_residual_norm is single-rank");
+    cudaStream_t cs = (cudaStream_t)s;
+    int64_t N = g->G.n[0] * g->G.n[1] * g->G.n[2];
+    int nb = grid_blocks(N, RED_THREADS);
+    k_residual<<<nb, RED_THREADS, 0, cs>>>(g->G, g->F[0], g->F[1], g->F[2], g->X[g->cur], g->B, nullptr, g->partial);
+    g->launches++;
+    CK(cudaGetLastError());
+    sw_status st;
+    if ((st = finish(g, nb, 2, 0, &g->cg->rr, cs)) != SW_OK) return st;
+    if ((st = finish(g, nb, 2, 1, &g->cg->bb, cs)) != SW_OK) return st;
+    CgScalars h;
+    CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamSynchronize(cs));
+    *rel_out = h.bb > 0 ? sqrt(h.rr) / sqrt(h.bb) : sqrt(h.rr);
+    return sw_check_status(g, s);
+}
+
+extern "C" sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    sw_status st = ensure_work(g);
+    if (st != SW_OK) return st;
+    KParams P = base_params(g);
+    P.mode = M_FACTOR;
+    P.base = base_bits(g->dim, phase);
+    P.out = g->invD;
+    if ((st = launch_generic(g, P, (cudaStream_t)s)) != SW_OK) return st;
+    g->factored = true;
+    g->factor_phase = phase;
+    return SW_OK;
+}
+
+// shared by ILU(0) and SSOR application
+static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
+                           cudaStream_t s) {
+    if (g->nranks > 1) return fail(SW_EINVAL, "preconditioner application is single-rank in this build");
+    sw_status st = ensure_work(g);
+    if (st != SW_OK) return st;
+    if (ilu && !g->factored) return fail(SW_ESTATE, "sw_ilu0_factor must precede sw_ilu_apply");
+    if (!ilu && !(omega > 0.0 && omega < 2.0)) return fail(SW_EINVAL, "omega must lie in (0,2)");
+    if (!r || !z || z == g->Y || r == z) return fail(SW_EINVAL, "bad r/z pointers");
+    KParams P = base_params(g);
+    P.alpha_mode = ilu ? A_INVD : A_OMEGA_AP;
+    P.invD = g->invD;
+    for (int i = 0; i < 8; ++i) P.omega[i] = omega;
+    int base = base_bits(g->dim, g->factor_phase);
+    // forward: (D~ + L) y = r   (row-normalised: r0 = alpha r)
+    P.mode = M_FWD;
+    P.rhs = R_SCALE;
+    P.base = base;
+    P.src = r;
+    P.out = g->Y;
+    if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+    P.src = g->Y;
+    P.out = z;
+    P.rhs = R_COEF;
+    P.coef = ilu ? 1.0 : 2.0 - omega;
+    if (pairing == SW_PAIR_PAPER) {
+        P.mode = M_FWD;
+        P.base = base ^ ((1 << g->dim) - 1);
+        return launch_generic(g, P, s);
+    }
+    // SYMMETRIC: (D~ + L^T) z = D~ y, non-coupled nodes first, then coupled sets by degree
+    P.mode = M_T1;
+    if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+    for (int j = 1; j <= g->dim; ++j) {
+        P.mode = M_T2;
+        P.j = j;
+        if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_ilu_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_pairing pairing, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    return tri_apply(g, true, 1.0, r_dev, z_dev, pairing, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev, double *z_dev, sw_pairing pairing,
+                                   sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    return tri_apply(g, false, omega, r_dev, z_dev, pairing, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pairing pairing, double rtol, int maxit,
+                                  int *iters_out, double *relres_out, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->nranks > 1) return fail(SW_EINVAL, "sw_pcg_solve is single-rank in this build");
+    if (!iters_out || !relres_out || maxit < 1 || !(rtol > 0)) return fail(SW_EINVAL, "bad arguments");
+    sw_status st = ensure_work(g);
+    if (st != SW_OK) return st;
+    cudaStream_t cs = (cudaStream_t)s;
+    const Geo &G = g->G;
+    int64_t N = G.n[0] * G.n[1] * G.n[2];
+    int nb = grid_blocks(N, RED_THREADS);
+    double *x = g->X[g->cur];
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)g->nelem, cs));
+    CK(cudaMemcpyAsync(g->R, g->B, sizeof(double) * (size_t)g->nelem, cudaMemcpyDeviceToDevice, cs));
+    if (pc == SW_PC_ILU0) {
+        if ((st = sw_ilu0_factor(g, 0, s)) != SW_OK) return st;
+    } else {
+        g->factor_phase = 0;
+    }
+    double *z = (pc == SW_PC_NONE) ? g->R : g->Z;
+    auto apply_pc = [&]() -> sw_status {
+        if (pc == SW_PC_NONE) return SW_OK;
+        return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, cs);
+    };
+    // b.b
+    k_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->B, g->B, g->partial);
+    g->launches++;
+    if ((st = finish(g, nb, 1, 0, &g->cg->bb, cs)) != SW_OK) return st;
+    if ((st = apply_pc()) != SW_OK) return st;
+    k_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->R, z, g->partial);
+    g->launches++;
+    if ((st = finish(g, nb, 1, 0, &g->cg->rz, cs)) != SW_OK) return st;
+    k_pupdate<<<nb, RED_THREADS, 0, cs>>>(G, g->cg, 1, z, g->Pv);
+    g->launches++;
+    CgScalars h;
+    CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamSynchronize(cs));
+    double bnorm = sqrt(h.bb);
+    *iters_out = 0;
+    *relres_out = 1.0;
+    if (bnorm == 0.0) { *relres_out = 0.0; return SW_OK; }
+    for (int it = 1; it <= maxit; ++it) {
+        k_spmv_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->F[0], g->F[1], g->F[2], g->Pv, g->Q, g->partial);
+        g->launches++;
+        if ((st = finish(g, nb, 1, 0, &g->cg->pq, cs)) != SW_OK) return st;
+        k_cg_alpha<<<1, 1, 0, cs>>>(g->cg);
+        g->launches++;
+        k_axpy2_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->cg, x, g->R, g->Pv, g->Q, g->partial);
+        g->launches++;
+        if ((st = finish(g, nb, 1, 0, &g->cg->rr, cs)) != SW_OK) return st;
+        CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
+        CK(cudaStreamSynchronize(cs));
+        *iters_out = it;
+        *relres_out = sqrt(h.rr) / bnorm;
+        if (*relres_out < rtol) return sw_check_status(g, s);
+        if (!(h.rr == h.rr)) return fail(SW_ENOCONV, "PCG produced NaN");
+        if ((st = apply_pc()) != SW_OK) return st;
+        k_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->R, z, g->partial);
+        g->launches++;
+        if ((st = finish(g, nb, 1, 0, &g->cg->rz_new, cs)) != SW_OK) return st;
+        k_cg_beta<<<1, 1, 0, cs>>>(g->cg);
+        g->launches++;
+        k_pupdate<<<nb, RED_THREADS, 0, cs>>>(G, g->cg, 0, z, g->Pv);
+        g->launches++;
+        CK(cudaGetLastError());
+    }
+    st = sw_check_status(g, s);
+    if (st != SW_OK) return st;
+    return fail(SW_ENOCONV, "PCG reached maxit");
+}
+
+extern "C" int64_t sw_launch_count(const sw_grid *g) { return g ? g->launches : 0; }
+
+extern "C" sw_status sw_destroy(sw_grid *g) {
+    if (!g) return SW_OK;
+    cudaSetDevice(g->dev);
+    free_all(g);
+    delete g;
+    return SW_OK;
+}
