@@ -73,12 +73,14 @@ static double face_between(const or_grid *g, const int64_t c[3], int a, int sd) 
 }
 
 /* a_P = a^W + a^E + a^S + a^N (+ a^B + a^F) + beta, PAPER:429-430 (2D), 192 (1D);
- * summed in the fixed order x-, x+, y-, y+, z-, z+, then beta (reading R-7). */
+ * summed per axis pair first, a_P = ((F_x- + F_x+) + (F_y- + F_y+)) + (F_z- + F_z+), then
+ * beta (reading R-7).  Each pair sum is commutative, so the value does not depend on the
+ * direction a box is swept in. */
 static double a_p(const or_grid *g, const int64_t c[3]) {
     double s = 0.0;
     for (int a = 0; a < g->dim; ++a) {
-        s += face_between(g, c, a, -1);
-        s += face_between(g, c, a, +1);
+        double pair = face_between(g, c, a, -1) + face_between(g, c, a, +1);
+        s = (a == 0) ? pair : s + pair;
     }
     return s + g->beta;
 }

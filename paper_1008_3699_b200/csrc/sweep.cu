@@ -12,6 +12,7 @@
 #include "blas.cuh"
 #include "generic.cuh"
 #include "sweep2d.cuh"
+#include "sweep2p.cuh"
 
 using namespace sw;
 
@@ -396,7 +397,11 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
         int base = base_bits(g->dim, k);
         const double *xo = g->X[g->cur];
         double *xn = g->X[1 - g->cur];
-        if (g->dim == 2 && g->fast2d && g->maps.ok) {
+        if (g->dim == 2 && g->fast2d && g->maps.ok && g->G.poisson) {
+            cudaError_t e = launch_sweep2p(g->maps.x[g->cur], g->G, base, w8, g->B, xn, g->flag, cs);
+            g->launches++;
+            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2p launch: ") + cudaGetErrorString(e));
+        } else if (g->dim == 2 && g->fast2d && g->maps.ok) {
             cudaError_t e = launch_sweep2d(g->maps, g->cur, g->G, base, w8, g->B, g->F, xn, g->flag, !g->G.poisson, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2d launch: ") + cudaGetErrorString(e));

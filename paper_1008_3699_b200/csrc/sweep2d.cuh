@@ -59,12 +59,9 @@ __device__ __forceinline__ double fyb(const double *fy, int a, int wc) {
 // a_P of window node (wr, wc): x-, x+, y-, y+, then beta (DESIGN R-7)
 template <bool FACES>
 __device__ __forceinline__ double ap_w(const double *fx, const double *fy, int wr, int wc, double beta) {
-    double s = 0.0;
-    s += fxb<FACES>(fx, wr, wc - 1);
-    s += fxb<FACES>(fx, wr, wc);
-    s += fyb<FACES>(fy, wr - 1, wc);
-    s += fyb<FACES>(fy, wr, wc);
-    return s + beta;
+    const double sx = fxb<FACES>(fx, wr, wc - 1) + fxb<FACES>(fx, wr, wc);
+    const double sy = fyb<FACES>(fy, wr - 1, wc) + fyb<FACES>(fy, wr, wc);
+    return (sx + sy) + beta;
 }
 
 // Gaussian elimination without pivoting, reciprocal pivots, fused updates: identical to
@@ -156,11 +153,7 @@ __device__ __forceinline__ void sweep2d_tile(const CUtensorMap *tmx, const Sweep
             a2 = __ldg(Fy + g);
             a3 = __ldg(Fy + g + P0);
         }
-        double s = 0.0;                       // a_P: x-, x+, y-, y+, then beta
-        s += a0;
-        s += a1;
-        s += a2;
-        s += a3;
+        const double s = (a0 + a1) + (a2 + a3);     // a_P (R-7), beta added below
         const double al = w / (s + beta);
         const double cex = ex > 0 ? a1 : a0, cey = ey > 0 ? a3 : a2;
         const double cix = ex > 0 ? a0 : a1, ciy = ey > 0 ? a2 : a3;
@@ -295,9 +288,7 @@ __device__ __forceinline__ void sweep2d_tile(const CUtensorMap *tmx, const Sweep
                     const double xm0 = fxv.x, xp0 = fxv.y, xm1 = fxv.y, xp1 = fx2;
                     const double ym0 = SY ? fyn.x : fyc.x, yp0 = SY ? fyc.x : fyn.x;
                     const double ym1 = SY ? fyn.y : fyc.y, yp1 = SY ? fyc.y : fyn.y;
-                    double s0 = 0.0, s1 = 0.0;
-                    s0 += xm0; s0 += xp0; s0 += ym0; s0 += yp0;
-                    s1 += xm1; s1 += xp1; s1 += ym1; s1 += yp1;
+                    const double s0 = (xm0 + xp0) + (ym0 + yp0), s1 = (xm1 + xp1) + (ym1 + yp1);
                     const double al0 = w_own / (s0 + beta), al1 = w_own / (s1 + beta);
                     double ea = fma(SX ? xm0 : xp0, e0, bb.x);
                     ea = fma(SY ? ym0 : yp0, nb.x, ea);

@@ -22,6 +22,10 @@ CASES = [
     # (n, tile, variable coefficients?, beta, omega)
     ((256, 256), (64, 64), False, 0.0, [1.975848]),                  # config 2 shape
     ((256, 256), (64, 64), True, 0.0, [1.0]),                       # config 3 law, small
+    ((320, 192), (64, 64), False, 0.1, [0.7, 1.3, 1.1, 1.6]),       # Poisson kernel, per-direction omega, beta
+    ((64, 64), (64, 64), False, 0.0, [1.9]),                        # Poisson kernel, one box
+    ((128, 64), (64, 64), False, 0.0, [1.99]),                      # Poisson kernel, one tile row
+    ((64, 192), (64, 64), False, 0.3, [0.5]),                       # Poisson kernel, one tile column
     ((192, 320), (64, 64), True, 0.1, [0.7, 1.3, 1.1, 1.6]),        # odd tile counts, per-direction omega
     ((130, 66), (26, 22), False, 0.0, [1.5]),                       # ragged tiles, 5x3 boxes
     ((64, 64), (64, 64), True, 0.0, [1.2]),                         # one box
