@@ -174,7 +174,7 @@ extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int n
     CK(cudaMemset(g->flag, 0, sizeof(int)));
     CK(cudaMemset(g->cg, 0, sizeof(CgScalars)));
     if (d == 2 && sweep2d_supported(G))
-        make_maps2d(g->maps, g->X[0], g->X[1], g->pad[0], g->pad[1]);
+        make_maps2d(g->maps, g->X[0], g->X[1], g->B, g->pad[0], g->pad[1]);
     g->decomposed = true;
     return SW_OK;
 }
@@ -398,7 +398,7 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
         const double *xo = g->X[g->cur];
         double *xn = g->X[1 - g->cur];
         if (g->dim == 2 && g->fast2d && g->maps.ok && g->G.poisson) {
-            cudaError_t e = launch_sweep2p(g->maps.x[g->cur], g->G, base, w8, g->B, xn, g->flag, cs);
+            cudaError_t e = launch_sweep2p(g->maps.x[g->cur], g->maps.b, g->G, base, w8, g->B, xn, g->flag, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2p launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 2 && g->fast2d && g->maps.ok) {

@@ -31,6 +31,7 @@ constexpr int WSZ = WW * WW;
 
 struct Maps2d {
     CUtensorMap x[2];
+    CUtensorMap b;       // 64 x 64 tiles of b (L2 prefetch)
     bool ok = false;
 };
 
@@ -525,8 +526,9 @@ inline bool encode_2d(CUtensorMap *m, const double *base, int64_t pad0, int64_t 
     return r == CUDA_SUCCESS;
 }
 
-inline bool make_maps2d(Maps2d &M, const double *x0, const double *x1, int64_t pad0, int64_t pad1) {
-    M.ok = encode_2d(&M.x[0], x0, pad0, pad1, WW, WW) && encode_2d(&M.x[1], x1, pad0, pad1, WW, WW);
+inline bool make_maps2d(Maps2d &M, const double *x0, const double *x1, const double *b, int64_t pad0, int64_t pad1) {
+    M.ok = encode_2d(&M.x[0], x0, pad0, pad1, WW, WW) && encode_2d(&M.x[1], x1, pad0, pad1, WW, WW) &&
+           encode_2d(&M.b, b, pad0, pad1, T2, T2);
     return M.ok;
 }
 

@@ -2,11 +2,11 @@
 // sm_100a.  Version 2 of the 2D kernel (the v1 kernel in sweep2d.cuh still serves the
 // variable-coefficient case).
 //
-// One CTA = one warp = one box.  Six CTAs fit on an SM (36 KB of shared
-// memory each).  Per box:
+// One CTA = two warps = one box.  Six CTAs fit on an SM (36 KB of shared
+// memory each), so 12 warps share the latency of the staged loads.  Per box:
 //  1. Stage-in: one TMA load of the 68 x 68 window of x_old (box + 2-node halo,
-//     PAPER:828-833) into shared memory; the 64 rows of b are prefetched into L2 with bulk
-//     prefetches and read back coalesced through a register ring.
+//     PAPER:828-833) into shared memory; the 64 x 64 b tile is prefetched into L2 by a TMA
+//     tensor prefetch and read back coalesced through a register ring.
 //  2. Explicit parts (data parallel, coalesced): every owned node's
 //        r0 = fma(w/a_P, (b + u_E) + u_N, (1-w) u)         (DESIGN R-7)
 //     is written over its x_old in the window (rows in sweep order, so the north value is
@@ -16,13 +16,14 @@
 //  3. Corner and start-face chains: lane 0 solves the corner set (4 x 4, eq 2d:sor4b4, or
 //     2 x 2 / 1 x 1); then lane 0 runs the chain of 2 x 2 systems along local row 0 and
 //     lane 1 the chain along local column 0 (eq 2d:sor2b2), or the plain recurrence when
-//     the face is a physical boundary.
+//     the face is a physical boundary, with one branch-free body for all cases.
 //  4. Wavefront on rows 1..63 x columns 1..63: lane l owns rows 2l+1 and 2l+2 and at step s
 //     updates column c = s - l + 1 of both:
 //        u_A = fma(a, S, fma(a, W_A, r0_A)),   u_B = fma(a, u_A, fma(a, W_B, r0_B))
 //     with W from the lane's registers and S from lane l-1 by shfl.up (lane 0: row 0 in
 //     shared memory).  94 steps, in place.
-//  5. Write-back: 64 one-row bulk copies (cp.async.bulk) of the box to x_new.
+//  5. Write-back: coalesced 16-byte streaming stores of the 64 rows to x_new (per-lane bulk
+//     copies would need uniform operands and compile to a 32-way waterfall loop).
 // Elimination order and every fused operation follow the oracle (DESIGN R-7, R-8), so the
 // result is bitwise identical to it, independent of CTA schedule and GPU count.
 #pragma once
@@ -50,8 +51,9 @@ struct Sweep2pArgs {
     int *flag;
 };
 
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+                 : "memory");
 }
 
 // Gaussian elimination without pivoting (oracle ge_solve, DESIGN R-8).
@@ -85,7 +87,8 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
                                              bool cx, bool cy) {
     using namespace p2;
     const Geo &G = A.G;
-    const int lane = threadIdx.x;
+    const int warp = threadIdx.x >> 5;            // two warps per box
+    const int lane = threadIdx.x & 31;
     const int64_t P0 = G.P0;
     const int x0 = tx * T;                        // padded column of the window origin
     const int64_t y0 = (int64_t)ty * T;           // padded (slab-local) row of the window origin
@@ -102,81 +105,94 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
     const double w_o = A.omega[bits], w_x = A.omega[bits ^ 1], w_y = A.omega[bits ^ 2], w_d = A.omega[bits ^ 3];
     const double al = w_o / ap, al_x = w_x / ap, al_y = w_y / ap, al_d = w_d / ap;
     const double omw = 1.0 - w_o;
+    const int i00 = WI(0, 0);
 
     // ---------------------------------------------------------------- 1. stage-in
+    // Warp w computes local rows 32w .. 32w+31 of the prologue; its b rows stream through a
+    // register ring (the whole b tile was prefetched into L2 with the TMA load).
     const int wc = 2 + 2 * lane;                  // prologue: window columns wc, wc + 1
-    auto brow = [&](int t) { return reinterpret_cast<const double2 *>(Bg + (y0 + WY(t)) * P0 + x0 + wc); };
+    const int t_first = warp * (T / 2);
+    const int64_t bstep = (SY ? -P0 : P0) / 2;    // one local row of b, in double2 (P0 % 8 == 0)
+    const double2 *bp = reinterpret_cast<const double2 *>(Bg + (y0 + WY(t_first)) * P0 + x0 + wc);
     double2 ring[RING];
 #pragma unroll
-    for (int k = 0; k < RING; ++k) ring[k] = __ldg(brow(k));
-    prefetch_l2(brow(RING + lane), T * sizeof(double));                 // rows RING .. RING+31
-    if (lane < T - RING - 32) prefetch_l2(brow(RING + 32 + lane), T * sizeof(double));
-    // right-hand sides of the partner nodes
-    double bpx[2] = {0.0, 0.0}, bpy[2] = {0.0, 0.0}, bpd = 0.0;
+    for (int k = 0; k < RING; ++k) ring[k] = __ldg(bp + k * bstep);
+    bp += RING * bstep;
+    // right-hand sides of the partner nodes: warp 0 the y-face row, warp 1 the x-face column
+    // (and the diagonal corner partner)
+    double bp2[2] = {0.0, 0.0}, bpd = 0.0;
+    const bool cpl = warp ? cx : cy;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int k = h * 32 + lane;
-        if (cx) bpx[h] = __ldg(BG(WI(0, k) - dX));
-        if (cy) bpy[h] = __ldg(BG(WI(k, 0) - dY));
+        if (cpl) bp2[h] = __ldg(BG(warp ? WI(0, k) - dX : WI(k, 0) - dY));
     }
-    const int i00 = WI(0, 0);
-    if (cx && cy && lane == 0) bpd = __ldg(BG(i00 - dX - dY));
+    if (cx && cy && warp == 1 && lane == 0) bpd = __ldg(BG(i00 - dX - dY));
     mbar_wait(bar, 0);
 
     // ---------------------------------------------------------------- 2a. partner r0 (halo)
     // A partner across the x face sweeps x the other way and y our way: explicit
     // neighbours (-2, k) and (-1, k+1).  Across the y face: (k+1, -1) and (k, -2).
-    double rpx[2], rpy[2], rpd = 0.0;
+    {
+        const double alp = warp ? al_x : al_y, omp = 1.0 - (warp ? w_x : w_y);
+        const int ex = warp ? -dX : dX, ey = warp ? dY : -dY;   // explicit neighbour offsets
+        double rp[2], rpd = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int k = h * 32 + lane;
-        const int ix = WI(0, k) - dX, iy = WI(k, 0) - dY;
-        rpx[h] = fma(al_x, (bpx[h] + xw[ix - dX]) + xw[ix + dY], (1.0 - w_x) * xw[ix]);
-        rpy[h] = fma(al_y, (bpy[h] + xw[iy + dX]) + xw[iy - dY], (1.0 - w_y) * xw[iy]);
-    }
-    if (lane == 0) {
-        const int id = i00 - dX - dY;
-        rpd = fma(al_d, (bpd + xw[id - dX]) + xw[id - dY], (1.0 - w_d) * xw[id]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int k = h * 32 + lane;
-        if (cx) xw[WI(0, k) - dX] = rpx[h];
-        if (cy) xw[WI(k, 0) - dY] = rpy[h];
-    }
-    if (cx && cy && lane == 0) xw[i00 - dX - dY] = rpd;
-
-    // ---------------------------------------------------------------- 2b. own r0 (rows in sweep order)
-#pragma unroll 1
-    for (int t0 = 0; t0 < T; t0 += RING) {
-#pragma unroll
-        for (int k = 0; k < RING; ++k) {
-            const int t = t0 + k;
-            const int i = WY(t) * W + wc;
-            const double2 own = *reinterpret_cast<const double2 *>(xw + i);
-            const double2 nb = *reinterpret_cast<const double2 *>(xw + i + dY);
-            double e0, e1;                             // explicit (local +x) neighbours
-            if constexpr (SX) {
-                const double up = __shfl_up_sync(0xffffffffu, own.y, 1);
-                e0 = (lane == 0) ? xw[i - 1] : up;
-                e1 = own.x;
-            } else {
-                const double dn = __shfl_down_sync(0xffffffffu, own.x, 1);
-                e0 = own.y;
-                e1 = (lane == 31) ? xw[i + 2] : dn;
-            }
-            const double2 bb = ring[k];
-            const double r00 = fma(al, (bb.x + e0) + nb.x, omw * own.x);
-            const double r01 = fma(al, (bb.y + e1) + nb.y, omw * own.y);
-            *reinterpret_cast<double2 *>(xw + i) = make_double2(r00, r01);
-            if (t + RING < T) ring[k] = __ldg(brow(t + RING));
+        for (int h = 0; h < 2; ++h) {
+            const int k = h * 32 + lane;
+            const int ip = warp ? WI(0, k) - dX : WI(k, 0) - dY;
+            rp[h] = fma(alp, (bp2[h] + xw[ip + ex]) + xw[ip + ey], omp * xw[ip]);
         }
-    }
-    __syncwarp();
+        const int id = i00 - dX - dY;
+        if (warp == 1 && lane == 0) rpd = fma(al_d, (bpd + xw[id - dX]) + xw[id - dY], (1.0 - w_d) * xw[id]);
+        // warp 0 keeps the old values of row 32 (the north neighbours of its last row)
+        double2 save = make_double2(0.0, 0.0);
+        if (warp == 0) save = *reinterpret_cast<const double2 *>(xw + WY(T / 2) * W + wc);
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = h * 32 + lane;
+            if (cpl) xw[warp ? WI(0, k) - dX : WI(k, 0) - dY] = rp[h];
+        }
+        if (cx && cy && warp == 1 && lane == 0) xw[id] = rpd;
 
-    // ---------------------------------------------------------------- 3. corner and chains
-    if (lane == 0) {
+        // ------------------------------------------------------------ 2b. own r0 (rows in sweep order)
+        double *px = xw + WY(t_first) * W + wc;
+        double2 cur = *reinterpret_cast<const double2 *>(px);
+        auto row = [&](double2 bb, bool last) {
+            const double2 nb = (last && warp == 0) ? save : *reinterpret_cast<const double2 *>(px + dY);
+            double e0, e1;                                                    // explicit (local +x) neighbours
+            if constexpr (SX) {
+                const double up = __shfl_up_sync(0xffffffffu, cur.y, 1);
+                e0 = (lane == 0) ? px[-1] : up;
+                e1 = cur.x;
+            } else {
+                const double dn = __shfl_down_sync(0xffffffffu, cur.x, 1);
+                e0 = cur.y;
+                e1 = (lane == 31) ? px[2] : dn;
+            }
+            const double r00 = fma(al, (bb.x + e0) + nb.x, omw * cur.x);
+            const double r01 = fma(al, (bb.y + e1) + nb.y, omw * cur.y);
+            *reinterpret_cast<double2 *>(px) = make_double2(r00, r01);
+            cur = nb;
+            px += dY;
+        };
+#pragma unroll 1
+        for (int t0 = 0; t0 < T / 2 - RING; t0 += RING) {
+#pragma unroll
+            for (int k = 0; k < RING; ++k) {
+                row(ring[k], false);
+                ring[k] = __ldg(bp);
+                bp += bstep;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < RING; ++k) row(ring[k], k == RING - 1);
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------------- 3. corner and chains (warp 1)
+    if (warp == 1 && lane == 0) {
         if (cx && cy) {
             // members in ascending global index: (lo y, lo x), (lo y, hi x), (hi y, lo x), (hi y, hi x)
             constexpr int xlo_p = (SX == 0), ylo_p = (SY == 0);
@@ -214,43 +230,45 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
         // (no coupling: u(0,0) = r0, already in place)
     }
     __syncwarp();
-    if (lane < 2) {
+    if (warp == 1 && lane < 2) {
         // lane 0: chain along local row 0 (pairs across the y start face)
         // lane 1: chain along local column 0 (pairs across the x start face)
+        // Kept in member order: a = lower global index, row a: u_a - m_ab u_b = r_a (oracle
+        // ge_solve: u_b = fma(m_ba, r_a, r_b) / (1 - m_ba m_ab), u_a = fma(m_ab, u_b, r_a)).
+        // An uncoupled face (physical boundary) runs the same code with b = own node, a = the
+        // zero ghost node and m_ab = m_ba = 0, which leaves u_b = fma(al, W, r0) exactly.
         const int step = lane ? dY : dX;
         const int perp = lane ? dX : dY;
         const bool coupled = lane ? cx : cy;
         const bool pfirst = lane ? (SX == 0) : (SY == 0);
         const double alp = lane ? al_x : al_y;
-        // member a = lower global index; row a: u_a - m_ab u_b = r_a
-        const double mab = pfirst ? alp : al, mba = pfirst ? al : alp;
+        const bool a_is_p = pfirst || !coupled;
+        int ia = a_is_p ? i00 - perp : i00;
+        int ib = a_is_p ? i00 : i00 - perp;
+        const double ma = coupled ? (pfirst ? alp : al) : 0.0;
+        const double mb = pfirst || !coupled ? al : alp;
+        const double mab = coupled ? ma : 0.0, mba = coupled ? mb : 0.0;
         const double M11 = fma(mba, -mab, 1.0);
         if (coupled && !(fabs(M11) >= 1e-14)) atomicOr(A.flag, 1);
-        const double inv1 = 1.0 / M11;
-        int io = i00;
-        double po = xw[io], pp = coupled ? xw[io - perp] : 0.0;
+        const double inv1 = coupled ? 1.0 / M11 : 1.0;
+        double pa = xw[ia], pb = xw[ib];
 #pragma unroll 4
         for (int k = 1; k < T; ++k) {
-            io += step;
-            const double ro = fma(al, po, xw[io]);
-            if (coupled) {
-                const double rp = fma(alp, pp, xw[io - perp]);
-                const double ra = pfirst ? rp : ro, rb = pfirst ? ro : rp;
-                const double ub = fma(mba, ra, rb) * inv1;
-                const double ua = fma(mab, ub, ra) * 1.0;
-                po = pfirst ? ub : ua;
-                pp = pfirst ? ua : ub;
-                xw[io - perp] = pp;
-            } else {
-                po = ro;
-            }
-            xw[io] = po;
+            ia += step;
+            ib += step;
+            const double ra = fma(ma, pa, xw[ia]);
+            const double rb = fma(mb, pb, xw[ib]);
+            pb = fma(mba, ra, rb) * inv1;
+            pa = fma(mab, pb, ra);
+            xw[ia] = pa;
+            xw[ib] = pb;
         }
     }
     __syncwarp();
 
-    // ---------------------------------------------------------------- 4. wavefront
-    {
+    // ---------------------------------------------------------------- 4. wavefront (warp 0)
+    __syncthreads();
+    if (warp == 0) {
         const int rA = 2 * lane + 1;                       // rows A = 2l+1, B = 2l+2 (lane 31: B = 64, halo)
         double *pA = xw + WI(1, rA);                       // node (c, A) at pA + (c-1) dX
         double WA = pA[-dX];                               // u(0, A), u(0, B) from the column chain
@@ -283,24 +301,26 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
         for (int s = 63; s < 94; ++s) stepf(s, true);
     }
 
-    // ---------------------------------------------------------------- 5. write-back
-    fence_proxy_async_smem();
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int r = h * 32 + lane;                       // window row 2 + r
-        double *dst = A.xnew + (y0 + r + 2) * P0 + (x0 + 2);
-        bulk_store(dst, xw + (r + 2) * W + 2, T * sizeof(double));
+    // ---------------------------------------------------------------- 5. write-back (32 rows per warp)
+    __syncthreads();
+    {
+        const int r0 = 2 + warp * (T / 2);
+        const double *src = xw + r0 * W + wc;
+        double2 *dst = reinterpret_cast<double2 *>(A.xnew + (y0 + r0) * P0 + x0 + wc);
+#pragma unroll 8
+        for (int r = 0; r < T / 2; ++r) {
+            const double2 v = *reinterpret_cast<const double2 *>(src + r * W);
+            __stcs(dst + r * (P0 / 2), v);
+        }
     }
-    bulk_commit();
-    bulk_wait_read0();
 }
 
-__global__ void __launch_bounds__(32, 6) k_sweep2p(const __grid_constant__ CUtensorMap tmx, Sweep2pArgs A) {
+__global__ void __launch_bounds__(64, 6)
+    k_sweep2p(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, Sweep2pArgs A) {
     extern __shared__ __align__(128) double xw[];
     __shared__ uint64_t bar;
     const Geo &G = A.G;
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x;
     const int tx = blockIdx.x % G.nt[0];
     const int ty = blockIdx.x / G.nt[0];
     const int64_t R0 = tx, R1 = ty + G.toff[1];
@@ -308,13 +328,14 @@ __global__ void __launch_bounds__(32, 6) k_sweep2p(const __grid_constant__ CUten
     const int sy = ((A.base >> 1) & 1) ^ (int)(R1 & 1);
     const bool cx = sx ? (R0 < G.ntg[0] - 1) : (R0 > 0);
     const bool cy = sy ? (R1 < G.ntg[1] - 1) : (R1 > 0);
-    if (lane == 0) {
+    if (tid == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
         mbar_expect_tx(&bar, (uint32_t)p2::SMEM);
         tma_load_2d(xw, &tmx, tx * p2::T, ty * p2::T, &bar);
+        tma_prefetch_2d(&tmb, tx * p2::T + 2, ty * p2::T + 2);      // b tile into L2
     }
-    __syncwarp();
+    __syncthreads();
     switch (sx | (sy << 1)) {
         case 0: sweep2p_tile<0, 0>(A, xw, &bar, tx, ty, cx, cy); break;
         case 1: sweep2p_tile<1, 0>(A, xw, &bar, tx, ty, cx, cy); break;
@@ -323,7 +344,7 @@ __global__ void __launch_bounds__(32, 6) k_sweep2p(const __grid_constant__ CUten
     }
 }
 
-inline cudaError_t launch_sweep2p(const CUtensorMap &tmx, const Geo &G, int base, const double *w8, const double *b,
+inline cudaError_t launch_sweep2p(const CUtensorMap &tmx, const CUtensorMap &tmb, const Geo &G, int base, const double *w8, const double *b,
                                   double *xn, int *flag, cudaStream_t s) {
     Sweep2pArgs A;
     A.G = G;
@@ -339,7 +360,7 @@ inline cudaError_t launch_sweep2p(const CUtensorMap &tmx, const Geo &G, int base
         attr = true;
     }
     const unsigned tiles = (unsigned)((int64_t)G.nt[0] * G.nt[1]);
-    k_sweep2p<<<tiles, 32, p2::SMEM, s>>>(tmx, A);
+    k_sweep2p<<<tiles, 64, p2::SMEM, s>>>(tmx, tmb, A);
     return cudaGetLastError();
 }
 
