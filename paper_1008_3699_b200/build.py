@@ -23,7 +23,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in sources())
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, SRC, "-lcuda"]
+    extra = ["-DSW_TRACE"] if os.environ.get("SW_TRACE") == "1" else []
+    extra += [f"-D{d}" for d in os.environ.get("SW_DEFINES", "").split()]
+    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB, SRC, "-lcuda"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

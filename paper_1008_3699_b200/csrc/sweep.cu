@@ -610,3 +610,16 @@ extern "C" sw_status sw_destroy(sw_grid *g) {
     delete g;
     return SW_OK;
 }
+
+// Tuning aid (not part of sweep.h): per-phase clock sums of the traced kernels, then reset.
+extern "C" int sw_debug_phase_times(unsigned long long out[16]) {
+#ifdef SW_TRACE
+    unsigned long long zero[16] = {0};
+    if (cudaMemcpyFromSymbol(out, sw_trace_sum, sizeof(zero)) != cudaSuccess) return -1;
+    cudaMemcpyToSymbol(sw_trace_sum, zero, sizeof(zero));
+    return 16;
+#else
+    (void)out;
+    return 0;
+#endif
+}

@@ -21,7 +21,8 @@
 //     updates column c = s - l + 1 of both:
 //        u_A = fma(a, S, fma(a, W_A, r0_A)),   u_B = fma(a, u_A, fma(a, W_B, r0_B))
 //     with W from the lane's registers and S from lane l-1 by shfl.up (lane 0: row 0 in
-//     shared memory).  94 steps, in place.
+//     shared memory).  94 steps, in place, branch-free (idle lanes of the ramps only
+//     predicate their stores).
 //  5. Write-back: coalesced 16-byte streaming stores of the 64 rows to x_new (per-lane bulk
 //     copies would need uniform operands and compile to a 32-way waterfall loop).
 // Elimination order and every fused operation follow the oracle (DESIGN R-7, R-8), so the
@@ -54,6 +55,29 @@ struct Sweep2pArgs {
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
                  : "memory");
+}
+
+// Branch-free building blocks for the wavefront (the compiler otherwise turns guarded stores
+// and selects into divergent branches with reconvergence barriers around every shuffle).
+__device__ __forceinline__ void st_shared_if(double *addr, double v, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.f64 [%0], %1;\n}\n" ::"r"(smem_u32(addr)), "d"(v),
+        "r"((int)pred)
+        : "memory");
+}
+__device__ __forceinline__ double sel_f64(bool pred, double a, double b) {
+    double r;
+    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n selp.f64 %0, %2, %3, p;\n}\n" : "=d"(r) : "r"((int)pred), "d"(a), "d"(b));
+    return r;
+}
+__device__ __forceinline__ double shfl_up1_f64(double v) {   // full warp, converged by construction
+    int lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, 0xffffffff;" : "+r"(lo));
+    asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, 0xffffffff;" : "+r"(hi));
+    double r;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+    return r;
 }
 
 // Gaussian elimination without pivoting (oracle ge_solve, DESIGN R-8).
@@ -106,6 +130,7 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
     const double al = w_o / ap, al_x = w_x / ap, al_y = w_y / ap, al_d = w_d / ap;
     const double omw = 1.0 - w_o;
     const int i00 = WI(0, 0);
+    SW_TMARK(t_start);
 
     // ---------------------------------------------------------------- 1. stage-in
     // Warp w computes local rows 32w .. 32w+31 of the prologue; its b rows stream through a
@@ -129,6 +154,7 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
     }
     if (cx && cy && warp == 1 && lane == 0) bpd = __ldg(BG(i00 - dX - dY));
     mbar_wait(bar, 0);
+    SW_TMARK(t_staged);
 
     // ---------------------------------------------------------------- 2a. partner r0 (halo)
     // A partner across the x face sweeps x the other way and y our way: explicit
@@ -191,7 +217,9 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
     }
     __syncthreads();
 
+    SW_TMARK(t_prologue);
     // ---------------------------------------------------------------- 3. corner and chains (warp 1)
+    SW_TMARK(t_c0);
     if (warp == 1 && lane == 0) {
         if (cx && cy) {
             // members in ascending global index: (lo y, lo x), (lo y, hi x), (hi y, lo x), (hi y, hi x)
@@ -252,12 +280,18 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
         if (coupled && !(fabs(M11) >= 1e-14)) atomicOr(A.flag, 1);
         const double inv1 = coupled ? 1.0 / M11 : 1.0;
         double pa = xw[ia], pb = xw[ib];
+        // loads of step k+1 are issued before the stores of step k (they never alias, but the
+        // compiler cannot prove it for a run-time stride)
+        double na = xw[ia + step], nb = xw[ib + step];
 #pragma unroll 4
         for (int k = 1; k < T; ++k) {
             ia += step;
             ib += step;
-            const double ra = fma(ma, pa, xw[ia]);
-            const double rb = fma(mb, pb, xw[ib]);
+            const double r0a = na, r0b = nb;
+            na = xw[ia + step];
+            nb = xw[ib + step];
+            const double ra = fma(ma, pa, r0a);
+            const double rb = fma(mb, pb, r0b);
             pb = fma(mba, ra, rb) * inv1;
             pa = fma(mab, pb, ra);
             xw[ia] = pa;
@@ -265,44 +299,76 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
         }
     }
     __syncwarp();
+    SW_TMARK(t_c1);
+    SW_TADDT(6, t_c0, t_c1, 32);
 
     // ---------------------------------------------------------------- 4. wavefront (warp 0)
     __syncthreads();
+    SW_TMARK(t_chains);
+    SW_TMARK(t_w0);
     if (warp == 0) {
-        const int rA = 2 * lane + 1;                       // rows A = 2l+1, B = 2l+2 (lane 31: B = 64, halo)
+        // Lane l owns rows A = 2l+1, B = 2l+2 (lane 31: B = 64, halo, never stored) and at step
+        // s updates column c = s - SKEW l + 1 of both.  SKEW = 2 would give the shuffle carrying
+        // u_B of lane l-1 (needed as S by lane l) a whole step to arrive, at the price of 31
+        // more steps; measured, SKEW = 1 is faster.
+#ifndef SW_SKEW
+#define SW_SKEW 1
+#endif
+        constexpr int SKEW = SW_SKEW, NSTEP = (T - 1) + SKEW * 31;
+        const int rA = 2 * lane + 1;
         double *pA = xw + WI(1, rA);                       // node (c, A) at pA + (c-1) dX
         double WA = pA[-dX];                               // u(0, A), u(0, B) from the column chain
         double WB = pA[dY - dX];
-        double uB = 0.0;
-        auto stepf = [&](int s, bool pred) {
-            const int c = s - lane + 1;
-            const bool act = !pred || (c >= 1 && c <= T - 1);
-            double *p = pA + (c - 1) * dX;
-            const double r0A = p[0], r0B = p[dY];
-            const double row0 = p[-(rA)*dY];               // u(c, 0): only lane 0 uses it
-            const double sh = __shfl_up_sync(0xffffffffu, uB, 1);
-            const double S = (lane == 0) ? row0 : sh;
+        double uBp = 0.0, shv = 0.0;
+        // values of the current step, loaded during the previous one (before its stores: the
+        // addresses never alias, but the row-0 offset is lane dependent and the compiler
+        // would otherwise order every load after the previous step's stores)
+        double *p = pA + (-SKEW * lane) * dX;             // step 0: c = 1 - SKEW l
+        double nr0A = p[0], nr0B = p[dY], nrow0 = p[-(rA)*dY];
+        // RAMP: 1 = lanes join (lane l is idle before step SKEW l and keeps W = u(0, .)),
+        // 2 = lanes leave (lane l is done after step SKEW l + 62).  Branch-free: idle lanes
+        // only suppress their stores and, while joining, their W updates.  (u_B needs no
+        // guard: lane l+1 uses it only when lane l was busy.)
+        auto stepf = [&](int s, int RAMP) {
+            const int c = s - SKEW * lane + 1;
+            const bool act = RAMP == 1 ? c >= 1 : c <= T - 1;
+            const double r0A = nr0A, r0B = nr0B, row0 = nrow0;  // u(c, 0): only lane 0 uses row0
+            double *q = p + dX;
+            nr0A = q[0];
+            nr0B = q[dY];
+            nrow0 = q[-(rA)*dY];
+            double S;                                           // u_B of lane l-1 at column c
+            if constexpr (SKEW == 1) {                          // computed in the previous step
+                S = sel_f64(lane == 0, row0, shfl_up1_f64(uBp));
+            } else {                                            // two steps ago: shuffled last step
+                S = sel_f64(lane == 0, row0, shv);
+                shv = shfl_up1_f64(uBp);
+            }
             const double uA = fma(al, S, fma(al, WA, r0A));
             const double nB = fma(al, uA, fma(al, WB, r0B));
-            if (act) {
-                p[0] = uA;
-                if (lane < 31) p[dY] = nB;
+            st_shared_if(p, uA, act);
+            st_shared_if(p + dY, nB, act && lane < 31);
+            if (RAMP == 1) {
+                WA = sel_f64(act, uA, WA);
+                WB = sel_f64(act, nB, WB);
+            } else {
                 WA = uA;
                 WB = nB;
-                uB = nB;
             }
+            uBp = nB;
+            p = q;
         };
-        // ramp-up: lane l joins at step l; steady: all 32 lanes; ramp-down: lane l leaves after step l + 62
-#pragma unroll 2
-        for (int s = 0; s < 31; ++s) stepf(s, true);
 #pragma unroll 4
-        for (int s = 31; s < 63; ++s) stepf(s, false);
-#pragma unroll 2
-        for (int s = 63; s < 94; ++s) stepf(s, true);
+        for (int s = 0; s < SKEW * 31; ++s) stepf(s, 1);
+#pragma unroll 4
+        for (int s = SKEW * 31; s < NSTEP; ++s) stepf(s, 2);
+        SW_TMARK(t_w1);
+        SW_TADDT(7, t_w0, t_w1, 0);
     }
 
     // ---------------------------------------------------------------- 5. write-back (32 rows per warp)
     __syncthreads();
+    SW_TMARK(t_wave);
     {
         const int r0 = 2 + warp * (T / 2);
         const double *src = xw + r0 * W + wc;
@@ -313,6 +379,13 @@ __device__ __forceinline__ void sweep2p_tile(const Sweep2pArgs &A, double *xw, u
             __stcs(dst + r * (P0 / 2), v);
         }
     }
+    SW_TMARK(t_end);
+    SW_TADD(0, t_start, t_staged);
+    SW_TADD(1, t_staged, t_prologue);
+    SW_TADD(2, t_prologue, t_chains);
+    SW_TADD(3, t_chains, t_wave);
+    SW_TADD(4, t_wave, t_end);
+    SW_TADD(5, 0, 1);
 }
 
 __global__ void __launch_bounds__(64, 6)
