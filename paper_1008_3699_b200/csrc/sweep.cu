@@ -13,6 +13,7 @@
 #include "generic.cuh"
 #include "sweep2d.cuh"
 #include "sweep2p.cuh"
+#include "sweep2v.cuh"
 
 using namespace sw;
 
@@ -79,8 +80,9 @@ extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, d
     g->kind = kind;
     g->beta = beta;
     g->dev = cuda_device;
-    const char *env = getenv("SW_DISABLE_FAST2D");
+    const char *env = getenv("SW_DISABLE_FAST2D");   // 1: generic kernel only; 2: v1 2D kernel for faces
     if (env && env[0] == '1') g->fast2d = 0;
+    if (env && env[0] == '2') g->fast2d = 2;
     *out = g;
     return SW_OK;
 }
@@ -174,7 +176,7 @@ extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int n
     CK(cudaMemset(g->flag, 0, sizeof(int)));
     CK(cudaMemset(g->cg, 0, sizeof(CgScalars)));
     if (d == 2 && sweep2d_supported(G))
-        make_maps2d(g->maps, g->X[0], g->X[1], g->B, g->pad[0], g->pad[1]);
+        make_maps2d(g->maps, g->X[0], g->X[1], g->B, g->F[0], g->F[1], g->pad[0], g->pad[1]);
     g->decomposed = true;
     return SW_OK;
 }
@@ -401,6 +403,11 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             cudaError_t e = launch_sweep2p(g->maps.x[g->cur], g->maps.b, g->G, base, w8, g->B, xn, g->flag, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2p launch: ") + cudaGetErrorString(e));
+        } else if (g->dim == 2 && g->fast2d && g->maps.ok && g->maps.fok && g->fast2d != 2) {
+            cudaError_t e = launch_sweep2v(g->maps.x[g->cur], g->maps.b, g->maps.f[0], g->maps.f[1], g->G, base, w8,
+                                           g->B, g->F[0], g->F[1], xn, g->flag, cs);
+            g->launches++;
+            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2v launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 2 && g->fast2d && g->maps.ok) {
             cudaError_t e = launch_sweep2d(g->maps, g->cur, g->G, base, w8, g->B, g->F, xn, g->flag, !g->G.poisson, cs);
             g->launches++;

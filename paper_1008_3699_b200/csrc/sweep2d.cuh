@@ -32,7 +32,8 @@ constexpr int WSZ = WW * WW;
 struct Maps2d {
     CUtensorMap x[2];
     CUtensorMap b;       // 64 x 64 tiles of b (L2 prefetch)
-    bool ok = false;
+    CUtensorMap f[2];    // 64 x 64 tiles of F_x, F_y (L2 prefetch; variable coefficients only)
+    bool ok = false, fok = false;
 };
 
 struct Sweep2dArgs {
@@ -526,9 +527,11 @@ inline bool encode_2d(CUtensorMap *m, const double *base, int64_t pad0, int64_t 
     return r == CUDA_SUCCESS;
 }
 
-inline bool make_maps2d(Maps2d &M, const double *x0, const double *x1, const double *b, int64_t pad0, int64_t pad1) {
+inline bool make_maps2d(Maps2d &M, const double *x0, const double *x1, const double *b, const double *fx,
+                        const double *fy, int64_t pad0, int64_t pad1) {
     M.ok = encode_2d(&M.x[0], x0, pad0, pad1, WW, WW) && encode_2d(&M.x[1], x1, pad0, pad1, WW, WW) &&
            encode_2d(&M.b, b, pad0, pad1, T2, T2);
+    M.fok = fx && fy && encode_2d(&M.f[0], fx, pad0, pad1, T2, T2) && encode_2d(&M.f[1], fy, pad0, pad1, T2, T2);
     return M.ok;
 }
 
