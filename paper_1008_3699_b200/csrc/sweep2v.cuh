@@ -32,7 +32,7 @@ constexpr int NW = 4;                   // warps per box
 constexpr int ROWS = T / NW;            // prologue rows per warp
 constexpr int RING = 4;                 // rows in flight per warp
 constexpr int NCOEF = T * T;            // m_W / m_S arrays, pitch 64 (window column order)
-constexpr int NCH = 4 * T + 4;          // chain partner couplings + diagonal couplings + zero
+constexpr int NCH = 6 * T + 4;          // chain partner couplings, chain pivots, diagonal couplings, 0, 1
 constexpr size_t SMEM = sizeof(double) * (WS + 2 * NCOEF + NCH);
 }  // namespace v2
 
@@ -45,6 +45,13 @@ struct Sweep2vArgs {
     int *flag;
 };
 
+// Shared-memory store that the compiler does not treat as a memory clobber: used for the
+// coupling arrays, which no load of the same phase reads (the explicit-part loads of later
+// rows would otherwise be ordered after every coupling store).
+__device__ __forceinline__ void st_shared_v2_noalias(double *addr, double a, double b) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(addr)), "d"(a), "d"(b));
+}
+
 template <int SX, int SY>
 __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, uint64_t *bar, int tx, int ty, bool cx,
                                              bool cy) {
@@ -56,7 +63,9 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
     double *ych_p = ych_c + T;             //                        coupling to own (k,0)
     double *xch_c = ych_p + T;             // x-face partner (-1,k): coupling to (-1,k-1)
     double *xch_p = xch_c + T;             //                        coupling to own (0,k)
-    double *dg = xch_p + T;                // [0] diagonal -> (0,-1), [1] diagonal -> (-1,0), [2] = 0.0
+    double *inv_y = xch_p + T;             // 1 / (1 - m_own m_partner) of the y-face pairs (k,0),(k,-1)
+    double *inv_x = inv_y + T;             //                              x-face pairs (0,k),(-1,k)
+    double *dg = inv_x + T;                // [0] diagonal -> (0,-1), [1] diagonal -> (-1,0), [2] = 0, [3] = 1
 
     const Geo &G = A.G;
     const int warp = threadIdx.x >> 5;
@@ -119,13 +128,13 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             const double bv = __ldg(Bg + g);
             const double ap = ((xl + xh) + (yl + yh)) + beta;
             if (warp == 0) {        // y-face partner: x as ours, y flipped
-                const double al = w_y / ap;
+                const double al = div_rn(w_y, ap);
                 const double e = fma(SY ? yh : yl, xw[ip - dY], fma(SX ? xl : xh, xw[ip + dX], bv));
                 rp[h] = fma(al, e, (1.0 - w_y) * xw[ip]);
                 mc[h] = al * (SX ? xh : xl);
                 mp[h] = al * (SY ? yl : yh);
             } else {                // x-face partner: x flipped, y as ours
-                const double al = w_x / ap;
+                const double al = div_rn(w_x, ap);
                 const double e = fma(SY ? yl : yh, xw[ip + dY], fma(SX ? xh : xl, xw[ip - dX], bv));
                 rp[h] = fma(al, e, (1.0 - w_x) * xw[ip]);
                 mc[h] = al * (SY ? yh : yl);
@@ -138,7 +147,7 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             const double xl = __ldg(Fx + g), xh = __ldg(Fx + g + 1), yl = __ldg(Fy + g), yh = __ldg(Fy + g + P0);
             const double bv = __ldg(Bg + g);
             const double ap = ((xl + xh) + (yl + yh)) + beta;
-            const double al = w_d / ap;
+            const double al = div_rn(w_d, ap);
             const double e = fma(SY ? yh : yl, xw[id - dY], fma(SX ? xh : xl, xw[id - dX], bv));
             rpd = fma(al, e, (1.0 - w_d) * xw[id]);
             dmx = al * (SX ? xl : xh);
@@ -162,6 +171,7 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             dg[0] = dmx;
             dg[1] = dmy;
             dg[2] = 0.0;
+            dg[3] = 1.0;
         }
     }
 
@@ -193,13 +203,13 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             const double xl0 = fx.x, xh0 = fx.y, xl1 = fx.y, xh1 = fx2;
             const double ap0 = ((xl0 + xh0) + (ylo.x + yhi.x)) + beta;
             const double ap1 = ((xl1 + xh1) + (ylo.y + yhi.y)) + beta;
-            const double a0 = w_o / ap0, a1 = w_o / ap1;
+            const double a0 = div_rn(w_o, ap0), a1 = div_rn(w_o, ap1);
             const double2 bb = rb[k];
             const double r00 = fma(a0, fma(SY ? ylo.x : yhi.x, nb.x, fma(SX ? xl0 : xh0, e0, bb.x)), omw * cur.x);
             const double r01 = fma(a1, fma(SY ? ylo.y : yhi.y, nb.y, fma(SX ? xl1 : xh1, e1, bb.y)), omw * cur.y);
             *reinterpret_cast<double2 *>(px) = make_double2(r00, r01);
-            *reinterpret_cast<double2 *>(pw) = make_double2(a0 * (SX ? xh0 : xl0), a1 * (SX ? xh1 : xl1));
-            *reinterpret_cast<double2 *>(pw + NCOEF) = make_double2(a0 * (SY ? yhi.x : ylo.x), a1 * (SY ? yhi.y : ylo.y));
+            st_shared_v2_noalias(pw, a0 * (SX ? xh0 : xl0), a1 * (SX ? xh1 : xl1));
+            st_shared_v2_noalias(pw + NCOEF, a0 * (SY ? yhi.x : ylo.x), a1 * (SY ? yhi.y : ylo.y));
             cur = nb;
             px += dY;
             pw += dYw;
@@ -263,6 +273,20 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             xw[ip] = pfirst ? uu[0] : uu[1];
         }
     }
+    if (warp == 1) {
+        // pivots of the chain pairs, all k in parallel: fma(m_ba, -m_ab, 1) is symmetric in the
+        // two couplings (exact product), so member order does not matter here
+        int fl = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = h * 32 + lane;
+            const double my = fma(cS[CI(k, 0)], -ych_p[k], 1.0), mx = fma(cW[CI(0, k)], -xch_p[k], 1.0);
+            fl |= (cy && !(fabs(my) >= 1e-14)) || (cx && !(fabs(mx) >= 1e-14));
+            inv_y[k] = div_rn(1.0, my);
+            inv_x[k] = div_rn(1.0, mx);
+        }
+        if (fl) atomicOr(A.flag, 1);
+    }
     __syncwarp();
     SW_TMARK(t_c0);
     if (warp == 1 && lane < 2) {
@@ -285,27 +309,26 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
         const double *qab = a_is_p ? (coupled ? pp : zero) : op;
         const double *qba = a_is_p ? (coupled ? op : zero) : pp;
         const int sba = a_is_p ? (coupled ? cstep : 0) : 1;
+        const double *qi = coupled ? (lane ? inv_x : inv_y) : dg + 3;
+        const int si = coupled ? 1 : 0;
         int ia = a_is_p ? i00 - perp : i00;
         int ib = a_is_p ? i00 : i00 - perp;
         double pa = xw[ia], pb2 = xw[ib];
         // step k+1 operands are loaded before the stores of step k
         double n_ra = xw[ia + step], n_rb = xw[ib + step];
-        double n_ma = qa[sa], n_mb = qb[sb], n_mab = qab[sa], n_mba = qba[sba];
-        int fl = 0;
+        double n_ma = qa[sa], n_mb = qb[sb], n_mab = qab[sa], n_mba = qba[sba], n_inv = qi[si];
 #pragma unroll 2
         for (int k = 1; k < T; ++k) {
             ia += step;
             ib += step;
-            const double r0a = n_ra, r0b = n_rb, ma = n_ma, mb = n_mb, mab = n_mab, mba = n_mba;
+            const double r0a = n_ra, r0b = n_rb, ma = n_ma, mb = n_mb, mab = n_mab, mba = n_mba, inv1 = n_inv;
             n_ra = xw[ia + step];
             n_rb = xw[ib + step];
             n_ma = qa[(k + 1) * sa];
             n_mb = qb[(k + 1) * sb];
             n_mab = qab[(k + 1) * sa];
             n_mba = qba[(k + 1) * sba];
-            const double M11 = fma(mba, -mab, 1.0);
-            fl |= coupled && !(fabs(M11) >= 1e-14);
-            const double inv1 = 1.0 / M11;
+            n_inv = qi[(k + 1) * si];
             const double ra = fma(ma, pa, r0a);
             const double rb = fma(mb, pb2, r0b);
             pb2 = fma(mba, ra, rb) * inv1;
@@ -313,7 +336,6 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             xw[ia] = pa;
             xw[ib] = pb2;
         }
-        if (fl) atomicOr(A.flag, 1);
     }
     __syncwarp();
     SW_TMARK(t_c1);
