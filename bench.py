@@ -55,7 +55,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -182,7 +182,7 @@ def run_ours(args):
     kavg = float(np.mean(kern_ms))
     achieved = per_launch_bytes / (kavg * 1e-3) / 1e9
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "sweep2d_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "sweep2p_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("bytes_per_launch")
@@ -210,8 +210,11 @@ def run_ours(args):
             times.append(e0.elapsed_time(e1))
         t = min(times)
         e2e = {"value": round(NX * nl_y * nsw / (t * 1e-3) / 1e9, 3), "unit": "GLUP/s",
-               "h2d_bytes_per_step": int(2 * NX * nl_y * 8), "d2h_bytes_per_step": int(NX * nl_y * 8),
-               "step": f"one job: b,x0 H2D from pinned host + {nsw} sweeps + x D2H", "ms_per_job": round(t, 3)}
+               "h2d_bytes_per_step": int(2 * NX * nl_y * 8) // nsw, "d2h_bytes_per_step": int(NX * nl_y * 8) // nsw,
+               "step": f"one user job through the C ABI: b and x0 copied H2D from pinned host memory, {nsw} sweeps "
+                       f"(config 4's count), x copied D2H; bytes per step = job bytes / {nsw}",
+               "h2d_bytes_per_job": int(2 * NX * nl_y * 8), "d2h_bytes_per_job": int(NX * nl_y * 8),
+               "ms_per_job": round(t, 3)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -229,7 +232,7 @@ def run_ours(args):
                        "l2": "inputs (2.1 GB per array) exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "sweep (decomposed SOR, 24 algorithmic B/LUP)", "peak_source": peak_src,
+                         "kernel": "k_sweep2p (decomposed SOR, 24 algorithmic B/LUP)", "peak_source": peak_src,
                          "kernel_ms": round(kavg, 4)},
             "e2e": e2e,
             "gpu_launches": launches,
@@ -291,7 +294,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU session: parity tests, smoke, bench, launch list, one ncu --set full capture.
+# One GPU session: parity tests, smoke, bench, launch list, ncu --set full of the bench's top kernel.
 # usage (under gpurun): bash tools/gpu_round.sh [tag]
 set -u
 TAG=${1:-r01}
@@ -11,11 +11,11 @@ python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { ec
 timeout 900 python -m pytest tests -m gpu -x -q --timeout 180 > $OUT/pytest_gpu.log 2>&1; echo "pytest gpu exit $?"; tail -3 $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?"; tail -2 $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?"; cat $OUT/bench.json
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref exit $?"; cat $OUT/bench_ref.json
+CMD="python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu"
 timeout 300 $CMD > $OUT/plain_launch.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "ncu launches exit $?"
-PCMD="python tools/profile_case.py --n 16384 --sweeps 2"
-timeout 300 $PCMD > $OUT/plain_prof.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep2d -s 2 -c 1 -o $OUT/sweep2d_poisson $PCMD > $OUT/ncu_full.log 2>&1
+timeout 300 $CMD > $OUT/plain_prof.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep2p -s 4 -c 1 -o $OUT/sweep2p $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu full exit $?"
