@@ -14,6 +14,7 @@
 #include "sweep2d.cuh"
 #include "sweep2p.cuh"
 #include "sweep2v.cuh"
+#include "tri2t.cuh"
 
 using namespace sw;
 
@@ -56,7 +57,26 @@ struct sw_grid {
     int64_t launches = 0;
     int fast2d = 1;
     Maps2d maps;
+    struct MapEntry {
+        const void *ptr;
+        int box;
+        CUtensorMap map;
+    };
+    std::vector<MapEntry> mapcache;   // TMA descriptors of arrays used as solve inputs
 };
+
+// TMA descriptor (box x box window at the padded origin) of a padded array, cached by pointer
+static const CUtensorMap *get_map(sw_grid *g, const double *ptr, int box) {
+    for (auto &e : g->mapcache)
+        if (e.ptr == ptr && e.box == box) return &e.map;
+    sw_grid::MapEntry e;
+    e.ptr = ptr;
+    e.box = box;
+    if (!encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box)) return nullptr;
+    if (g->mapcache.size() > 32) g->mapcache.erase(g->mapcache.begin());
+    g->mapcache.push_back(e);
+    return &g->mapcache.back().map;
+}
 
 extern "C" const char *sw_last_error(void) { return g_err.c_str(); }
 
@@ -494,11 +514,37 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     if (ilu && !g->factored) return fail(SW_ESTATE, "sw_ilu0_factor must precede sw_ilu_apply");
     if (!ilu && !(omega > 0.0 && omega < 2.0)) return fail(SW_EINVAL, "omega must lie in (0,2)");
     if (!r || !z || z == g->Y || r == z) return fail(SW_EINVAL, "bad r/z pointers");
+    int base = base_bits(g->dim, g->factor_phase);
+    if (g->dim == 2 && g->fast2d && g->maps.ok) {
+        // fast 64 x 64 path: forward solve, then the PAPER backward (forward solve at the reversed
+        // corner) or the SYMMETRIC backward (uncoupled reversed solve + start-face chain pass)
+        const double *invd = ilu ? g->invD : nullptr;
+        const double *fx = g->G.poisson ? nullptr : g->F[0], *fy = g->G.poisson ? nullptr : g->F[1];
+        const CUtensorMap &mfx = g->G.poisson ? g->maps.b : g->maps.f[0];
+        const CUtensorMap &mfy = g->G.poisson ? g->maps.b : g->maps.f[1];
+        const CUtensorMap *mr = get_map(g, r, WW), *my = get_map(g, g->Y, WW), *maux = get_map(g, g->invD, T2);
+        if (!mr || !my || !maux) return fail(SW_ECUDA, "cuTensorMapEncodeTiled failed");
+        const double coef = ilu ? 1.0 : 2.0 - omega;
+        cudaError_t e = launch_tri2v(*mr, *maux, mfx, mfy, g->G, base, omega, invd, fx, fy, true, 1.0, true, g->Y,
+                                     g->flag, s);
+        g->launches++;
+        if (e == cudaSuccess) {
+            const int rev = base ^ 3;
+            e = launch_tri2v(*my, *maux, mfx, mfy, g->G, rev, omega, invd, fx, fy, false, coef,
+                             pairing == SW_PAIR_PAPER, z, g->flag, s);
+            g->launches++;
+        }
+        if (e == cudaSuccess && pairing == SW_PAIR_SYMMETRIC) {
+            e = launch_tri2t(g->G, base, omega, invd, fx, fy, g->Y, z, coef, g->flag, s);
+            g->launches += 2;
+        }
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("tri2 launch: ") + cudaGetErrorString(e));
+        return SW_OK;
+    }
     KParams P = base_params(g);
     P.alpha_mode = ilu ? A_INVD : A_OMEGA_AP;
     P.invD = g->invD;
     for (int i = 0; i < 8; ++i) P.omega[i] = omega;
-    int base = base_bits(g->dim, g->factor_phase);
     // forward: (D~ + L) y = r   (row-normalised: r0 = alpha r)
     P.mode = M_FWD;
     P.rhs = R_SCALE;

@@ -36,13 +36,22 @@ constexpr int NCH = 6 * T + 4;          // chain partner couplings, chain pivots
 constexpr size_t SMEM = sizeof(double) * (WS + 2 * NCOEF + NCH);
 }  // namespace v2
 
+// MODE_SOR: one decomposed SOR sweep (window = x_old, aux = b).
+// MODE_TRI: one block-triangular solve (D/alpha + A_I) out = r (the ILU / SSOR factors,
+//   SURVEY §8(a) a11-a12): window = src, r0 = alpha src (rscale) or coef src, alpha = 1/D~ from
+//   aux (invd_mode, ILU) or omega / a_P (SSOR); couple = 0 drops the start-face coupling (the
+//   first phase of the transposed solve, run at the reversed corner).
+enum { MODE_SOR = 0, MODE_TRI = 1 };
+
 struct Sweep2vArgs {
     Geo G;
     int base;
     double omega[4];
-    const double *b, *fx, *fy;   // padded b, F_x, F_y
+    const double *b, *fx, *fy;   // padded aux (b or 1/D~), F_x, F_y
     double *xnew;
     int *flag;
+    double coef;
+    int invd_mode, rscale, couple;
 };
 
 // Shared-memory store that the compiler does not treat as a memory clobber: used for the
@@ -52,9 +61,12 @@ __device__ __forceinline__ void st_shared_v2_noalias(double *addr, double a, dou
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(addr)), "d"(a), "d"(b));
 }
 
-template <int SX, int SY>
+template <int MODE, bool FACES, int SX, int SY>
 __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, uint64_t *bar, int tx, int ty, bool cx,
                                              bool cy) {
+    constexpr bool SOR = (MODE == MODE_SOR);
+    const bool invd = !SOR && A.invd_mode;      // alpha = 1/D~ from the aux array (ILU)
+    const bool load_aux = SOR || invd;
     using namespace v2;
     double *xw = sm;                       // x window; r0 and results in place
     double *cW = xw + WS;                  // m_W per own node, index (wr-2)*64 + (wc-2)
@@ -100,13 +112,19 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
     double rfe[RING];
 #pragma unroll
     for (int k = 0; k < RING; ++k) {
-        rb[k] = __ldg(reinterpret_cast<const double2 *>(pb + k * rstep));
-        rfx[k] = __ldg(reinterpret_cast<const double2 *>(pfx + k * rstep));
-        rfe[k] = (lane == 31) ? __ldg(pfx + k * rstep + 2) : 0.0;
-        rfy[k] = __ldg(reinterpret_cast<const double2 *>(pfy + k * rstep));
+        rb[k] = load_aux ? __ldg(reinterpret_cast<const double2 *>(pb + k * rstep)) : make_double2(0.0, 0.0);
+        if constexpr (FACES) {
+            rfx[k] = __ldg(reinterpret_cast<const double2 *>(pfx + k * rstep));
+            rfe[k] = (lane == 31) ? __ldg(pfx + k * rstep + 2) : 0.0;
+            rfy[k] = __ldg(reinterpret_cast<const double2 *>(pfy + k * rstep));
+        } else {
+            rfx[k] = rfy[k] = make_double2(1.0, 1.0);
+            rfe[k] = 1.0;
+        }
     }
     // F_y row carried in from the row before the first one
-    double2 fcarry = __ldg(reinterpret_cast<const double2 *>(Fy + g_first + (SY ? P0 : 0)));
+    double2 fcarry = make_double2(1.0, 1.0);
+    if constexpr (FACES) fcarry = __ldg(reinterpret_cast<const double2 *>(Fy + g_first + (SY ? P0 : 0)));
     pb += RING * rstep;
     pfx += RING * rstep;
     pfy += RING * rstep;
@@ -124,19 +142,30 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             const int k = h * 32 + lane;
             const int ip = warp ? WI(0, k) - dX : WI(k, 0) - dY;
             const int64_t g = PI(ip);
-            const double xl = __ldg(Fx + g), xh = __ldg(Fx + g + 1), yl = __ldg(Fy + g), yh = __ldg(Fy + g + P0);
-            const double bv = __ldg(Bg + g);
+            double xl = 1.0, xh = 1.0, yl = 1.0, yh = 1.0;
+            if constexpr (FACES) {
+                xl = __ldg(Fx + g); xh = __ldg(Fx + g + 1); yl = __ldg(Fy + g); yh = __ldg(Fy + g + P0);
+            }
+            const double bv = load_aux ? __ldg(Bg + g) : 0.0;
             const double ap = ((xl + xh) + (yl + yh)) + beta;
             if (warp == 0) {        // y-face partner: x as ours, y flipped
-                const double al = div_rn(w_y, ap);
-                const double e = fma(SY ? yh : yl, xw[ip - dY], fma(SX ? xl : xh, xw[ip + dX], bv));
-                rp[h] = fma(al, e, (1.0 - w_y) * xw[ip]);
+                const double al = invd ? bv : div_rn(w_y, ap);
+                if constexpr (SOR) {
+                    const double e = fma(SY ? yh : yl, xw[ip - dY], fma(SX ? xl : xh, xw[ip + dX], bv));
+                    rp[h] = fma(al, e, (1.0 - w_y) * xw[ip]);
+                } else {
+                    rp[h] = A.rscale ? al * xw[ip] : A.coef * xw[ip];
+                }
                 mc[h] = al * (SX ? xh : xl);
                 mp[h] = al * (SY ? yl : yh);
             } else {                // x-face partner: x flipped, y as ours
-                const double al = div_rn(w_x, ap);
-                const double e = fma(SY ? yl : yh, xw[ip + dY], fma(SX ? xh : xl, xw[ip - dX], bv));
-                rp[h] = fma(al, e, (1.0 - w_x) * xw[ip]);
+                const double al = invd ? bv : div_rn(w_x, ap);
+                if constexpr (SOR) {
+                    const double e = fma(SY ? yl : yh, xw[ip + dY], fma(SX ? xh : xl, xw[ip - dX], bv));
+                    rp[h] = fma(al, e, (1.0 - w_x) * xw[ip]);
+                } else {
+                    rp[h] = A.rscale ? al * xw[ip] : A.coef * xw[ip];
+                }
                 mc[h] = al * (SY ? yh : yl);
                 mp[h] = al * (SX ? xl : xh);
             }
@@ -144,19 +173,26 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
         if (warp == 1 && lane == 0) {   // diagonal partner: both flipped
             const int id = i00 - dX - dY;
             const int64_t g = PI(id);
-            const double xl = __ldg(Fx + g), xh = __ldg(Fx + g + 1), yl = __ldg(Fy + g), yh = __ldg(Fy + g + P0);
-            const double bv = __ldg(Bg + g);
+            double xl = 1.0, xh = 1.0, yl = 1.0, yh = 1.0;
+            if constexpr (FACES) {
+                xl = __ldg(Fx + g); xh = __ldg(Fx + g + 1); yl = __ldg(Fy + g); yh = __ldg(Fy + g + P0);
+            }
+            const double bv = load_aux ? __ldg(Bg + g) : 0.0;
             const double ap = ((xl + xh) + (yl + yh)) + beta;
-            const double al = div_rn(w_d, ap);
-            const double e = fma(SY ? yh : yl, xw[id - dY], fma(SX ? xh : xl, xw[id - dX], bv));
-            rpd = fma(al, e, (1.0 - w_d) * xw[id]);
+            const double al = invd ? bv : div_rn(w_d, ap);
+            if constexpr (SOR) {
+                const double e = fma(SY ? yh : yl, xw[id - dY], fma(SX ? xh : xl, xw[id - dX], bv));
+                rpd = fma(al, e, (1.0 - w_d) * xw[id]);
+            } else {
+                rpd = A.rscale ? al * xw[id] : A.coef * xw[id];
+            }
             dmx = al * (SX ? xl : xh);
             dmy = al * (SY ? yl : yh);
         }
     }
     // each warp keeps the old values of the row after its last one (north of its last row)
     double2 save = make_double2(0.0, 0.0);
-    if (warp < NW - 1) save = *reinterpret_cast<const double2 *>(xw + WY(t_first + ROWS) * W + wc);
+    if (SOR && warp < NW - 1) save = *reinterpret_cast<const double2 *>(xw + WY(t_first + ROWS) * W + wc);
     __syncthreads();
     if (warp < 2) {
 #pragma unroll
@@ -180,19 +216,9 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
         double *px = xw + WY(t_first) * W + wc;
         double *pw = cW + (WY(t_first) - 2) * T + (wc - 2);
         constexpr int dYw = SY ? -T : T;
-        double2 cur = *reinterpret_cast<const double2 *>(px);
+        double2 cur = make_double2(0.0, 0.0);
+        if constexpr (SOR) cur = *reinterpret_cast<const double2 *>(px);
         auto row = [&](int k, bool last) {
-            const double2 nb = (last && warp < NW - 1) ? save : *reinterpret_cast<const double2 *>(px + dY);
-            double e0, e1;                                   // explicit (local +x) neighbours
-            if constexpr (SX) {
-                const double up = __shfl_up_sync(0xffffffffu, cur.y, 1);
-                e0 = (lane == 0) ? px[-1] : up;
-                e1 = cur.x;
-            } else {
-                const double dn = __shfl_down_sync(0xffffffffu, cur.x, 1);
-                e0 = cur.y;
-                e1 = (lane == 31) ? px[2] : dn;
-            }
             // faces, global orientation: node 0 = column wc, node 1 = wc + 1
             const double2 fx = rfx[k];
             const double fxn = __shfl_down_sync(0xffffffffu, fx.x, 1);   // all lanes take part
@@ -200,17 +226,43 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
             const double2 fn = rfy[k];
             const double2 ylo = SY ? fn : fcarry, yhi = SY ? fcarry : fn;
             fcarry = fn;
-            const double xl0 = fx.x, xh0 = fx.y, xl1 = fx.y, xh1 = fx2;
-            const double ap0 = ((xl0 + xh0) + (ylo.x + yhi.x)) + beta;
-            const double ap1 = ((xl1 + xh1) + (ylo.y + yhi.y)) + beta;
-            const double a0 = div_rn(w_o, ap0), a1 = div_rn(w_o, ap1);
+            const double xl0 = fx.x, xh0 = fx.y, xl1 = fx.y, xh1 = FACES ? fx2 : 1.0;
             const double2 bb = rb[k];
-            const double r00 = fma(a0, fma(SY ? ylo.x : yhi.x, nb.x, fma(SX ? xl0 : xh0, e0, bb.x)), omw * cur.x);
-            const double r01 = fma(a1, fma(SY ? ylo.y : yhi.y, nb.y, fma(SX ? xl1 : xh1, e1, bb.y)), omw * cur.y);
+            double a0, a1, r00, r01;
+            if constexpr (SOR) {
+                const double2 nb = (last && warp < NW - 1) ? save : *reinterpret_cast<const double2 *>(px + dY);
+                double e0, e1;                               // explicit (local +x) neighbours
+                if constexpr (SX) {
+                    const double up = __shfl_up_sync(0xffffffffu, cur.y, 1);
+                    e0 = (lane == 0) ? px[-1] : up;
+                    e1 = cur.x;
+                } else {
+                    const double dn = __shfl_down_sync(0xffffffffu, cur.x, 1);
+                    e0 = cur.y;
+                    e1 = (lane == 31) ? px[2] : dn;
+                }
+                const double ap0 = ((xl0 + xh0) + (ylo.x + yhi.x)) + beta;
+                const double ap1 = ((xl1 + xh1) + (ylo.y + yhi.y)) + beta;
+                a0 = div_rn(w_o, ap0);
+                a1 = div_rn(w_o, ap1);
+                r00 = fma(a0, fma(SY ? ylo.x : yhi.x, nb.x, fma(SX ? xl0 : xh0, e0, bb.x)), omw * cur.x);
+                r01 = fma(a1, fma(SY ? ylo.y : yhi.y, nb.y, fma(SX ? xl1 : xh1, e1, bb.y)), omw * cur.y);
+                cur = nb;
+            } else {
+                const double2 sv = *reinterpret_cast<const double2 *>(px);
+                if (invd) {
+                    a0 = bb.x;
+                    a1 = bb.y;
+                } else {
+                    a0 = div_rn(w_o, ((xl0 + xh0) + (ylo.x + yhi.x)) + beta);
+                    a1 = div_rn(w_o, ((xl1 + xh1) + (ylo.y + yhi.y)) + beta);
+                }
+                r00 = A.rscale ? a0 * sv.x : A.coef * sv.x;
+                r01 = A.rscale ? a1 * sv.y : A.coef * sv.y;
+            }
             *reinterpret_cast<double2 *>(px) = make_double2(r00, r01);
             st_shared_v2_noalias(pw, a0 * (SX ? xh0 : xl0), a1 * (SX ? xh1 : xl1));
             st_shared_v2_noalias(pw + NCOEF, a0 * (SY ? yhi.x : ylo.x), a1 * (SY ? yhi.y : ylo.y));
-            cur = nb;
             px += dY;
             pw += dYw;
         };
@@ -219,10 +271,12 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
 #pragma unroll
             for (int k = 0; k < RING; ++k) {
                 row(k, false);
-                rb[k] = __ldg(reinterpret_cast<const double2 *>(pb));
-                rfx[k] = __ldg(reinterpret_cast<const double2 *>(pfx));
-                rfe[k] = (lane == 31) ? __ldg(pfx + 2) : 0.0;
-                rfy[k] = __ldg(reinterpret_cast<const double2 *>(pfy));
+                if (load_aux) rb[k] = __ldg(reinterpret_cast<const double2 *>(pb));
+                if constexpr (FACES) {
+                    rfx[k] = __ldg(reinterpret_cast<const double2 *>(pfx));
+                    rfe[k] = (lane == 31) ? __ldg(pfx + 2) : 0.0;
+                    rfy[k] = __ldg(reinterpret_cast<const double2 *>(pfy));
+                }
                 pb += rstep;
                 pfx += rstep;
                 pfy += rstep;
@@ -411,6 +465,7 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
     SW_TADD(5, 0, 1);
 }
 
+template <int MODE, bool FACES>
 __global__ void __launch_bounds__(v2::NW * 32, 2)
     k_sweep2v(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
               const __grid_constant__ CUtensorMap tmfx, const __grid_constant__ CUtensorMap tmfy, Sweep2vArgs A) {
@@ -422,30 +477,46 @@ __global__ void __launch_bounds__(v2::NW * 32, 2)
     const int64_t R0 = tx, R1 = ty + G.toff[1];
     const int sx = ((A.base >> 0) & 1) ^ (int)(R0 & 1);
     const int sy = ((A.base >> 1) & 1) ^ (int)(R1 & 1);
-    const bool cx = sx ? (R0 < G.ntg[0] - 1) : (R0 > 0);
-    const bool cy = sy ? (R1 < G.ntg[1] - 1) : (R1 > 0);
+    const bool cx = A.couple && (sx ? (R0 < G.ntg[0] - 1) : (R0 > 0));
+    const bool cy = A.couple && (sy ? (R1 < G.ntg[1] - 1) : (R1 > 0));
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
         mbar_expect_tx(&bar, (uint32_t)(sizeof(double) * v2::WS));
         tma_load_2d(sm, &tmx, tx * v2::T, ty * v2::T, &bar);
-        tma_prefetch_2d(&tmb, tx * v2::T + 2, ty * v2::T + 2);
-        tma_prefetch_2d(&tmfx, tx * v2::T + 2, ty * v2::T + 2);
-        tma_prefetch_2d(&tmfy, tx * v2::T + 2, ty * v2::T + 2);
+        if (MODE == MODE_SOR || A.invd_mode) tma_prefetch_2d(&tmb, tx * v2::T + 2, ty * v2::T + 2);
+        if (FACES) {
+            tma_prefetch_2d(&tmfx, tx * v2::T + 2, ty * v2::T + 2);
+            tma_prefetch_2d(&tmfy, tx * v2::T + 2, ty * v2::T + 2);
+        }
     }
     __syncthreads();
     switch (sx | (sy << 1)) {
-        case 0: sweep2v_tile<0, 0>(A, sm, &bar, tx, ty, cx, cy); break;
-        case 1: sweep2v_tile<1, 0>(A, sm, &bar, tx, ty, cx, cy); break;
-        case 2: sweep2v_tile<0, 1>(A, sm, &bar, tx, ty, cx, cy); break;
-        default: sweep2v_tile<1, 1>(A, sm, &bar, tx, ty, cx, cy); break;
+        case 0: sweep2v_tile<MODE, FACES, 0, 0>(A, sm, &bar, tx, ty, cx, cy); break;
+        case 1: sweep2v_tile<MODE, FACES, 1, 0>(A, sm, &bar, tx, ty, cx, cy); break;
+        case 2: sweep2v_tile<MODE, FACES, 0, 1>(A, sm, &bar, tx, ty, cx, cy); break;
+        default: sweep2v_tile<MODE, FACES, 1, 1>(A, sm, &bar, tx, ty, cx, cy); break;
     }
+}
+
+template <int MODE, bool FACES>
+inline cudaError_t launch_k2v(const CUtensorMap &tmx, const CUtensorMap &tmb, const CUtensorMap &tmfx,
+                              const CUtensorMap &tmfy, const Sweep2vArgs &A, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sweep2v<MODE, FACES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2::SMEM);
+        cudaFuncSetAttribute(k_sweep2v<MODE, FACES>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1]);
+    k_sweep2v<MODE, FACES><<<tiles, v2::NW * 32, v2::SMEM, s>>>(tmx, tmb, tmfx, tmfy, A);
+    return cudaGetLastError();
 }
 
 inline cudaError_t launch_sweep2v(const CUtensorMap &tmx, const CUtensorMap &tmb, const CUtensorMap &tmfx,
                                   const CUtensorMap &tmfy, const Geo &G, int base, const double *w8, const double *b,
                                   const double *fx, const double *fy, double *xn, int *flag, cudaStream_t s) {
-    Sweep2vArgs A;
+    Sweep2vArgs A{};
     A.G = G;
     A.base = base;
     for (int i = 0; i < 4; ++i) A.omega[i] = w8[i];
@@ -454,15 +525,32 @@ inline cudaError_t launch_sweep2v(const CUtensorMap &tmx, const CUtensorMap &tmb
     A.fy = fy;
     A.xnew = xn;
     A.flag = flag;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_sweep2v, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2::SMEM);
-        cudaFuncSetAttribute(k_sweep2v, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
-    }
-    const unsigned tiles = (unsigned)((int64_t)G.nt[0] * G.nt[1]);
-    k_sweep2v<<<tiles, v2::NW * 32, v2::SMEM, s>>>(tmx, tmb, tmfx, tmfy, A);
-    return cudaGetLastError();
+    A.couple = 1;
+    return launch_k2v<MODE_SOR, true>(tmx, tmb, tmfx, tmfy, A, s);
+}
+
+// One block-triangular solve out = (D/alpha + A_I)^-1 r0 over the 64 x 64 boxes at corner bits
+// `base` (see MODE_TRI above).  tsrc: 68 x 68 window map of src; taux: 64 x 64 map of 1/D~
+// (ILU) for the L2 prefetch; faces may be null (unit coefficients).
+inline cudaError_t launch_tri2v(const CUtensorMap &tsrc, const CUtensorMap &taux, const CUtensorMap &tmfx,
+                                const CUtensorMap &tmfy, const Geo &G, int base, double omega, const double *invd,
+                                const double *fx, const double *fy, bool rscale, double coef, bool couple, double *out,
+                                int *flag, cudaStream_t s) {
+    Sweep2vArgs A{};
+    A.G = G;
+    A.base = base;
+    for (int i = 0; i < 4; ++i) A.omega[i] = omega;
+    A.b = invd;
+    A.fx = fx;
+    A.fy = fy;
+    A.xnew = out;
+    A.flag = flag;
+    A.coef = coef;
+    A.invd_mode = invd != nullptr;
+    A.rscale = rscale;
+    A.couple = couple;
+    if (fx) return launch_k2v<MODE_TRI, true>(tsrc, taux, tmfx, tmfy, A, s);
+    return launch_k2v<MODE_TRI, false>(tsrc, taux, tmfx, tmfy, A, s);
 }
 
 }  // namespace sw

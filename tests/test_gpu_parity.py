@@ -93,15 +93,18 @@ def test_faces_from_k_matches_oracle(gpu_lib):
         assert np.array_equal(g.get_vector(gpu_lib.X), O.sweep(pb, [1.1], x0, b, phase=0))
 
 
-TRI_CASES = [((64, 64), (16, 16)), ((96, 64), (32, 16)), ((256, 256), (64, 64)), ((16, 16, 16), (8, 8, 8)),
-             ((20, 12, 8), (10, 4, 4)), ((200,), (40,))]
+TRI_CASES = [((64, 64), (16, 16), True, 0.0), ((96, 64), (32, 16), True, 0.0), ((256, 256), (64, 64), True, 0.0),
+             ((16, 16, 16), (8, 8, 8), True, 0.0), ((20, 12, 8), (10, 4, 4), True, 0.0), ((200,), (40,), True, 0.0),
+             # 64 x 64 boxes: the fast 2D engine (unit and variable coefficients, beta, one box, strips)
+             ((192, 128), (64, 64), False, 0.0), ((128, 320), (64, 64), True, 0.3), ((64, 64), (64, 64), True, 0.0),
+             ((320, 64), (64, 64), False, 0.1), ((64, 256), (64, 64), True, 0.0)]
 
 
-@pytest.mark.parametrize("n,tile", TRI_CASES)
-def test_ilu_and_ssor_apply_match_oracle(gpu_lib, n, tile):
-    faces = rand_faces(n, 17)
-    pb = O.tiled(n, tile, faces=faces)
-    g = make_grid(gpu_lib, n, tile, faces)
+@pytest.mark.parametrize("n,tile,var,beta", TRI_CASES)
+def test_ilu_and_ssor_apply_match_oracle(gpu_lib, n, tile, var, beta):
+    faces = rand_faces(n, 17) if var else None
+    pb = O.tiled(n, tile, faces=faces, beta=beta)
+    g = make_grid(gpu_lib, n, tile, faces, beta)
     r = gen.uniform_field(5, gen.STREAM_TEST, pb.shape)
     g.ilu0_factor(0)
     inv = O.ilu0_factor(pb, phase=0)
@@ -124,7 +127,8 @@ def test_ilu_and_ssor_apply_match_oracle(gpu_lib, n, tile):
 
 @pytest.mark.parametrize("n,tile,var,pc", [((64, 64), (16, 16), False, 2), ((256, 256), (64, 64), False, 2),
                                            ((256, 256), (64, 64), True, 2), ((128, 128), (32, 32), True, 1),
-                                           ((16, 16, 16), (8, 8, 8), True, 2), ((128, 64), (32, 32), False, 0)])
+                                           ((16, 16, 16), (8, 8, 8), True, 2), ((128, 64), (32, 32), False, 0),
+                                           ((192, 256), (64, 64), True, 1), ((256, 128), (64, 64), False, 1)])
 def test_pcg_iterations_match_oracle(gpu_lib, n, tile, var, pc):
     faces = None
     if var:
