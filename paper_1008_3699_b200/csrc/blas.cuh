@@ -148,6 +148,152 @@ __global__ void k_dot(Geo G, const double *a, const double *b, DD *partial) {
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
+// ---------------------------------------------------------------------------------------
+// Row-segment kernels (the PCG hot path): a work item is a segment of up to 2*RSEG interior
+// nodes of one grid row (x fastest); thread i of the CTA handles nodes i and i + RSEG of the
+// segment, so every access is a fully coalesced row run and no thread divides by the row
+// length.  CTAs stride over items in a fixed order and write one double-double partial each,
+// so every reduction is deterministic for a given launch shape.
+constexpr int RSEG = RED_THREADS;               // double2 per item and CTA
+
+struct Rows {
+    int64_t n0, n1, rows, segs, items;          // interior row length, rows, segments per row
+    int64_t P0, P01, origin;
+};
+
+__host__ __device__ inline Rows make_rows(const Geo &G) {
+    Rows R;
+    R.n0 = G.n[0];
+    R.n1 = G.n[1];
+    R.rows = G.n[1] * G.n[2];
+    R.segs = (G.n[0] + 2 * RSEG - 1) / (2 * RSEG);
+    R.items = R.rows * R.segs;
+    R.P0 = G.P0;
+    R.P01 = G.P01;
+    R.origin = G.origin;
+    return R;
+}
+
+// padded index of (x, row)
+__device__ inline int64_t row_base(const Rows &R, int64_t row) {
+    const int64_t y = row % R.n1, z = row / R.n1;
+    return R.origin + y * R.P0 + z * R.P01;
+}
+
+// (A x)_p as in the oracle: s = a_P x_p, then s = fma(-c, x_q, s) over x-, x+, y-, y+, z-, z+
+template <int DIM, bool FACES>
+__device__ __forceinline__ double apply_A_fast(const double *__restrict__ F0, const double *__restrict__ F1,
+                                               const double *__restrict__ F2, const double *__restrict__ x,
+                                               int64_t i, int64_t P0, int64_t P01, double beta) {
+    double c0 = 1.0, c1 = 1.0, c2 = 1.0, c3 = 1.0, c4 = 1.0, c5 = 1.0;
+    if (FACES) {
+        c0 = F0[i]; c1 = F0[i + 1];
+        if (DIM > 1) { c2 = F1[i]; c3 = F1[i + P0]; }
+        if (DIM > 2) { c4 = F2[i]; c5 = F2[i + P01]; }
+    }
+    double ap = c0 + c1;
+    if (DIM > 1) ap = ap + (c2 + c3);
+    if (DIM > 2) ap = ap + (c4 + c5);
+    ap = ap + beta;
+    double s = ap * x[i];
+    s = fma(-c0, x[i - 1], s);
+    s = fma(-c1, x[i + 1], s);
+    if (DIM > 1) {
+        s = fma(-c2, x[i - P0], s);
+        s = fma(-c3, x[i + P0], s);
+    }
+    if (DIM > 2) {
+        s = fma(-c4, x[i - P01], s);
+        s = fma(-c5, x[i + P01], s);
+    }
+    return s;
+}
+
+// q = A p ; partial[blk] = sum p.q
+template <int DIM, bool FACES>
+__global__ void __launch_bounds__(RED_THREADS) k_spmv_dot_r(Rows R, double beta, const double *__restrict__ F0,
+                                                            const double *__restrict__ F1,
+                                                            const double *__restrict__ F2,
+                                                            const double *__restrict__ p, double *__restrict__ q,
+                                                            DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    DD acc = {0.0, 0.0};
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t b = row_base(R, row);
+        for (int h = 0; h < 2; ++h) {
+            const int64_t x = xb + h * RSEG;
+            if (x < R.n0) {
+                const int64_t i = b + x;
+                const double v = apply_A_fast<DIM, FACES>(F0, F1, F2, p, i, R.P0, R.P01, beta);
+                q[i] = v;
+                dd_add_prod(acc, p[i], v);
+            }
+        }
+    }
+    DD sm = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm;
+}
+
+// partial[blk] = sum a.b
+__global__ void __launch_bounds__(RED_THREADS) k_dot_r(Rows R, const double *__restrict__ a,
+                                                       const double *__restrict__ b, DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    DD acc = {0.0, 0.0};
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h)
+            if (xb + h * RSEG < R.n0) dd_add_prod(acc, a[base + xb + h * RSEG], b[base + xb + h * RSEG]);
+    }
+    DD sm = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm;
+}
+
+// x = fma(alpha, p, x) ; r = fma(-alpha, q, r) ; partial = sum r.r
+__global__ void __launch_bounds__(RED_THREADS) k_axpy2_dot_r(Rows R, const double *alpha_dev, double *__restrict__ x,
+                                                             double *__restrict__ r, const double *__restrict__ p,
+                                                             const double *__restrict__ q, DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    const double al = *alpha_dev;
+    DD acc = {0.0, 0.0};
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h) {
+            if (xb + h * RSEG < R.n0) {
+                const int64_t i = base + xb + h * RSEG;
+                x[i] = fma(al, p[i], x[i]);
+                const double rv = fma(-al, q[i], r[i]);
+                r[i] = rv;
+                dd_add_prod(acc, rv, rv);
+            }
+        }
+    }
+    DD sm = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm;
+}
+
+// p = fma(beta, p, z)   (first: p = z)
+__global__ void __launch_bounds__(RED_THREADS) k_pupdate_r(Rows R, const double *beta_dev, int first,
+                                                           const double *__restrict__ z, double *__restrict__ p) {
+    const double be = first ? 0.0 : *beta_dev;
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h) {
+            if (xb + h * RSEG < R.n0) {
+                const int64_t i = base + xb + h * RSEG;
+                p[i] = first ? z[i] : fma(be, p[i], z[i]);
+            }
+        }
+    }
+}
+
 // PCG scalars kept on the device
 struct CgScalars {
     double rz, pq, alpha, beta, rr, bb, rz_new;

@@ -5,6 +5,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -15,6 +17,7 @@
 #include "sweep2p.cuh"
 #include "sweep2v.cuh"
 #include "tri2t.cuh"
+#include "sweep3.cuh"
 
 using namespace sw;
 
@@ -62,7 +65,7 @@ struct sw_grid {
         int box;
         CUtensorMap map;
     };
-    std::vector<MapEntry> mapcache;   // TMA descriptors of arrays used as solve inputs
+    std::deque<MapEntry> mapcache;    // TMA descriptors of arrays used as solve inputs (stable references)
 };
 
 // TMA descriptor (box x box window at the padded origin) of a padded array, cached by pointer
@@ -72,8 +75,10 @@ static const CUtensorMap *get_map(sw_grid *g, const double *ptr, int box) {
     sw_grid::MapEntry e;
     e.ptr = ptr;
     e.box = box;
-    if (!encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box)) return nullptr;
-    if (g->mapcache.size() > 32) g->mapcache.erase(g->mapcache.begin());
+    const bool ok = (g->dim == 3) ? encode_3d(&e.map, ptr, g->pad, g->tile[0] + 4, g->tile[1] + 4, g->tile[2] + 4)
+                                  : encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box);
+    if (!ok) return nullptr;
+    if (g->mapcache.size() > 32) g->mapcache.pop_front();   // never one of the (<= 3) maps of the current call
     g->mapcache.push_back(e);
     return &g->mapcache.back().map;
 }
@@ -428,6 +433,23 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
                                            g->B, g->F[0], g->F[1], xn, g->flag, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2v launch: ") + cudaGetErrorString(e));
+        } else if (g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
+            const CUtensorMap *mx = get_map(g, xo, 0);
+            if (!mx) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+            Sweep3Args A3{};
+            A3.G = g->G;
+            A3.base = base;
+            for (int i = 0; i < 8; ++i) A3.omega[i] = w8[i];
+            A3.aux = g->B;
+            A3.f0 = g->G.poisson ? nullptr : g->F[0];
+            A3.f1 = g->G.poisson ? nullptr : g->F[1];
+            A3.f2 = g->G.poisson ? nullptr : g->F[2];
+            A3.out = xn;
+            A3.flag = g->flag;
+            A3.couple = 1;
+            cudaError_t e = launch_sweep3(*mx, A3, cs);
+            g->launches++;
+            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 2 && g->fast2d && g->maps.ok) {
             cudaError_t e = launch_sweep2d(g->maps, g->cur, g->G, base, w8, g->B, g->F, xn, g->flag, !g->G.poisson, cs);
             g->launches++;
@@ -545,6 +567,52 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     P.alpha_mode = ilu ? A_INVD : A_OMEGA_AP;
     P.invD = g->invD;
     for (int i = 0; i < 8; ++i) P.omega[i] = omega;
+    if (g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
+        // fast 3D path for the forward solves; the coupled-set phase of the SYMMETRIC backward
+        // stays on the generic kernel
+        const CUtensorMap *mr = get_map(g, r, 0), *my = get_map(g, g->Y, 0);
+        if (!mr || !my) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+        Sweep3Args A3{};
+        A3.G = g->G;
+        A3.base = base;
+        for (int i = 0; i < 8; ++i) A3.omega[i] = omega;
+        A3.aux = ilu ? g->invD : nullptr;
+        A3.f0 = g->G.poisson ? nullptr : g->F[0];
+        A3.f1 = g->G.poisson ? nullptr : g->F[1];
+        A3.f2 = g->G.poisson ? nullptr : g->F[2];
+        A3.flag = g->flag;
+        A3.tri = 1;
+        A3.invd_mode = ilu;
+        A3.rscale = 1;
+        A3.coef = 1.0;
+        A3.couple = 1;
+        A3.out = g->Y;
+        cudaError_t e = launch_sweep3(*mr, A3, s);
+        g->launches++;
+        if (e == cudaSuccess) {
+            A3.base = base ^ 7;
+            A3.rscale = 0;
+            A3.coef = ilu ? 1.0 : 2.0 - omega;
+            A3.couple = pairing == SW_PAIR_PAPER;
+            A3.out = z;
+            e = launch_sweep3(*my, A3, s);
+            g->launches++;
+        }
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
+        if (pairing == SW_PAIR_PAPER) return SW_OK;
+        if (getenv("SW_DEBUG_T1ONLY")) return SW_OK;
+        P.src = g->Y;
+        P.out = z;
+        P.rhs = R_COEF;
+        P.coef = ilu ? 1.0 : 2.0 - omega;
+        P.base = base;
+        for (int j = 1; j <= g->dim; ++j) {
+            P.mode = M_T2;
+            P.j = j;
+            if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+        }
+        return SW_OK;
+    }
     // forward: (D~ + L) y = r   (row-normalised: r0 = alpha r)
     P.mode = M_FWD;
     P.rhs = R_SCALE;
@@ -564,6 +632,7 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     // SYMMETRIC: (D~ + L^T) z = D~ y, non-coupled nodes first, then coupled sets by degree
     P.mode = M_T1;
     if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+    if (getenv("SW_DEBUG_T1ONLY")) return SW_OK;
     for (int j = 1; j <= g->dim; ++j) {
         P.mode = M_T2;
         P.j = j;
@@ -607,15 +676,29 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         if (pc == SW_PC_NONE) return SW_OK;
         return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, cs);
     };
+    // row-segment kernels, launch shape fixed per grid (deterministic reductions)
+    const Rows RW = make_rows(G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const bool fc = !G.poisson;
+    auto spmv = [&]() {
+        const double *F0 = g->F[0], *F1 = g->F[1], *F2 = g->F[2];
+        if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
+                            : k_spmv_dot_r<1, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        else if (g->dim == 2) fc ? k_spmv_dot_r<2, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
+                                 : k_spmv_dot_r<2, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        else fc ? k_spmv_dot_r<3, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
+                : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        g->launches++;
+    };
     // b.b
-    k_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->B, g->B, g->partial);
+    k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->B, g->B, g->partial);
     g->launches++;
-    if ((st = finish(g, nb, 1, 0, &g->cg->bb, cs)) != SW_OK) return st;
+    if ((st = finish(g, nr, 1, 0, &g->cg->bb, cs)) != SW_OK) return st;
     if ((st = apply_pc()) != SW_OK) return st;
-    k_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->R, z, g->partial);
+    k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->R, z, g->partial);
     g->launches++;
-    if ((st = finish(g, nb, 1, 0, &g->cg->rz, cs)) != SW_OK) return st;
-    k_pupdate<<<nb, RED_THREADS, 0, cs>>>(G, g->cg, 1, z, g->Pv);
+    if ((st = finish(g, nr, 1, 0, &g->cg->rz, cs)) != SW_OK) return st;
+    k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 1, z, g->Pv);
     g->launches++;
     CgScalars h;
     CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
@@ -625,14 +708,13 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     *relres_out = 1.0;
     if (bnorm == 0.0) { *relres_out = 0.0; return SW_OK; }
     for (int it = 1; it <= maxit; ++it) {
-        k_spmv_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->F[0], g->F[1], g->F[2], g->Pv, g->Q, g->partial);
-        g->launches++;
-        if ((st = finish(g, nb, 1, 0, &g->cg->pq, cs)) != SW_OK) return st;
+        spmv();
+        if ((st = finish(g, nr, 1, 0, &g->cg->pq, cs)) != SW_OK) return st;
         k_cg_alpha<<<1, 1, 0, cs>>>(g->cg);
         g->launches++;
-        k_axpy2_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->cg, x, g->R, g->Pv, g->Q, g->partial);
+        k_axpy2_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->alpha, x, g->R, g->Pv, g->Q, g->partial);
         g->launches++;
-        if ((st = finish(g, nb, 1, 0, &g->cg->rr, cs)) != SW_OK) return st;
+        if ((st = finish(g, nr, 1, 0, &g->cg->rr, cs)) != SW_OK) return st;
         CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
         CK(cudaStreamSynchronize(cs));
         *iters_out = it;
@@ -640,12 +722,12 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         if (*relres_out < rtol) return sw_check_status(g, s);
         if (!(h.rr == h.rr)) return fail(SW_ENOCONV, "PCG produced NaN");
         if ((st = apply_pc()) != SW_OK) return st;
-        k_dot<<<nb, RED_THREADS, 0, cs>>>(G, g->R, z, g->partial);
+        k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->R, z, g->partial);
         g->launches++;
-        if ((st = finish(g, nb, 1, 0, &g->cg->rz_new, cs)) != SW_OK) return st;
+        if ((st = finish(g, nr, 1, 0, &g->cg->rz_new, cs)) != SW_OK) return st;
         k_cg_beta<<<1, 1, 0, cs>>>(g->cg);
         g->launches++;
-        k_pupdate<<<nb, RED_THREADS, 0, cs>>>(G, g->cg, 0, z, g->Pv);
+        k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 0, z, g->Pv);
         g->launches++;
         CK(cudaGetLastError());
     }
@@ -673,6 +755,18 @@ extern "C" int sw_debug_phase_times(unsigned long long out[16]) {
     return 16;
 #else
     (void)out;
+    return 0;
+#endif
+}
+
+// Tuning aid (not part of sweep.h): window of one 3D box after the set phase (SW_DEBUG3 builds).
+extern "C" int sw_debug3(int block, double *out, int n) {
+#ifdef SW_DEBUG3
+    if (block >= -1) cudaMemcpyToSymbol(sw_dbg3_block, &block, sizeof(int));
+    if (out) cudaMemcpyFromSymbol(out, sw_dbg3, sizeof(double) * (size_t)n);
+    return 1;
+#else
+    (void)block; (void)out; (void)n;
     return 0;
 #endif
 }

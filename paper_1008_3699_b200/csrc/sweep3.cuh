@@ -1,0 +1,328 @@
+// sweep3.cuh -- 3D decomposed SOR sweep and block-triangular solves (7-point stencil), any box
+// T0 x T1 x T2 whose window fits in shared memory, sm_100a.
+//
+// One CTA (4 warps) per box.  Shared memory holds four arrays over the (T+4)^3 window (global
+// orientation): X (x_old / src, then r0, then the results, in place) and C0, C1, C2, the coupling
+// alpha c of every active node toward its implicit side along x, y, z.  Active nodes are the
+// box's own nodes and the partner layers across its coupled start faces (the other members of
+// the coupled 2x2 / 4x4 / 8x8 systems), recomputed redundantly by both boxes.
+//  1. Stage-in: one 3D TMA load of the window of x_old (SOR) or src (triangular solves).
+//  2. Prologue (all warps): r0 and the three couplings of every active node (DESIGN R-7), one
+//     branch-free correctly rounded division per node.
+//  3. Sets of two or more coupled faces (thread 0 the corner, then one thread per edge chain):
+//     Gaussian elimination without pivoting in ascending global index (DESIGN R-8).
+//  4. Level loop (warp 0): at level d every line (j, k) updates its node (d - j - k, j, k); a node
+//     on one coupled face solves its 2 x 2 pair with the partner layer.  __syncwarp per level.
+//  5. Write-back of the box.
+// Same operations and order as the oracle, so the result is bitwise identical to it.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "sweep2p.cuh"
+#include "tma.cuh"
+
+namespace sw {
+
+namespace k3 {
+constexpr int NT = 128;        // threads per CTA
+constexpr int KMAX = 16;       // prologue nodes per thread: (T0+1)(T1+1)(T2+1) <= NT * KMAX
+constexpr int MAXLINES = 64;   // T1 * T2
+}  // namespace k3
+
+struct Sweep3Args {
+    Geo G;
+    int base;
+    double omega[8];
+    const double *aux;          // b (SOR) or 1/D~ (ILU) or null
+    const double *f0, *f1, *f2; // face arrays or null (unit)
+    double *out;
+    int *flag;
+    double coef;
+    int tri, invd_mode, rscale, couple;
+};
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Solve one coupled set on the axes AXES (K = 2^popcount members) whose own member sits at
+// window word w.  Member S (bit t set = across the t-th set axis) is w - sum_t st[ax_t]; in
+// ascending global index its rank is S ^ m, m_t = (s_{ax_t} == 0), so the system is built
+// directly in rank space with compile-time indices.  Row of member S:
+//   u_S - sum_t C_{ax_t}(S) u_{S ^ (1<<t)} = r0_S + sum_{b not in AXES, axis order} C_b(S) u(S - st_b).
+template <int AXES>
+__device__ __forceinline__ void solve_set3(double *X, double *const C[3], int w, const int st[3], int sbits,
+                                           int *flag) {
+    constexpr int NA = ((AXES >> 0) & 1) + ((AXES >> 1) & 1) + ((AXES >> 2) & 1);
+    constexpr int K = 1 << NA;
+    constexpr int A0 = (AXES & 1) ? 0 : ((AXES & 2) ? 1 : 2);
+    constexpr int A1 = (NA < 2) ? -1 : ((AXES & 1) ? ((AXES & 2) ? 1 : 2) : 2);
+    constexpr int A2 = (NA < 3) ? -1 : 2;
+    constexpr int AX[3] = {A0, A1, A2};
+    int m = 0;
+#pragma unroll
+    for (int t = 0; t < NA; ++t) m |= (((sbits >> AX[t]) & 1) == 0) << t;
+    double M[K][K], rhs[K], u[K];
+    int wi[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+        const int S = r ^ m;
+        int wS = w;
+#pragma unroll
+        for (int t = 0; t < NA; ++t)
+            if ((S >> t) & 1) wS -= st[AX[t]];
+        double acc = X[wS];
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            if (!((AXES >> b) & 1)) acc = fma(C[b][wS], X[wS - st[b]], acc);
+        rhs[r] = acc;
+        wi[r] = wS;
+#pragma unroll
+        for (int q = 0; q < K; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t = 0; t < NA; ++t) M[r][r ^ (1 << t)] = -C[AX[t]][wS];
+    }
+    ge_solve_k<K>(M, rhs, u, flag);
+#pragma unroll
+    for (int r = 0; r < K; ++r) X[wi[r]] = u[r];
+}
+
+#ifdef SW_DEBUG3
+__device__ double sw_dbg3[4 * 8192];
+__device__ int sw_dbg3_block = -1;
+#endif
+
+template <bool FACES>
+__global__ void __launch_bounds__(k3::NT, 2)
+    k_sweep3(const __grid_constant__ CUtensorMap tmx, Sweep3Args A) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ uint64_t bar;
+    const Geo &G = A.G;
+    const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
+    const int W0 = T0 + 4, W1 = T1 + 4, W2 = T2 + 4;
+    const int WS = W0 * W1 * W2;
+    double *X = sm;
+    double *C[3] = {sm + WS, sm + 2 * WS, sm + 3 * WS};
+    const int tid = threadIdx.x;
+    // box, direction bits, coupled start faces
+    const int tx = blockIdx.x % G.nt[0];
+    const int ty = (blockIdx.x / G.nt[0]) % G.nt[1];
+    const int tz = blockIdx.x / (G.nt[0] * G.nt[1]);
+    const int64_t R[3] = {tx, ty, tz + G.toff[2]};
+    int sb = 0, cb = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int s = ((A.base >> a) & 1) ^ (int)(R[a] & 1);
+        const bool c = A.couple && (s ? (R[a] < G.ntg[a] - 1) : (R[a] > 0));
+        sb |= s << a;
+        cb |= (int)c << a;
+    }
+    const int Tv[3] = {T0, T1, T2}, Sv[3] = {1, W0, W0 * W1};
+    int st[3];          // window step of local +a
+#pragma unroll
+    for (int a = 0; a < 3; ++a) st[a] = ((sb >> a) & 1) ? -Sv[a] : Sv[a];
+    auto wof = [&](int l0, int l1, int l2) {   // window word of local coordinates
+        const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - l0 : l0);
+        const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - l1 : l1);
+        const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - l2 : l2);
+        return w0 + W0 * (w1 + W1 * w2);
+    };
+    const int64_t P0 = G.P0, P01 = G.P01;
+    const int64_t gbase = (int64_t)tz * T2 * P01 + (int64_t)ty * T1 * P0 + (int64_t)tx * T0;   // padded index of window word 0
+
+    // ---------------------------------------------------------------- 1. stage-in
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&bar, (uint32_t)(sizeof(double) * WS));
+        tma_load_3d(X, &tmx, tx * T0, ty * T1, tz * T2, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+
+    // ---------------------------------------------------------------- 2. prologue
+    const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1, NE = E0 * E1 * E2;   // local [-1, T) per axis
+    double r0v[k3::KMAX];
+    int wv[k3::KMAX];
+#pragma unroll
+    for (int it = 0; it < k3::KMAX; ++it) {
+        const int e = tid + it * k3::NT;
+        wv[it] = -1;
+        if (e >= NE) continue;
+        const int l0 = e % E0 - 1, l1 = (e / E0) % E1 - 1, l2 = e / (E0 * E1) - 1;
+        int L = 0;
+        if (l0 < 0) L |= 1;
+        if (l1 < 0) L |= 2;
+        if (l2 < 0) L |= 4;
+        if ((L & cb) != L) continue;                      // not an active node
+        const int w = wof(l0, l1, l2);
+        const int64_t g = gbase + (w % W0) + (int64_t)((w / W0) % W1) * P0 + (int64_t)(w / (W0 * W1)) * P01;
+        double f[3][2] = {{1.0, 1.0}, {1.0, 1.0}, {1.0, 1.0}};
+        if (FACES) {
+            f[0][0] = A.f0[g]; f[0][1] = A.f0[g + 1];
+            f[1][0] = A.f1[g]; f[1][1] = A.f1[g + P0];
+            f[2][0] = A.f2[g]; f[2][1] = A.f2[g + P01];
+        }
+        const double ap = (((f[0][0] + f[0][1]) + (f[1][0] + f[1][1])) + (f[2][0] + f[2][1])) + G.beta;
+        const int db = sb ^ L;                             // direction bits of the node's box
+        double al, r0;
+        if (!A.tri) {
+            const double w_ = A.omega[db];
+            al = div_rn(w_, ap);
+            double ev = A.aux[g];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
+                const int wexp = hi ? w - Sv[a] : w + Sv[a];
+                ev = fma(hi ? f[a][0] : f[a][1], X[wexp], ev);
+            }
+            r0 = fma(al, ev, (1.0 - w_) * X[w]);
+        } else {
+            al = A.invd_mode ? A.aux[g] : div_rn(A.omega[0], ap);
+            r0 = A.rscale ? al * X[w] : A.coef * X[w];
+        }
+        const int lv[3] = {l0, l1, l2};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);
+            // no coupling across an uncoupled start face: the oracle omits the term (physical
+            // boundary) and the first pass of the transposed solve must not see the neighbour box
+            const bool cut = !((L >> a) & 1) && lv[a] == 0 && !((cb >> a) & 1);
+            C[a][w] = cut ? 0.0 : al * (hi ? f[a][1] : f[a][0]);
+        }
+        r0v[it] = r0;
+        wv[it] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < k3::KMAX; ++it)
+        if (wv[it] >= 0) X[wv[it]] = r0v[it];
+    __syncthreads();
+
+    // ---------------------------------------------------------------- 3. corner and edge sets
+    const int ncpl = __popc(cb);
+    if (ncpl >= 2) {
+        // one thread: the corner set, then the edge chains (a chain of 4-sets along axis c where
+        // the two other axes are coupled; its only outside dependency is the previous set)
+        if (tid == 0) {
+            const int w = wof(0, 0, 0);
+            switch (cb) {
+                case 7: solve_set3<7>(X, C, w, st, sb, A.flag); break;
+                case 3: solve_set3<3>(X, C, w, st, sb, A.flag); break;
+                case 5: solve_set3<5>(X, C, w, st, sb, A.flag); break;
+                default: solve_set3<6>(X, C, w, st, sb, A.flag); break;
+            }
+            if ((cb & 6) == 6)
+                for (int t = 1; t < T0; ++t) solve_set3<6>(X, C, wof(t, 0, 0), st, sb, A.flag);
+            if ((cb & 5) == 5)
+                for (int t = 1; t < T1; ++t) solve_set3<5>(X, C, wof(0, t, 0), st, sb, A.flag);
+            if ((cb & 3) == 3)
+                for (int t = 1; t < T2; ++t) solve_set3<3>(X, C, wof(0, 0, t), st, sb, A.flag);
+        }
+        __syncthreads();
+    }
+
+#ifdef SW_DEBUG3
+    if ((int)blockIdx.x == sw_dbg3_block)
+        for (int i = tid; i < WS; i += k3::NT) {
+            sw_dbg3[i] = X[i];
+            sw_dbg3[8192 + i] = C[0][i];
+        }
+#endif
+    // ---------------------------------------------------------------- 4. level loop (warp 0)
+    if (tid < 32) {
+        const int nl = T1 * T2, nlev = T0 + T1 + T2 - 2;
+        int fl = 0;
+        for (int d = 0; d < nlev; ++d) {
+            for (int ln = tid; ln < nl; ln += 32) {
+                const int j = ln % T1, k = ln / T1, i = d - j - k;
+                if (i < 0 || i >= T0) continue;
+                const int m = (i == 0 ? (cb & 1) : 0) | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
+                const int w = wof(i, j, k);
+                if (m == 0) {
+                    double acc = X[w];
+                    acc = fma(C[0][w], X[w - st[0]], acc);
+                    acc = fma(C[1][w], X[w - st[1]], acc);
+                    acc = fma(C[2][w], X[w - st[2]], acc);
+                    X[w] = acc;
+                } else if ((m & (m - 1)) == 0) {               // one coupled face: 2 x 2 pair
+                    const int a = __ffs(m) - 1;
+                    const int q = w - st[a];
+                    double rp = X[w], rq = X[q];
+#pragma unroll
+                    for (int b = 0; b < 3; ++b)
+                        if (b != a) {
+                            rp = fma(C[b][w], X[w - st[b]], rp);
+                            rq = fma(C[b][q], X[q - st[b]], rq);
+                        }
+                    const bool qfirst = ((sb >> a) & 1) == 0;   // partner has the lower global index
+                    const double ra = qfirst ? rq : rp, rb = qfirst ? rp : rq;
+                    const double mab = qfirst ? C[a][q] : C[a][w], mba = qfirst ? C[a][w] : C[a][q];
+                    const double m11 = fma(mba, -mab, 1.0);
+                    fl |= !(fabs(m11) >= 1e-14);
+                    const double ub = fma(mba, ra, rb) * div_rn(1.0, m11);
+                    const double ua = fma(mab, ub, ra) * 1.0;
+                    X[w] = qfirst ? ub : ua;
+                    X[q] = qfirst ? ua : ub;
+                }
+                // (sets on two or three faces were solved in step 3)
+            }
+            __syncwarp();
+        }
+        if (fl) atomicOr(A.flag, 1);
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------------- 5. write-back
+    const int nrow = T1 * T2;
+    for (int e = tid; e < nrow * T0; e += k3::NT) {
+        const int x = e % T0, row = e / T0;
+        const int w1 = 2 + row % T1, w2 = 2 + row / T1;
+        const int w = 2 + x + W0 * (w1 + W1 * w2);
+        A.out[gbase + 2 + x + (int64_t)w1 * P0 + (int64_t)w2 * P01] = X[w];
+    }
+}
+
+inline bool encode_3d(CUtensorMap *m, const double *base, const int64_t pad[3], int b0, int b1, int b2) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc || !base) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)pad[0], (cuuint64_t)pad[1], (cuuint64_t)pad[2]};
+    cuuint64_t strides[2] = {(cuuint64_t)(pad[0] * sizeof(double)), (cuuint64_t)(pad[0] * pad[1] * sizeof(double))};
+    cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+inline size_t sweep3_smem(const Geo &G) {
+    return sizeof(double) * 4 * (size_t)(G.T[0] + 4) * (G.T[1] + 4) * (G.T[2] + 4);
+}
+
+// the fast 3D path handles boxes whose window fits and whose extended box fits the prologue
+inline bool sweep3_supported(const Geo &G) {
+    if (G.dim != 3) return false;
+    const int64_t ne = (int64_t)(G.T[0] + 1) * (G.T[1] + 1) * (G.T[2] + 1);
+    return (G.T[0] % 2 == 0) && G.T[0] + 4 <= 256 && G.T[1] + 4 <= 256 && G.T[2] + 4 <= 256 &&
+           sweep3_smem(G) <= 227 * 1024 && ne <= (int64_t)k3::NT * k3::KMAX && G.T[1] * G.T[2] <= k3::MAXLINES &&
+           G.off[0] == 0 && G.off[1] == 0;
+}
+
+inline cudaError_t launch_sweep3(const CUtensorMap &tmx, const Sweep3Args &A, cudaStream_t s) {
+    const size_t smem = sweep3_smem(A.G);
+    const bool faces = A.f0 != nullptr;
+    if (faces) cudaFuncSetAttribute(k_sweep3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else cudaFuncSetAttribute(k_sweep3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1] * A.G.nt[2]);
+    if (faces) k_sweep3<true><<<tiles, k3::NT, smem, s>>>(tmx, A);
+    else k_sweep3<false><<<tiles, k3::NT, smem, s>>>(tmx, A);
+    return cudaGetLastError();
+}
+
+}  // namespace sw

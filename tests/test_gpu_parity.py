@@ -34,6 +34,10 @@ CASES = [
     ((32, 32, 32), (16, 8, 8), True, 0.0, [1.0]),                   # 3D, boxes long in x
     ((24, 16, 16), (8, 8, 8), False, 0.0, [1.3]),
     ((12, 12, 12), (4, 6, 3), True, 0.2, list(0.6 + 0.15 * np.arange(8))),
+    ((64, 32, 16), (32, 8, 4), True, 0.0, [1.0]),                   # 3D kernel, C5-shaped boxes
+    ((64, 16, 16), (32, 8, 4), False, 0.1, list(1.9 - 0.1 * np.arange(8))),   # Poisson, per-direction omega
+    ((32, 8, 4), (32, 8, 4), True, 0.0, [1.3]),                     # one box
+    ((15, 12, 12), (5, 4, 6), True, 0.0, [1.1]),                    # odd box edge: generic kernel
 ]
 
 
@@ -97,7 +101,9 @@ TRI_CASES = [((64, 64), (16, 16), True, 0.0), ((96, 64), (32, 16), True, 0.0), (
              ((16, 16, 16), (8, 8, 8), True, 0.0), ((20, 12, 8), (10, 4, 4), True, 0.0), ((200,), (40,), True, 0.0),
              # 64 x 64 boxes: the fast 2D engine (unit and variable coefficients, beta, one box, strips)
              ((192, 128), (64, 64), False, 0.0), ((128, 320), (64, 64), True, 0.3), ((64, 64), (64, 64), True, 0.0),
-             ((320, 64), (64, 64), False, 0.1), ((64, 256), (64, 64), True, 0.0)]
+             ((320, 64), (64, 64), False, 0.1), ((64, 256), (64, 64), True, 0.0),
+             # 3D kernel (forward solves; coupled-set phase of the transposed solve on the generic kernel)
+             ((64, 32, 16), (32, 8, 4), True, 0.0), ((32, 16, 8), (16, 8, 4), False, 0.2)]
 
 
 @pytest.mark.parametrize("n,tile,var,beta", TRI_CASES)

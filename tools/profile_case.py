@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--faces", action="store_true")
     ap.add_argument("--sweeps", type=int, default=4)
     ap.add_argument("--pcg", action="store_true")
+    ap.add_argument("--maxit", type=int, default=20000)
+    ap.add_argument("--pc", type=int, default=2, help="0 none, 1 SSOR, 2 ILU(0)")
     args = ap.parse_args()
     import torch
     d = args.dim
@@ -40,7 +42,7 @@ def main():
     g.set_vector(binding.B, b)
     if args.pcg:
         t = time.time()
-        it, rel, ok = g.pcg_solve(binding.PC_ILU0, 1.0, 0, 1e-8, 20000)
+        it, rel, ok = g.pcg_solve(args.pc, 1.0, 0, 1e-8, args.maxit)
         print("pcg", it, rel, ok, time.time() - t)
         return
     torch.cuda.synchronize()
