@@ -435,7 +435,10 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2v launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
             const CUtensorMap *mx = get_map(g, xo, 0);
-            if (!mx) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+            const CUtensorMap *m0 = g->G.poisson ? mx : get_map(g, g->F[0], 0);
+            const CUtensorMap *m1 = g->G.poisson ? mx : get_map(g, g->F[1], 0);
+            const CUtensorMap *m2 = g->G.poisson ? mx : get_map(g, g->F[2], 0);
+            if (!mx || !m0 || !m1 || !m2) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
             Sweep3Args A3{};
             A3.G = g->G;
             A3.base = base;
@@ -447,7 +450,7 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             A3.out = xn;
             A3.flag = g->flag;
             A3.couple = 1;
-            cudaError_t e = launch_sweep3(*mx, A3, cs);
+            cudaError_t e = launch_sweep3(*mx, *m0, *m1, *m2, A3, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 2 && g->fast2d && g->maps.ok) {
@@ -571,7 +574,10 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
         // fast 3D path for the forward solves; the coupled-set phase of the SYMMETRIC backward
         // stays on the generic kernel
         const CUtensorMap *mr = get_map(g, r, 0), *my = get_map(g, g->Y, 0);
-        if (!mr || !my) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+        const CUtensorMap *m0 = g->G.poisson ? mr : get_map(g, g->F[0], 0);
+        const CUtensorMap *m1 = g->G.poisson ? mr : get_map(g, g->F[1], 0);
+        const CUtensorMap *m2 = g->G.poisson ? mr : get_map(g, g->F[2], 0);
+        if (!mr || !my || !m0 || !m1 || !m2) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
         Sweep3Args A3{};
         A3.G = g->G;
         A3.base = base;
@@ -587,7 +593,7 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
         A3.coef = 1.0;
         A3.couple = 1;
         A3.out = g->Y;
-        cudaError_t e = launch_sweep3(*mr, A3, s);
+        cudaError_t e = launch_sweep3(*mr, *m0, *m1, *m2, A3, s);
         g->launches++;
         if (e == cudaSuccess) {
             A3.base = base ^ 7;
@@ -595,7 +601,7 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
             A3.coef = ilu ? 1.0 : 2.0 - omega;
             A3.couple = pairing == SW_PAIR_PAPER;
             A3.out = z;
-            e = launch_sweep3(*my, A3, s);
+            e = launch_sweep3(*my, *m0, *m1, *m2, A3, s);
             g->launches++;
         }
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));

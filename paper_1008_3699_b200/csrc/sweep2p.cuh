@@ -88,7 +88,7 @@ __device__ __forceinline__ void ge_solve_k(double (&M)[K][K], double (&rhs)[K], 
     for (int p = 0; p < K; ++p) {
         const double piv = M[p][p];
         if (!(fabs(piv) >= 1e-14)) atomicOr(flag, 1);
-        inv[p] = 1.0 / piv;
+        inv[p] = div_rn(1.0, piv);          // = 1.0 / piv (IEEE), without the slow-path call
 #pragma unroll
         for (int q = p + 1; q < K; ++q) {
             const double l = M[q][p] * inv[p];

@@ -25,8 +25,8 @@
 namespace sw {
 
 namespace k3 {
-constexpr int NT = 128;        // threads per CTA
-constexpr int KMAX = 16;       // prologue nodes per thread: (T0+1)(T1+1)(T2+1) <= NT * KMAX
+constexpr int NT = 256;        // threads per CTA
+constexpr int KMAX = 8;        // prologue nodes per thread: (T0+1)(T1+1)(T2+1) <= NT * KMAX
 constexpr int MAXLINES = 64;   // T1 * T2
 }  // namespace k3
 
@@ -99,7 +99,8 @@ __device__ int sw_dbg3_block = -1;
 
 template <bool FACES>
 __global__ void __launch_bounds__(k3::NT, 2)
-    k_sweep3(const __grid_constant__ CUtensorMap tmx, Sweep3Args A) {
+    k_sweep3(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tf0,
+             const __grid_constant__ CUtensorMap tf1, const __grid_constant__ CUtensorMap tf2, Sweep3Args A) {
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t bar;
     const Geo &G = A.G;
@@ -135,38 +136,58 @@ __global__ void __launch_bounds__(k3::NT, 2)
     const int64_t P0 = G.P0, P01 = G.P01;
     const int64_t gbase = (int64_t)tz * T2 * P01 + (int64_t)ty * T1 * P0 + (int64_t)tx * T0;   // padded index of window word 0
 
+    SW_TMARK(t_start);
     // ---------------------------------------------------------------- 1. stage-in
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
-        mbar_expect_tx(&bar, (uint32_t)(sizeof(double) * WS));
+        mbar_expect_tx(&bar, (uint32_t)(sizeof(double) * WS * (FACES ? 4 : 1)));
         tma_load_3d(X, &tmx, tx * T0, ty * T1, tz * T2, &bar);
+        if (FACES) {   // face windows land in the coupling arrays and are converted in place
+            tma_load_3d(C[0], &tf0, tx * T0, ty * T1, tz * T2, &bar);
+            tma_load_3d(C[1], &tf1, tx * T0, ty * T1, tz * T2, &bar);
+            tma_load_3d(C[2], &tf2, tx * T0, ty * T1, tz * T2, &bar);
+        }
     }
     __syncthreads();
     mbar_wait(&bar, 0);
+    SW_TMARK(t_staged);
 
     // ---------------------------------------------------------------- 2. prologue
     const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1, NE = E0 * E1 * E2;   // local [-1, T) per axis
-    double r0v[k3::KMAX];
+    // pass 1: every active node's r0 and couplings into registers (reads faces from the coupling
+    // arrays and x_old from the window); pass 2, after a barrier: write them in place
+    double r0v[k3::KMAX], cv[k3::KMAX][3];
     int wv[k3::KMAX];
+    double auxv[k3::KMAX];
 #pragma unroll
-    for (int it = 0; it < k3::KMAX; ++it) {
+    for (int it = 0; it < k3::KMAX; ++it) {     // aux loads first (coalesced along x)
         const int e = tid + it * k3::NT;
+        auxv[it] = 0.0;
         wv[it] = -1;
         if (e >= NE) continue;
         const int l0 = e % E0 - 1, l1 = (e / E0) % E1 - 1, l2 = e / (E0 * E1) - 1;
-        int L = 0;
-        if (l0 < 0) L |= 1;
-        if (l1 < 0) L |= 2;
-        if (l2 < 0) L |= 4;
+        const int L = (l0 < 0 ? 1 : 0) | (l1 < 0 ? 2 : 0) | (l2 < 0 ? 4 : 0);
         if ((L & cb) != L) continue;                      // not an active node
         const int w = wof(l0, l1, l2);
-        const int64_t g = gbase + (w % W0) + (int64_t)((w / W0) % W1) * P0 + (int64_t)(w / (W0 * W1)) * P01;
-        double f[3][2] = {{1.0, 1.0}, {1.0, 1.0}, {1.0, 1.0}};
-        if (FACES) {
-            f[0][0] = A.f0[g]; f[0][1] = A.f0[g + 1];
-            f[1][0] = A.f1[g]; f[1][1] = A.f1[g + P0];
-            f[2][0] = A.f2[g]; f[2][1] = A.f2[g + P01];
+        wv[it] = w;
+        if (!A.tri || A.invd_mode) {
+            const int64_t g = gbase + (w % W0) + (int64_t)((w / W0) % W1) * P0 + (int64_t)(w / (W0 * W1)) * P01;
+            auxv[it] = A.aux[g];
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < k3::KMAX; ++it) {
+        const int w = wv[it];
+        if (w < 0) continue;
+        const int e = tid + it * k3::NT;
+        const int lv[3] = {e % E0 - 1, (e / E0) % E1 - 1, e / (E0 * E1) - 1};
+        const int L = (lv[0] < 0 ? 1 : 0) | (lv[1] < 0 ? 2 : 0) | (lv[2] < 0 ? 4 : 0);
+        double f[3][2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            f[a][0] = FACES ? C[a][w] : 1.0;
+            f[a][1] = FACES ? C[a][w + Sv[a]] : 1.0;
         }
         const double ap = (((f[0][0] + f[0][1]) + (f[1][0] + f[1][1])) + (f[2][0] + f[2][1])) + G.beta;
         const int db = sb ^ L;                             // direction bits of the node's box
@@ -174,36 +195,38 @@ __global__ void __launch_bounds__(k3::NT, 2)
         if (!A.tri) {
             const double w_ = A.omega[db];
             al = div_rn(w_, ap);
-            double ev = A.aux[g];
+            double ev = auxv[it];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
-                const int wexp = hi ? w - Sv[a] : w + Sv[a];
-                ev = fma(hi ? f[a][0] : f[a][1], X[wexp], ev);
+                ev = fma(hi ? f[a][0] : f[a][1], X[hi ? w - Sv[a] : w + Sv[a]], ev);
             }
             r0 = fma(al, ev, (1.0 - w_) * X[w]);
         } else {
-            al = A.invd_mode ? A.aux[g] : div_rn(A.omega[0], ap);
+            al = A.invd_mode ? auxv[it] : div_rn(A.omega[0], ap);
             r0 = A.rscale ? al * X[w] : A.coef * X[w];
         }
-        const int lv[3] = {l0, l1, l2};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);
             // no coupling across an uncoupled start face: the oracle omits the term (physical
             // boundary) and the first pass of the transposed solve must not see the neighbour box
             const bool cut = !((L >> a) & 1) && lv[a] == 0 && !((cb >> a) & 1);
-            C[a][w] = cut ? 0.0 : al * (hi ? f[a][1] : f[a][0]);
+            cv[it][a] = cut ? 0.0 : al * (hi ? f[a][1] : f[a][0]);
         }
         r0v[it] = r0;
-        wv[it] = w;
     }
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < k3::KMAX; ++it)
-        if (wv[it] >= 0) X[wv[it]] = r0v[it];
+        if (wv[it] >= 0) {
+            X[wv[it]] = r0v[it];
+            C[0][wv[it]] = cv[it][0];
+            C[1][wv[it]] = cv[it][1];
+            C[2][wv[it]] = cv[it][2];
+        }
     __syncthreads();
-
+    SW_TMARK(t_prologue);
     // ---------------------------------------------------------------- 3. corner and edge sets
     const int ncpl = __popc(cb);
     if (ncpl >= 2) {
@@ -217,13 +240,15 @@ __global__ void __launch_bounds__(k3::NT, 2)
                 case 5: solve_set3<5>(X, C, w, st, sb, A.flag); break;
                 default: solve_set3<6>(X, C, w, st, sb, A.flag); break;
             }
-            if ((cb & 6) == 6)
-                for (int t = 1; t < T0; ++t) solve_set3<6>(X, C, wof(t, 0, 0), st, sb, A.flag);
-            if ((cb & 5) == 5)
-                for (int t = 1; t < T1; ++t) solve_set3<5>(X, C, wof(0, t, 0), st, sb, A.flag);
-            if ((cb & 3) == 3)
-                for (int t = 1; t < T2; ++t) solve_set3<3>(X, C, wof(0, 0, t), st, sb, A.flag);
         }
+        __syncthreads();
+        // the edge chains (independent of each other), one per warp
+        if (tid == 0 && (cb & 6) == 6)
+            for (int t = 1; t < T0; ++t) solve_set3<6>(X, C, wof(t, 0, 0), st, sb, A.flag);
+        if (tid == 32 && (cb & 5) == 5)
+            for (int t = 1; t < T1; ++t) solve_set3<5>(X, C, wof(0, t, 0), st, sb, A.flag);
+        if (tid == 64 && (cb & 3) == 3)
+            for (int t = 1; t < T2; ++t) solve_set3<3>(X, C, wof(0, 0, t), st, sb, A.flag);
         __syncthreads();
     }
 
@@ -234,16 +259,30 @@ __global__ void __launch_bounds__(k3::NT, 2)
             sw_dbg3[8192 + i] = C[0][i];
         }
 #endif
+    SW_TMARK(t_sets);
     // ---------------------------------------------------------------- 4. level loop (warp 0)
     if (tid < 32) {
         const int nl = T1 * T2, nlev = T0 + T1 + T2 - 2;
+        // per-lane lines (at most two): offset j + k of the level, window word of node i = 0,
+        // coupled-face mask of the line (y-face if j == 0, z-face if k == 0)
+        int jk[2], wl[2], lm[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int ln = tid + 32 * h;
+            const int j = ln % T1, k = ln / T1;
+            jk[h] = (ln < nl) ? j + k : (1 << 20);          // never active
+            wl[h] = wof(0, ln < nl ? j : 0, ln < nl ? k : 0);
+            lm[h] = (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
+        }
+        const int s0 = st[0];
         int fl = 0;
         for (int d = 0; d < nlev; ++d) {
-            for (int ln = tid; ln < nl; ln += 32) {
-                const int j = ln % T1, k = ln / T1, i = d - j - k;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = d - jk[h];
                 if (i < 0 || i >= T0) continue;
-                const int m = (i == 0 ? (cb & 1) : 0) | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
-                const int w = wof(i, j, k);
+                const int m = (i == 0 ? (cb & 1) : 0) | lm[h];
+                const int w = wl[h] + i * s0;
                 if (m == 0) {
                     double acc = X[w];
                     acc = fma(C[0][w], X[w - st[0]], acc);
@@ -277,6 +316,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
         if (fl) atomicOr(A.flag, 1);
     }
     __syncthreads();
+    SW_TMARK(t_levels);
 
     // ---------------------------------------------------------------- 5. write-back
     const int nrow = T1 * T2;
@@ -286,6 +326,13 @@ __global__ void __launch_bounds__(k3::NT, 2)
         const int w = 2 + x + W0 * (w1 + W1 * w2);
         A.out[gbase + 2 + x + (int64_t)w1 * P0 + (int64_t)w2 * P01] = X[w];
     }
+    SW_TMARK(t_end);
+    SW_TADD(0, t_start, t_staged);
+    SW_TADD(1, t_staged, t_prologue);
+    SW_TADD(2, t_prologue, t_sets);
+    SW_TADD(3, t_sets, t_levels);
+    SW_TADD(4, t_levels, t_end);
+    SW_TADD(5, 0, 1);
 }
 
 inline bool encode_3d(CUtensorMap *m, const double *base, const int64_t pad[3], int b0, int b1, int b2) {
@@ -314,14 +361,15 @@ inline bool sweep3_supported(const Geo &G) {
            G.off[0] == 0 && G.off[1] == 0;
 }
 
-inline cudaError_t launch_sweep3(const CUtensorMap &tmx, const Sweep3Args &A, cudaStream_t s) {
+inline cudaError_t launch_sweep3(const CUtensorMap &tmx, const CUtensorMap &tf0, const CUtensorMap &tf1,
+                                 const CUtensorMap &tf2, const Sweep3Args &A, cudaStream_t s) {
     const size_t smem = sweep3_smem(A.G);
     const bool faces = A.f0 != nullptr;
     if (faces) cudaFuncSetAttribute(k_sweep3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     else cudaFuncSetAttribute(k_sweep3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1] * A.G.nt[2]);
-    if (faces) k_sweep3<true><<<tiles, k3::NT, smem, s>>>(tmx, A);
-    else k_sweep3<false><<<tiles, k3::NT, smem, s>>>(tmx, A);
+    if (faces) k_sweep3<true><<<tiles, k3::NT, smem, s>>>(tmx, tf0, tf1, tf2, A);
+    else k_sweep3<false><<<tiles, k3::NT, smem, s>>>(tmx, tf0, tf1, tf2, A);
     return cudaGetLastError();
 }
 

@@ -15,13 +15,17 @@ def main():
     import torch
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
     faces = len(sys.argv) > 2 and sys.argv[2] == "faces"
+    dim = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    tile = tuple(int(v) for v in sys.argv[4].split("x")) if len(sys.argv) > 4 else (64, 64)
     L = binding.load()
     L.sw_debug_phase_times.argtypes = [ctypes.c_void_p]
-    g = binding.Grid(2, (n, n), binding.COEF_FACES if faces else binding.COEF_POISSON).decompose((64, 64))
+    g = binding.Grid(dim, (n,) * dim, binding.COEF_FACES if faces else binding.COEF_POISSON).decompose(tile)
     if faces:
-        k = gen.lognormal_k(0, (n + 2, n + 2), 1.0)
-        g.set_coefficients_k(np.pad(k, [(1, 1), (0, 0)], constant_values=1.0), (1.0, 1.0))
-    g.set_vector(binding.B, gen.uniform_field(0, gen.STREAM_RHS, (n, n)) / float((n + 1) ** 2))
+        k = gen.lognormal_k(0, (n + 2,) * dim, 1.0)
+        pad = [(0, 0)] * dim
+        pad[0] = (1, 1)
+        g.set_coefficients_k(np.pad(k, pad, constant_values=1.0), (1.0,) * dim)
+    g.set_vector(binding.B, gen.uniform_field(0, gen.STREAM_RHS, (n,) * dim) / float((n + 1) ** 2))
     g.sor_sweep([1.9], 2, 0)
     torch.cuda.synchronize()
     out = (ctypes.c_ulonglong * 16)()
