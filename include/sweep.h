@@ -127,7 +127,8 @@ sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s);
 
 /* z = P^-1 r for the D-ILU(0) of sw_ilu0_factor.  r_dev / z_dev are device pointers to
  * PADDED arrays of the layout reported by sw_local_shape (e.g. from sw_ghost_view);
- * r's ghost layers must be current.  Borrowed.  Single rank. */
+ * r's ghost layers must be current.  Borrowed.  Single rank (several ranks: the staged form
+ * below). */
 sw_status sw_ilu_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_pairing pairing, sw_stream_t s);
 
 /* Same for the SSOR / SGS preconditioner z = w(2-w)(D + w L^T)^-1 D (D + w L)^-1 r at the
@@ -140,6 +141,33 @@ sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev, double *z
  * first.  SW_ENOCONV: iters/relres still valid.  Single rank. */
 sw_status sw_pcg_solve(sw_grid *g, sw_precond precond, double omega, sw_pairing pairing, double rtol, int maxit,
                        int *iters_out, double *relres_out, sw_stream_t s);
+
+/* Staged preconditioner application, for drivers that run one PCG over several ranks (the
+ * sw_*_apply calls above are the single-rank composition of all stages).  Stage 0 solves the
+ * forward factor (r -> the library's SW_Y array); stage 1 the backward factor (PAPER: the
+ * coupled solve at the reversed corner; SYMMETRIC: the pass over nodes outside coupled sets);
+ * stages 2 .. dim+1 (SYMMETRIC only) the coupled sets of degree 1 .. dim (R-C).  Between
+ * stages the caller refreshes the ghost layers of the slab axis: r (1 layer) before stage 0, Y
+ * (1 layer) before stage 1 for PAPER, Y (1) and z (2 layers) before every stage >= 2; 1/D~ (1)
+ * once after sw_ilu0_factor.  sw_precond_stages returns the number of stages (0 on NULL). */
+int sw_precond_stages(const sw_grid *g, sw_pairing pairing);
+sw_status sw_ilu_apply_stage(sw_grid *g, int stage, const double *r_dev, double *z_dev, sw_pairing pairing,
+                             sw_stream_t s);
+sw_status sw_ssor_apply_stage(sw_grid *g, int stage, double omega, const double *r_dev, double *z_dev,
+                              sw_pairing pairing, sw_stream_t s);
+
+/* PCG vector primitives on PADDED device arrays of the local slab (layout of sw_local_shape);
+ * each reduction is a fixed-order double-double sum over the local slab written as (hi, lo) to
+ * the 2-double DEVICE array *_dd (a multi-rank driver sums the ranks' pairs in rank order).
+ *   sw_apply_A: y = A x (ghost layers of x must be current), dot = x.y
+ *   sw_dot:     dot = a.b
+ *   sw_axpy2:   x += alpha p, r -= alpha q, rr = r.r
+ *   sw_xpby:    p = z + beta p                                                            */
+sw_status sw_apply_A(sw_grid *g, const double *x_dev, double *y_dev, double *dot_dd, sw_stream_t s);
+sw_status sw_dot(sw_grid *g, const double *a_dev, const double *b_dev, double *dot_dd, sw_stream_t s);
+sw_status sw_axpy2(sw_grid *g, double alpha, double *x_dev, double *r_dev, const double *p_dev, const double *q_dev,
+                   double *rr_dd, sw_stream_t s);
+sw_status sw_xpby(sw_grid *g, const double *z_dev, double beta, double *p_dev, sw_stream_t s);
 
 /* Synchronise `s` and report a deferred device-side error (singular coupled system). */
 sw_status sw_check_status(sw_grid *g, sw_stream_t s);

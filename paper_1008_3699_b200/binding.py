@@ -57,6 +57,14 @@ def load():
     L.sw_ilu_apply.argtypes = [P_, P_, P_, I, P_]
     L.sw_ssor_apply.argtypes = [P_, D, P_, P_, I, P_]
     L.sw_pcg_solve.argtypes = [P_, I, D, I, D, I, ctypes.POINTER(I), ctypes.POINTER(D), P_]
+    L.sw_precond_stages.argtypes = [P_, I]
+    L.sw_precond_stages.restype = I
+    L.sw_ilu_apply_stage.argtypes = [P_, I, P_, P_, I, P_]
+    L.sw_ssor_apply_stage.argtypes = [P_, I, D, P_, P_, I, P_]
+    L.sw_apply_A.argtypes = [P_, P_, P_, P_, P_]
+    L.sw_dot.argtypes = [P_, P_, P_, P_, P_]
+    L.sw_axpy2.argtypes = [P_, D, P_, P_, P_, P_, P_, P_]
+    L.sw_xpby.argtypes = [P_, P_, D, P_, P_]
     L.sw_check_status.argtypes = [P_, P_]
     L.sw_launch_count.argtypes = [P_]
     L.sw_launch_count.restype = I64
@@ -238,6 +246,40 @@ class Grid:
                                         ctypes.byref(it), ctypes.byref(rr), _stream(stream)), "sw_pcg_solve",
                     allow=(SW_ENOCONV,))
         return it.value, rr.value, st == SW_OK
+
+    # -------------------------------------------------------------- staged / vector primitives
+    # (device pointers of PADDED local-slab arrays; used by the multi-rank PCG in parallel.py)
+    def precond_stages(self, pairing: int = PAIR_SYMMETRIC) -> int:
+        return int(load().sw_precond_stages(self.h, int(pairing)))
+
+    def precond_apply_stage(self, precond: int, stage: int, r_ptr: int, z_ptr: int, omega: float = 1.0,
+                            pairing: int = PAIR_SYMMETRIC, stream=None):
+        if precond == PC_ILU0:
+            _check(load().sw_ilu_apply_stage(self.h, int(stage), ctypes.c_void_p(r_ptr), ctypes.c_void_p(z_ptr),
+                                             int(pairing), _stream(stream)), "sw_ilu_apply_stage")
+        elif precond == PC_SSOR:
+            _check(load().sw_ssor_apply_stage(self.h, int(stage), float(omega), ctypes.c_void_p(r_ptr),
+                                              ctypes.c_void_p(z_ptr), int(pairing), _stream(stream)),
+                   "sw_ssor_apply_stage")
+        else:
+            raise ValueError("no stages for this preconditioner")
+
+    def apply_A(self, x_ptr: int, y_ptr: int, dd_ptr: int, stream=None):
+        _check(load().sw_apply_A(self.h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr), ctypes.c_void_p(dd_ptr),
+                                 _stream(stream)), "sw_apply_A")
+
+    def dot(self, a_ptr: int, b_ptr: int, dd_ptr: int, stream=None):
+        _check(load().sw_dot(self.h, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), ctypes.c_void_p(dd_ptr),
+                             _stream(stream)), "sw_dot")
+
+    def axpy2(self, alpha: float, x_ptr: int, r_ptr: int, p_ptr: int, q_ptr: int, dd_ptr: int, stream=None):
+        _check(load().sw_axpy2(self.h, float(alpha), ctypes.c_void_p(x_ptr), ctypes.c_void_p(r_ptr),
+                               ctypes.c_void_p(p_ptr), ctypes.c_void_p(q_ptr), ctypes.c_void_p(dd_ptr),
+                               _stream(stream)), "sw_axpy2")
+
+    def xpby(self, z_ptr: int, beta: float, p_ptr: int, stream=None):
+        _check(load().sw_xpby(self.h, ctypes.c_void_p(z_ptr), float(beta), ctypes.c_void_p(p_ptr), _stream(stream)),
+               "sw_xpby")
 
     def check(self, stream=None):
         _check(load().sw_check_status(self.h, _stream(stream)), "sw_check_status")

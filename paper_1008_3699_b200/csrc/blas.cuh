@@ -308,6 +308,20 @@ __global__ void k_finish_sum(const DD *partial, int nparts, int stride, int off,
     if (threadIdx.x == 0) *dst = s.hi + s.lo;
 }
 
+// sum `nparts` partials in fixed order into dst[0] = hi, dst[1] = lo (double-double)
+__global__ void k_finish_dd(const DD *partial, int nparts, double *dst) {
+    __shared__ DD sh[RED_THREADS / 32];
+    DD acc = {0.0, 0.0};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc = dd_merge(acc, partial[i]);
+    DD s = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) {
+        dst[0] = s.hi;
+        dst[1] = s.lo;
+    }
+}
+
+__global__ void k_set_scalar(double *dst, double v) { *dst = v; }
+
 // alpha = rz / pq
 __global__ void k_cg_alpha(CgScalars *c) { c->alpha = c->rz / c->pq; }
 // beta = rz_new / rz ; rz = rz_new

@@ -322,6 +322,9 @@ extern "C" sw_status sw_set_faces(sw_grid *g, const double *const face_host[3], 
                         if (b == a && (gg[b] < 0 || gg[b] > G.ng[b])) phys = false;
                         if (b != a && (gg[b] < 0 || gg[b] >= G.ng[b])) phys = false;
                     }
+                    // (the outermost face of the slab extension has no slot in the padded array)
+                    for (int b = 0; b < d; ++b)
+                        if (c[b] + 2 >= g->pad[b]) phys = false;
                     if (!phys) continue;
                     if (!(v > 0.0)) return fail(SW_EINVAL, "face coefficients must be > 0");
                     hb[(size_t)(G.origin + c[0] + G.P0 * c[1] + G.P01 * c[2])] = v;
@@ -531,38 +534,40 @@ extern "C" sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s) {
 }
 
 // shared by ILU(0) and SSOR application
-static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
-                           cudaStream_t s) {
-    if (g->nranks > 1) return fail(SW_EINVAL, "preconditioner application is single-rank in this build");
+// Number of stages of a preconditioner application: 0 forward solve (r -> Y), 1 backward solve
+// (PAPER: coupled solve at the reversed corner; SYMMETRIC: uncoupled reversed pass), then for
+// SYMMETRIC one stage per coupled-set degree j = 1 .. dim (DESIGN R-C).  A multi-rank driver
+// refreshes ghost layers between stages (r before 0; Y before 1 for PAPER; Y and z before >= 2).
+static int tri_nstages(const sw_grid *g, sw_pairing pairing) { return pairing == SW_PAIR_PAPER ? 2 : 2 + g->dim; }
+
+static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
+                           int stage, cudaStream_t s) {
     sw_status st = ensure_work(g);
     if (st != SW_OK) return st;
     if (ilu && !g->factored) return fail(SW_ESTATE, "sw_ilu0_factor must precede sw_ilu_apply");
     if (!ilu && !(omega > 0.0 && omega < 2.0)) return fail(SW_EINVAL, "omega must lie in (0,2)");
     if (!r || !z || z == g->Y || r == z) return fail(SW_EINVAL, "bad r/z pointers");
-    int base = base_bits(g->dim, g->factor_phase);
+    if (stage < 0 || stage >= tri_nstages(g, pairing)) return fail(SW_EINVAL, "bad stage");
+    const int base = base_bits(g->dim, g->factor_phase), rev = base ^ ((1 << g->dim) - 1);
+    const double coef = ilu ? 1.0 : 2.0 - omega;
+    const double *invd = ilu ? g->invD : nullptr;
     if (g->dim == 2 && g->fast2d && g->maps.ok) {
-        // fast 64 x 64 path: forward solve, then the PAPER backward (forward solve at the reversed
-        // corner) or the SYMMETRIC backward (uncoupled reversed solve + start-face chain pass)
-        const double *invd = ilu ? g->invD : nullptr;
+        // 64 x 64 engine (sweep2v MODE_TRI, tri2t)
         const double *fx = g->G.poisson ? nullptr : g->F[0], *fy = g->G.poisson ? nullptr : g->F[1];
         const CUtensorMap &mfx = g->G.poisson ? g->maps.b : g->maps.f[0];
         const CUtensorMap &mfy = g->G.poisson ? g->maps.b : g->maps.f[1];
-        const CUtensorMap *mr = get_map(g, r, WW), *my = get_map(g, g->Y, WW), *maux = get_map(g, g->invD, T2);
-        if (!mr || !my || !maux) return fail(SW_ECUDA, "cuTensorMapEncodeTiled failed");
-        const double coef = ilu ? 1.0 : 2.0 - omega;
-        cudaError_t e = launch_tri2v(*mr, *maux, mfx, mfy, g->G, base, omega, invd, fx, fy, true, 1.0, true, g->Y,
-                                     g->flag, s);
-        g->launches++;
-        if (e == cudaSuccess) {
-            const int rev = base ^ 3;
-            e = launch_tri2v(*my, *maux, mfx, mfy, g->G, rev, omega, invd, fx, fy, false, coef,
+        const CUtensorMap *maux = get_map(g, g->invD, T2);
+        const CUtensorMap *msrc = get_map(g, stage == 0 ? r : g->Y, WW);
+        if (!msrc || !maux) return fail(SW_ECUDA, "cuTensorMapEncodeTiled failed");
+        cudaError_t e;
+        if (stage == 0)
+            e = launch_tri2v(*msrc, *maux, mfx, mfy, g->G, base, omega, invd, fx, fy, true, 1.0, true, g->Y, g->flag, s);
+        else if (stage == 1)
+            e = launch_tri2v(*msrc, *maux, mfx, mfy, g->G, rev, omega, invd, fx, fy, false, coef,
                              pairing == SW_PAIR_PAPER, z, g->flag, s);
-            g->launches++;
-        }
-        if (e == cudaSuccess && pairing == SW_PAIR_SYMMETRIC) {
-            e = launch_tri2t(g->G, base, omega, invd, fx, fy, g->Y, z, coef, g->flag, s);
-            g->launches += 2;
-        }
+        else
+            e = launch_tri2t_stage(g->G, base, omega, invd, fx, fy, g->Y, z, coef, g->flag, stage - 2, s);
+        g->launches++;
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("tri2 launch: ") + cudaGetErrorString(e));
         return SW_OK;
     }
@@ -570,81 +575,84 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     P.alpha_mode = ilu ? A_INVD : A_OMEGA_AP;
     P.invD = g->invD;
     for (int i = 0; i < 8; ++i) P.omega[i] = omega;
-    if (g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
-        // fast 3D path for the forward solves; the coupled-set phase of the SYMMETRIC backward
-        // stays on the generic kernel
-        const CUtensorMap *mr = get_map(g, r, 0), *my = get_map(g, g->Y, 0);
-        const CUtensorMap *m0 = g->G.poisson ? mr : get_map(g, g->F[0], 0);
-        const CUtensorMap *m1 = g->G.poisson ? mr : get_map(g, g->F[1], 0);
-        const CUtensorMap *m2 = g->G.poisson ? mr : get_map(g, g->F[2], 0);
-        if (!mr || !my || !m0 || !m1 || !m2) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+    if (stage <= 1 && g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
+        // 3D engine for the two forward-type solves
+        const double *src = stage == 0 ? r : g->Y;
+        const CUtensorMap *ms = get_map(g, src, 0);
+        const CUtensorMap *m0 = g->G.poisson ? ms : get_map(g, g->F[0], 0);
+        const CUtensorMap *m1 = g->G.poisson ? ms : get_map(g, g->F[1], 0);
+        const CUtensorMap *m2 = g->G.poisson ? ms : get_map(g, g->F[2], 0);
+        if (!ms || !m0 || !m1 || !m2) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
         Sweep3Args A3{};
         A3.G = g->G;
-        A3.base = base;
         for (int i = 0; i < 8; ++i) A3.omega[i] = omega;
-        A3.aux = ilu ? g->invD : nullptr;
+        A3.aux = invd;
         A3.f0 = g->G.poisson ? nullptr : g->F[0];
         A3.f1 = g->G.poisson ? nullptr : g->F[1];
         A3.f2 = g->G.poisson ? nullptr : g->F[2];
         A3.flag = g->flag;
         A3.tri = 1;
         A3.invd_mode = ilu;
-        A3.rscale = 1;
-        A3.coef = 1.0;
-        A3.couple = 1;
-        A3.out = g->Y;
-        cudaError_t e = launch_sweep3(*mr, *m0, *m1, *m2, A3, s);
+        if (stage == 0) {
+            A3.base = base; A3.rscale = 1; A3.coef = 1.0; A3.couple = 1; A3.out = g->Y;
+        } else {
+            A3.base = rev; A3.rscale = 0; A3.coef = coef; A3.couple = pairing == SW_PAIR_PAPER; A3.out = z;
+        }
+        cudaError_t e = launch_sweep3(*ms, *m0, *m1, *m2, A3, s);
         g->launches++;
-        if (e == cudaSuccess) {
-            A3.base = base ^ 7;
-            A3.rscale = 0;
-            A3.coef = ilu ? 1.0 : 2.0 - omega;
-            A3.couple = pairing == SW_PAIR_PAPER;
-            A3.out = z;
-            e = launch_sweep3(*my, *m0, *m1, *m2, A3, s);
-            g->launches++;
-        }
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
-        if (pairing == SW_PAIR_PAPER) return SW_OK;
-        if (getenv("SW_DEBUG_T1ONLY")) return SW_OK;
-        P.src = g->Y;
-        P.out = z;
-        P.rhs = R_COEF;
-        P.coef = ilu ? 1.0 : 2.0 - omega;
-        P.base = base;
-        for (int j = 1; j <= g->dim; ++j) {
-            P.mode = M_T2;
-            P.j = j;
-            if ((st = launch_generic(g, P, s)) != SW_OK) return st;
-        }
         return SW_OK;
     }
-    // forward: (D~ + L) y = r   (row-normalised: r0 = alpha r)
-    P.mode = M_FWD;
-    P.rhs = R_SCALE;
-    P.base = base;
-    P.src = r;
-    P.out = g->Y;
-    if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+    // generic kernel
+    if (stage == 0) {               // (D~ + L) y = r, row-normalised: r0 = alpha r
+        P.mode = M_FWD;
+        P.rhs = R_SCALE;
+        P.base = base;
+        P.src = r;
+        P.out = g->Y;
+        return launch_generic(g, P, s);
+    }
     P.src = g->Y;
     P.out = z;
     P.rhs = R_COEF;
-    P.coef = ilu ? 1.0 : 2.0 - omega;
+    P.coef = coef;
+    P.base = base;
     if (pairing == SW_PAIR_PAPER) {
         P.mode = M_FWD;
-        P.base = base ^ ((1 << g->dim) - 1);
+        P.base = rev;
         return launch_generic(g, P, s);
     }
-    // SYMMETRIC: (D~ + L^T) z = D~ y, non-coupled nodes first, then coupled sets by degree
-    P.mode = M_T1;
-    if ((st = launch_generic(g, P, s)) != SW_OK) return st;
-    if (getenv("SW_DEBUG_T1ONLY")) return SW_OK;
-    for (int j = 1; j <= g->dim; ++j) {
-        P.mode = M_T2;
-        P.j = j;
-        if ((st = launch_generic(g, P, s)) != SW_OK) return st;
+    if (stage == 1) {               // SYMMETRIC: (D~ + L^T) z = D~ y, nodes outside coupled sets
+        P.mode = M_T1;
+        return launch_generic(g, P, s);
+    }
+    P.mode = M_T2;                  // coupled sets of degree stage - 1
+    P.j = stage - 1;
+    return launch_generic(g, P, s);
+}
+
+static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
+                           cudaStream_t s) {
+    if (g->nranks > 1) return fail(SW_EINVAL, "multi-rank: apply the preconditioner stage by stage");
+    for (int stage = 0; stage < tri_nstages(g, pairing); ++stage) {
+        sw_status st = tri_stage(g, ilu, omega, r, z, pairing, stage, s);
+        if (st != SW_OK) return st;
     }
     return SW_OK;
+}
+
+extern "C" int sw_precond_stages(const sw_grid *g, sw_pairing pairing) { return g ? tri_nstages(g, pairing) : 0; }
+
+extern "C" sw_status sw_ilu_apply_stage(sw_grid *g, int stage, const double *r_dev, double *z_dev, sw_pairing pairing,
+                                        sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    return tri_stage(g, true, 1.0, r_dev, z_dev, pairing, stage, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_ssor_apply_stage(sw_grid *g, int stage, double omega, const double *r_dev, double *z_dev,
+                                         sw_pairing pairing, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    return tri_stage(g, false, omega, r_dev, z_dev, pairing, stage, (cudaStream_t)s);
 }
 
 extern "C" sw_status sw_ilu_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_pairing pairing, sw_stream_t s) {
@@ -740,6 +748,79 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     st = sw_check_status(g, s);
     if (st != SW_OK) return st;
     return fail(SW_ENOCONV, "PCG reached maxit");
+}
+
+// ------------------------------------------------------------------ vector primitives
+// (for drivers that run one PCG over several ranks; every reduction is a fixed-order
+// double-double sum over the local slab, returned as (hi, lo) in device memory)
+template <typename F>
+static sw_status spmv_launch(sw_grid *g, const Rows &RW, int nr, const double *x, double *y, cudaStream_t cs, F) {
+    const Geo &G = g->G;
+    const double *F0 = g->F[0], *F1 = g->F[1], *F2 = g->F[2];
+    const bool fc = !G.poisson;
+    if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, x, y, g->partial)
+                        : k_spmv_dot_r<1, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, x, y, g->partial);
+    else if (g->dim == 2) fc ? k_spmv_dot_r<2, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, x, y, g->partial)
+                             : k_spmv_dot_r<2, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, x, y, g->partial);
+    else fc ? k_spmv_dot_r<3, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, x, y, g->partial)
+            : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, x, y, g->partial);
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+static sw_status finish_dd(sw_grid *g, int nr, double *dst, cudaStream_t cs) {
+    k_finish_dd<<<1, RED_THREADS, 0, cs>>>(g->partial, nr, dst);
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+extern "C" sw_status sw_apply_A(sw_grid *g, const double *x, double *y, double *dot_dd, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!x || !y || !dot_dd || x == y) return fail(SW_EINVAL, "bad pointers");
+    const Rows RW = make_rows(g->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    sw_status st = spmv_launch(g, RW, nr, x, y, (cudaStream_t)s, 0);
+    return st != SW_OK ? st : finish_dd(g, nr, dot_dd, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_dot(sw_grid *g, const double *a, const double *b, double *dot_dd, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!a || !b || !dot_dd) return fail(SW_EINVAL, "bad pointers");
+    const Rows RW = make_rows(g->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    k_dot_r<<<nr, RED_THREADS, 0, (cudaStream_t)s>>>(RW, a, b, g->partial);
+    g->launches++;
+    CK(cudaGetLastError());
+    return finish_dd(g, nr, dot_dd, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_axpy2(sw_grid *g, double alpha, double *x, double *r, const double *p, const double *q,
+                              double *rr_dd, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!x || !r || !p || !q || !rr_dd) return fail(SW_EINVAL, "bad pointers");
+    cudaStream_t cs = (cudaStream_t)s;
+    const Rows RW = make_rows(g->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    k_set_scalar<<<1, 1, 0, cs>>>(&g->cg->alpha, alpha);
+    k_axpy2_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->alpha, x, r, p, q, g->partial);
+    g->launches += 2;
+    CK(cudaGetLastError());
+    return finish_dd(g, nr, rr_dd, cs);
+}
+
+extern "C" sw_status sw_xpby(sw_grid *g, const double *z, double beta, double *p, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!z || !p || z == p) return fail(SW_EINVAL, "bad pointers");
+    cudaStream_t cs = (cudaStream_t)s;
+    const Rows RW = make_rows(g->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    k_set_scalar<<<1, 1, 0, cs>>>(&g->cg->beta, beta);
+    k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 0, z, p);
+    g->launches += 2;
+    CK(cudaGetLastError());
+    return SW_OK;
 }
 
 extern "C" int64_t sw_launch_count(const sw_grid *g) { return g ? g->launches : 0; }

@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(32) k_tri2t(Tri2tArgs A) {
     }
 }
 
-inline cudaError_t launch_tri2t(const Geo &G, int base, double omega, const double *invd, const double *fx,
-                                const double *fy, const double *src, double *z, double coef, int *flag,
-                                cudaStream_t s) {
+inline cudaError_t launch_tri2t_stage(const Geo &G, int base, double omega, const double *invd, const double *fx,
+                                      const double *fy, const double *src, double *z, double coef, int *flag, int stage,
+                                      cudaStream_t s) {
     Tri2tArgs A;
     A.G = G;
     A.base = base;
@@ -196,15 +196,11 @@ inline cudaError_t launch_tri2t(const Geo &G, int base, double omega, const doub
     A.z = z;
     A.coef = coef;
     A.flag = flag;
+    A.stage = stage;
     const unsigned tiles = (unsigned)((int64_t)G.nt[0] * G.nt[1]);
-    for (int stage = 0; stage < 2; ++stage) {
-        A.stage = stage;
-        if (fx) k_tri2t<true><<<tiles, 32, 0, s>>>(A);
-        else k_tri2t<false><<<tiles, 32, 0, s>>>(A);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    if (fx) k_tri2t<true><<<tiles, 32, 0, s>>>(A);
+    else k_tri2t<false><<<tiles, 32, 0, s>>>(A);
+    return cudaGetLastError();
 }
 
 }  // namespace sw

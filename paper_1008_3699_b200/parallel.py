@@ -82,3 +82,129 @@ def exchange_ghosts_local(ts: Sequence, n_locals: Sequence[int], width: int = GH
             moves.append((peer, rs, ts[r][ss].clone()))
     for peer, rs, val in moves:
         ts[peer][rs].copy_(val)
+
+
+# ---------------------------------------------------------------------------------------------
+# One PCG over several slabs.  The arithmetic runs in the library's kernels
+# (staged preconditioner, SpMV, fused axpy / dot); this driver only orders the calls, refreshes
+# ghost layers between them and sums the ranks' double-double partials in rank order.
+
+def dd_sum(pairs) -> float:
+    """Sum (hi, lo) double-double pairs in the given order (TwoSum), rounded once."""
+    hi, lo = 0.0, 0.0
+    for h, l in pairs:
+        t = hi + h
+        bp = t - hi
+        err = (hi - (t - bp)) + (h - bp)
+        hi, lo = t, lo + err + l
+    return hi + lo
+
+
+class LocalComm:
+    """All ranks live in this process (virtual slabs, e.g. several Grids on one device)."""
+
+    def __init__(self, grids):
+        self.grids = list(grids)
+
+    def exchange(self, views, width):
+        exchange_ghosts_local(views, [g.n_local[-1] for g in self.grids], width)
+
+    def allsum(self, pairs):
+        return dd_sum(pairs)
+
+
+class DistComm:
+    """One rank per process: ghost layers by torch.distributed point-to-point (NCCL on GPUs),
+    reductions by all_gather of the (hi, lo) pairs and a rank-ordered sum on every rank."""
+
+    def __init__(self, grid, group=None, device=None):
+        import torch.distributed as dist
+        self.grids = [grid]
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.group = group
+        self.bufs = {}
+        self.device = device if device is not None else f"cuda:{grid.device}"
+
+    def exchange(self, views, width):
+        exchange_ghosts(views[0], self.grids[0].n_local[-1], self.rank, self.world, self.group, width, self.bufs)
+
+    def allsum(self, pairs):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(pairs[0], dtype=torch.float64, device=self.device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return dd_sum([tuple(o.tolist()) for o in out])
+
+
+def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol: float = 1e-8,
+              maxit: int = 10000):
+    """Preconditioned CG from x0 = 0 on the right-hand side SW_B of every slab grid of `comm`
+    (same algorithm and stop test as sw_pcg_solve).  Returns (iterations, relres, converged)."""
+    import torch
+
+    from . import binding as B
+    grids = comm.grids
+    dev = f"cuda:{grids[0].device}"
+    V = {w: [g.view(w) for g in grids] for w in (B.X, B.B, B.R, B.Z, B.P, B.Q, B.Y, B.INVD)}
+    ptr = {w: [t.data_ptr() for t in V[w]] for w in V}
+    dd = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in grids]
+
+    def reduce(fn):
+        for i, g in enumerate(grids):
+            fn(i, g)
+        torch.cuda.synchronize()
+        return comm.allsum([tuple(d.tolist()) for d in dd])
+
+    for i in range(len(grids)):
+        V[B.X][i].zero_()
+        V[B.R][i].copy_(V[B.B][i])
+    if precond == B.PC_ILU0:
+        for g in grids:
+            g.ilu0_factor(0)
+        comm.exchange(V[B.INVD], 1)
+    z = B.R if precond == B.PC_NONE else B.Z
+
+    def apply_pc():
+        if precond == B.PC_NONE:
+            return
+        comm.exchange(V[B.R], 1)
+        for st in range(grids[0].precond_stages(pairing)):
+            if st == 1 and pairing == B.PAIR_PAPER:
+                comm.exchange(V[B.Y], 1)
+            if st >= 2:
+                if st == 2:
+                    comm.exchange(V[B.Y], 1)
+                comm.exchange(V[B.Z], 2)
+            for i, g in enumerate(grids):
+                g.precond_apply_stage(precond, st, ptr[B.R][i], ptr[B.Z][i], omega, pairing)
+
+    bb = reduce(lambda i, g: g.dot(ptr[B.B][i], ptr[B.B][i], dd[i].data_ptr()))
+    bnorm = bb ** 0.5
+    if bnorm == 0.0:
+        return 0, 0.0, True
+    apply_pc()
+    rz = reduce(lambda i, g: g.dot(ptr[B.R][i], ptr[z][i], dd[i].data_ptr()))
+    for i in range(len(grids)):
+        V[B.P][i].copy_(V[z][i])
+    relres = 1.0
+    for it in range(1, maxit + 1):
+        comm.exchange(V[B.P], 1)
+        pq = reduce(lambda i, g: g.apply_A(ptr[B.P][i], ptr[B.Q][i], dd[i].data_ptr()))
+        alpha = rz / pq
+        rr = reduce(lambda i, g: g.axpy2(alpha, ptr[B.X][i], ptr[B.R][i], ptr[B.P][i], ptr[B.Q][i],
+                                         dd[i].data_ptr()))
+        relres = rr ** 0.5 / bnorm
+        if relres < rtol:
+            for g in grids:
+                g.check()
+            return it, relres, True
+        if relres != relres:
+            raise FloatingPointError("PCG produced NaN")
+        apply_pc()
+        rzn = reduce(lambda i, g: g.dot(ptr[B.R][i], ptr[z][i], dd[i].data_ptr()))
+        beta = rzn / rz
+        rz = rzn
+        for i, g in enumerate(grids):
+            g.xpby(ptr[z][i], beta, ptr[B.P][i])
+    return maxit, relres, False

@@ -100,3 +100,38 @@ def test_slab_rows_and_plan_validation():
     assert plan[1][1] == slice(8, 10) and plan[1][2] == slice(10, 12)
     with pytest.raises(ValueError):
         parallel.halo_plan(1, 0, 2)
+
+
+def _allsum_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = parallel.DistComm(None, device="cpu")
+        # rank r contributes the double-double (1 + r, r * 1e-20)
+        got = comm.allsum([(1.0 + rank, rank * 1e-20)])
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distcomm_allsum_is_rank_ordered_and_identical_on_all_ranks():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_allsum_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = parallel.dd_sum([(1.0 + r, r * 1e-20) for r in range(world)])
+    assert all(v == want for v in res.values()) and want == 6.0
+
+
+def test_dd_sum_is_exact_for_cancellation():
+    # (1e16 + 1) - 1e16 lost in plain doubles, kept by the double-double sum
+    assert parallel.dd_sum([(1e16, 0.0), (1.0, 0.0), (-1e16, 0.0)]) == 1.0
+    assert parallel.dd_sum([]) == 0.0
