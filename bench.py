@@ -216,6 +216,12 @@ def run_ours(args):
                "h2d_bytes_per_job": int(2 * NX * nl_y * 8), "d2h_bytes_per_job": int(NX * nl_y * 8),
                "ms_per_job": round(t, 3)}
 
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        del g
+        torch.cuda.empty_cache()
+        secondary = run_secondary(args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.seed, args.cpu_n, args.cpu_sweeps)
@@ -239,10 +245,90 @@ def run_ours(args):
             "cpu_baseline": cpu,
         }
         line["clocks"] = clk.summary()
+        if secondary:
+            line["secondary"] = secondary
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _time_sweeps(g, omega, nsw, phase=0):
+    import torch
+    g.sor_sweep(omega, 3, phase)                     # warm-up
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.sor_sweep(omega, nsw, phase + 3)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / nsw
+
+
+def run_secondary(args):
+    """The other BASELINE.json configurations, measured on the same GPU (not the headline):
+    config 3 (2D variable coefficients, 4096^2): 100 decomposed SOR sweeps at omega = 1 (R-10)
+    and ILU(0)-PCG (SYMMETRIC pairing) to 1e-8; config 5's sweep (3D anisotropic 512^3, boxes
+    32 x 8 x 4) at omega = 1; config 2 (256^2) iteration counts."""
+    import torch
+
+    from paper_1008_3699_b200 import binding, gen
+    out = {}
+    # ---- config 3
+    n = 4096
+    g = binding.Grid(2, (n, n), binding.COEF_FACES).decompose((64, 64))
+    k = gen.lognormal_k(args.seed, (n + 2, n + 2), 1.0)
+    g.set_coefficients_k(np.pad(k, [(1, 1), (0, 0)], constant_values=1.0), (1.0, 1.0))
+    del k
+    b = gen.uniform_field(args.seed, gen.STREAM_RHS, (n, n)) / float((n + 1) ** 2)
+    g.set_vector(binding.B, b)
+    ms = _time_sweeps(g, [1.0], 100)
+    out["c3_sor"] = {"n": [n, n], "sweeps": 100, "ms_per_sweep": round(ms, 4),
+                     "glups": round(n * n / (ms * 1e-3) / 1e9, 2), "algorithmic_B_per_lup": 40,
+                     "frac_of_measured_hbm": round(40 * n * n / (ms * 1e-3) / 1e9 / peaks()[0], 3)}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, rel, ok = g.pcg_solve(binding.PC_ILU0, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["c3_pcg_ilu0"] = {"iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
+                          "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
+    del g, b
+    torch.cuda.empty_cache()
+    # ---- config 5 sweep
+    n3 = 512
+    g = binding.Grid(3, (n3, n3, n3), binding.COEF_FACES).decompose((32, 8, 4))
+    k = gen.lognormal_k(args.seed, (n3 + 2,) * 3, 0.5)
+    g.set_coefficients_k(np.pad(k, [(1, 1), (0, 0), (0, 0)], constant_values=1.0), (1.0, 0.1, 0.01))
+    del k
+    g.set_vector(binding.B, gen.uniform_field(args.seed, gen.STREAM_RHS, (n3,) * 3) / float((n3 + 1) ** 2))
+    ms = _time_sweeps(g, [1.0], 8)
+    out["c5_sweep"] = {"n": [n3] * 3, "tile": [32, 8, 4], "ms_per_sweep": round(ms, 3),
+                       "glups": round(n3 ** 3 / (ms * 1e-3) / 1e9, 2), "algorithmic_B_per_lup": 48,
+                       "frac_of_measured_hbm": round(48 * n3 ** 3 / (ms * 1e-3) / 1e9 / peaks()[0], 3)}
+    del g
+    torch.cuda.empty_cache()
+    # ---- config 2 iteration counts (256^2 Poisson, 64 x 64 boxes)
+    n2 = 256
+    g = binding.Grid(2, (n2, n2)).decompose((64, 64))
+    b = gen.uniform_field(args.seed, gen.STREAM_RHS, (n2, n2)) / float((n2 + 1) ** 2)
+    g.set_vector(binding.B, b)
+    res = {}
+    for name, pc in (("ilu0", binding.PC_ILU0), ("ssor", binding.PC_SSOR), ("none", binding.PC_NONE)):
+        it, rel, ok = g.pcg_solve(pc, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
+        res[f"pcg_{name}"] = it
+    w = 2.0 / (1.0 + np.sin(np.pi / (n2 + 1)))
+    g.set_vector(binding.X, np.zeros((n2, n2)))
+    ph, sweeps = 0, 0
+    while sweeps < 20000:
+        ph = g.sor_sweep([w], 10, ph)
+        sweeps += 10
+        if g.residual_norm() < 1e-8:
+            break
+    res["sor_sweeps_to_1e-8 (checked every 10)"] = sweeps
+    out["c2_iterations"] = res
+    return out
 
 
 def cpu_baseline(seed, n, sweeps):
@@ -303,6 +389,7 @@ def main():
     ap.add_argument("--ref-n", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
