@@ -56,8 +56,8 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 // directly in rank space with compile-time indices.  Row of member S:
 //   u_S - sum_t C_{ax_t}(S) u_{S ^ (1<<t)} = r0_S + sum_{b not in AXES, axis order} C_b(S) u(S - st_b).
 template <int AXES>
-__device__ __forceinline__ void solve_set3(double *X, double *const C[3], int w, const int st[3], int sbits,
-                                           int *flag) {
+__device__ __forceinline__ void solve_set3(double *X, int WS, int w, const int st[3], int sbits, int *flag) {
+    // couplings of axis a live at X[(a + 1) WS + w] (one shared array: plain LDS addressing)
     constexpr int NA = ((AXES >> 0) & 1) + ((AXES >> 1) & 1) + ((AXES >> 2) & 1);
     constexpr int K = 1 << NA;
     constexpr int A0 = (AXES & 1) ? 0 : ((AXES & 2) ? 1 : 2);
@@ -79,13 +79,13 @@ __device__ __forceinline__ void solve_set3(double *X, double *const C[3], int w,
         double acc = X[wS];
 #pragma unroll
         for (int b = 0; b < 3; ++b)
-            if (!((AXES >> b) & 1)) acc = fma(C[b][wS], X[wS - st[b]], acc);
+            if (!((AXES >> b) & 1)) acc = fma(X[(b + 1) * WS + wS], X[wS - st[b]], acc);
         rhs[r] = acc;
         wi[r] = wS;
 #pragma unroll
         for (int q = 0; q < K; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
 #pragma unroll
-        for (int t = 0; t < NA; ++t) M[r][r ^ (1 << t)] = -C[AX[t]][wS];
+        for (int t = 0; t < NA; ++t) M[r][r ^ (1 << t)] = -X[(AX[t] + 1) * WS + wS];
     }
     ge_solve_k<K>(M, rhs, u, flag);
 #pragma unroll
@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(k3::NT, 2)
     const int W0 = T0 + 4, W1 = T1 + 4, W2 = T2 + 4;
     const int WS = W0 * W1 * W2;
     double *X = sm;
-    double *C[3] = {sm + WS, sm + 2 * WS, sm + 3 * WS};
+    double *const C0 = sm + WS, *const C1 = sm + 2 * WS, *const C2 = sm + 3 * WS;
+    auto CC = [&](int a, int w) -> double & { return sm[(a + 1) * WS + w]; };   // coupling of axis a
     const int tid = threadIdx.x;
     // box, direction bits, coupled start faces
     const int tx = blockIdx.x % G.nt[0];
@@ -144,9 +145,9 @@ __global__ void __launch_bounds__(k3::NT, 2)
         mbar_expect_tx(&bar, (uint32_t)(sizeof(double) * WS * (FACES ? 4 : 1)));
         tma_load_3d(X, &tmx, tx * T0, ty * T1, tz * T2, &bar);
         if (FACES) {   // face windows land in the coupling arrays and are converted in place
-            tma_load_3d(C[0], &tf0, tx * T0, ty * T1, tz * T2, &bar);
-            tma_load_3d(C[1], &tf1, tx * T0, ty * T1, tz * T2, &bar);
-            tma_load_3d(C[2], &tf2, tx * T0, ty * T1, tz * T2, &bar);
+            tma_load_3d(C0, &tf0, tx * T0, ty * T1, tz * T2, &bar);
+            tma_load_3d(C1, &tf1, tx * T0, ty * T1, tz * T2, &bar);
+            tma_load_3d(C2, &tf2, tx * T0, ty * T1, tz * T2, &bar);
         }
     }
     __syncthreads();
@@ -186,8 +187,8 @@ __global__ void __launch_bounds__(k3::NT, 2)
         double f[3][2];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            f[a][0] = FACES ? C[a][w] : 1.0;
-            f[a][1] = FACES ? C[a][w + Sv[a]] : 1.0;
+            f[a][0] = FACES ? CC(a, w) : 1.0;
+            f[a][1] = FACES ? CC(a, w + Sv[a]) : 1.0;
         }
         const double ap = (((f[0][0] + f[0][1]) + (f[1][0] + f[1][1])) + (f[2][0] + f[2][1])) + G.beta;
         const int db = sb ^ L;                             // direction bits of the node's box
@@ -221,9 +222,9 @@ __global__ void __launch_bounds__(k3::NT, 2)
     for (int it = 0; it < k3::KMAX; ++it)
         if (wv[it] >= 0) {
             X[wv[it]] = r0v[it];
-            C[0][wv[it]] = cv[it][0];
-            C[1][wv[it]] = cv[it][1];
-            C[2][wv[it]] = cv[it][2];
+            C0[wv[it]] = cv[it][0];
+            C1[wv[it]] = cv[it][1];
+            C2[wv[it]] = cv[it][2];
         }
     __syncthreads();
     SW_TMARK(t_prologue);
@@ -235,20 +236,20 @@ __global__ void __launch_bounds__(k3::NT, 2)
         if (tid == 0) {
             const int w = wof(0, 0, 0);
             switch (cb) {
-                case 7: solve_set3<7>(X, C, w, st, sb, A.flag); break;
-                case 3: solve_set3<3>(X, C, w, st, sb, A.flag); break;
-                case 5: solve_set3<5>(X, C, w, st, sb, A.flag); break;
-                default: solve_set3<6>(X, C, w, st, sb, A.flag); break;
+                case 7: solve_set3<7>(X, WS, w, st, sb, A.flag); break;
+                case 3: solve_set3<3>(X, WS, w, st, sb, A.flag); break;
+                case 5: solve_set3<5>(X, WS, w, st, sb, A.flag); break;
+                default: solve_set3<6>(X, WS, w, st, sb, A.flag); break;
             }
         }
         __syncthreads();
         // the edge chains (independent of each other), one per warp
         if (tid == 0 && (cb & 6) == 6)
-            for (int t = 1; t < T0; ++t) solve_set3<6>(X, C, wof(t, 0, 0), st, sb, A.flag);
+            for (int t = 1; t < T0; ++t) solve_set3<6>(X, WS, wof(t, 0, 0), st, sb, A.flag);
         if (tid == 32 && (cb & 5) == 5)
-            for (int t = 1; t < T1; ++t) solve_set3<5>(X, C, wof(0, t, 0), st, sb, A.flag);
+            for (int t = 1; t < T1; ++t) solve_set3<5>(X, WS, wof(0, t, 0), st, sb, A.flag);
         if (tid == 64 && (cb & 3) == 3)
-            for (int t = 1; t < T2; ++t) solve_set3<3>(X, C, wof(0, 0, t), st, sb, A.flag);
+            for (int t = 1; t < T2; ++t) solve_set3<3>(X, WS, wof(0, 0, t), st, sb, A.flag);
         __syncthreads();
     }
 
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
     if ((int)blockIdx.x == sw_dbg3_block)
         for (int i = tid; i < WS; i += k3::NT) {
             sw_dbg3[i] = X[i];
-            sw_dbg3[8192 + i] = C[0][i];
+            sw_dbg3[8192 + i] = C0[i];
         }
 #endif
     SW_TMARK(t_sets);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
             wl[h] = wof(0, ln < nl ? j : 0, ln < nl ? k : 0);
             lm[h] = (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
         }
-        const int s0 = st[0];
+        const int s0 = st[0], st0 = st[0], st1 = st[1], st2 = st[2];
         int fl = 0;
         for (int d = 0; d < nlev; ++d) {
 #pragma unroll
@@ -285,23 +286,26 @@ __global__ void __launch_bounds__(k3::NT, 2)
                 const int w = wl[h] + i * s0;
                 if (m == 0) {
                     double acc = X[w];
-                    acc = fma(C[0][w], X[w - st[0]], acc);
-                    acc = fma(C[1][w], X[w - st[1]], acc);
-                    acc = fma(C[2][w], X[w - st[2]], acc);
+                    acc = fma(C0[w], X[w - st0], acc);
+                    acc = fma(C1[w], X[w - st1], acc);
+                    acc = fma(C2[w], X[w - st2], acc);
                     X[w] = acc;
                 } else if ((m & (m - 1)) == 0) {               // one coupled face: 2 x 2 pair
-                    const int a = __ffs(m) - 1;
-                    const int q = w - st[a];
+                    const int a = (m & 1) ? 0 : ((m & 2) ? 1 : 2);
+                    const int sta = (m & 1) ? st0 : ((m & 2) ? st1 : st2);
+                    const int q = w - sta;
                     double rp = X[w], rq = X[q];
-#pragma unroll
-                    for (int b = 0; b < 3; ++b)
-                        if (b != a) {
-                            rp = fma(C[b][w], X[w - st[b]], rp);
-                            rq = fma(C[b][q], X[q - st[b]], rq);
-                        }
+                    // the two axes other than a, in axis order
+                    const int b1 = (a == 0) ? 1 : 0, b2 = (a == 2) ? 1 : 2;
+                    const int s1 = (a == 0) ? st1 : st0, s2 = (a == 2) ? st1 : st2;
+                    rp = fma(CC(b1, w), X[w - s1], rp);
+                    rq = fma(CC(b1, q), X[q - s1], rq);
+                    rp = fma(CC(b2, w), X[w - s2], rp);
+                    rq = fma(CC(b2, q), X[q - s2], rq);
                     const bool qfirst = ((sb >> a) & 1) == 0;   // partner has the lower global index
                     const double ra = qfirst ? rq : rp, rb = qfirst ? rp : rq;
-                    const double mab = qfirst ? C[a][q] : C[a][w], mba = qfirst ? C[a][w] : C[a][q];
+                    const double cw = CC(a, w), cq = CC(a, q);
+                    const double mab = qfirst ? cq : cw, mba = qfirst ? cw : cq;
                     const double m11 = fma(mba, -mab, 1.0);
                     fl |= !(fabs(m11) >= 1e-14);
                     const double ub = fma(mba, ra, rb) * div_rn(1.0, m11);
