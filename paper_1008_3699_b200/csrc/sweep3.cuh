@@ -92,6 +92,127 @@ __device__ __forceinline__ void solve_set3(double *X, int WS, int w, const int s
     for (int r = 0; r < K; ++r) X[wi[r]] = u[r];
 }
 
+__device__ __forceinline__ double shfl_up_f64(double v, int delta) {   // full warp, converged
+    int lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    asm volatile("shfl.sync.up.b32 %0, %0, %1, 0, 0xffffffff;" : "+r"(lo) : "r"(delta));
+    asm volatile("shfl.sync.up.b32 %0, %0, %1, 0, 0xffffffff;" : "+r"(hi) : "r"(delta));
+    double r;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+
+// A 4-member set (an edge of two coupled faces) split into the part that depends only on the
+// couplings (the elimination of the matrix: multipliers, eliminated upper triangle, reciprocal
+// pivots) and the part that depends on the chain (right-hand side, its elimination, back
+// substitution).  The operations and their order are exactly those of ge_solve_k<4>, so the
+// result is the same bit for bit; the split lets every set of an edge be factored in parallel.
+struct Fac4 {
+    double l[6], U[6], inv[4];
+};
+
+template <int AXES>
+__device__ __forceinline__ void factor4(const double *X, int WS, int w, const int st[3], int sbits, Fac4 &F,
+                                        int &fl) {
+    constexpr int A0 = (AXES & 1) ? 0 : 1;
+    constexpr int A1 = (AXES & 4) ? 2 : 1;
+    constexpr int AX[2] = {A0, A1};
+    int m = 0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) m |= (((sbits >> AX[t]) & 1) == 0) << t;
+    double M[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int S = r ^ m;
+        int wS = w;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+            if ((S >> t) & 1) wS -= st[AX[t]];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) M[r][r ^ (1 << t)] = -X[(AX[t] + 1) * WS + wS];
+    }
+    int li = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const double piv = M[p][p];
+        fl |= !(fabs(piv) >= 1e-14);
+        F.inv[p] = div_rn(1.0, piv);
+#pragma unroll
+        for (int q = p + 1; q < 4; ++q) {
+            const double l = M[q][p] * F.inv[p];
+            F.l[li++] = l;
+#pragma unroll
+            for (int j = p + 1; j < 4; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
+        }
+    }
+    int ui = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int j = p + 1; j < 4; ++j) F.U[ui++] = M[p][j];
+}
+
+template <int AXES>
+__device__ __forceinline__ void subst4(double *X, int WS, int w, const int st[3], int sbits, const Fac4 &F) {
+    constexpr int A0 = (AXES & 1) ? 0 : 1;
+    constexpr int A1 = (AXES & 4) ? 2 : 1;
+    constexpr int AX[2] = {A0, A1};
+    constexpr int B = 3 - A0 - A1;            // the chain axis
+    int m = 0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) m |= (((sbits >> AX[t]) & 1) == 0) << t;
+    double rhs[4], u[4];
+    int wi[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int S = r ^ m;
+        int wS = w;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+            if ((S >> t) & 1) wS -= st[AX[t]];
+        rhs[r] = fma(X[(B + 1) * WS + wS], X[wS - st[B]], X[wS]);
+        wi[r] = wS;
+    }
+    int li = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = p + 1; q < 4; ++q) {
+            rhs[q] = fma(-F.l[li], rhs[p], rhs[q]);
+            ++li;
+        }
+    constexpr int UI[4] = {0, 3, 5, 6};       // first U entry of row p
+#pragma unroll
+    for (int p = 3; p >= 0; --p) {
+        double sacc = rhs[p];
+#pragma unroll
+        for (int j = p + 1; j < 4; ++j) sacc = fma(-F.U[UI[p] + (j - p - 1)], u[j], sacc);
+        u[p] = sacc * F.inv[p];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) X[wi[r]] = u[r];
+}
+
+// one edge chain: lane t-1 of the calling warp owns set t (t = 1 .. T-1 <= 32); every lane
+// factors its set while the corner is being solved, then the sets are substituted in order
+template <int AXES>
+__device__ __forceinline__ void edge_chain(double *X, int WS, int lane, int T, int w1, int step, const int st[3],
+                                           int sbits, int *flag, bool run) {
+    Fac4 F;
+    int fl = 0;
+    const bool mine = run && lane + 1 < T;
+    if (mine) factor4<AXES>(X, WS, w1 + lane * step, st, sbits, F, fl);
+    if (fl) atomicOr(flag, 1);
+    __syncthreads();                          // the corner set is in place
+    if (run)
+        for (int t = 1; t < T; ++t) {
+            if (lane == t - 1) subst4<AXES>(X, WS, w1 + (t - 1) * step, st, sbits, F);
+            __syncwarp();
+        }
+}
+
 #ifdef SW_DEBUG3
 __device__ double sw_dbg3[4 * 8192];
 __device__ int sw_dbg3_block = -1;
@@ -227,6 +348,26 @@ __global__ void __launch_bounds__(k3::NT, 2)
             C2[wv[it]] = cv[it][2];
         }
     __syncthreads();
+    // pivots 1 / (1 - m m') of the face pairs that the level loop solves (y- and z-face sheets),
+    // stored in the free second halo layer at local y = -2 / z = -2 of the pair
+    const bool fast_lines = T1 * T2 <= 32;
+    if (fast_lines) {
+        const int ny = ((cb & 2) ? T0 * T2 : 0), nz = ((cb & 4) ? T0 * T1 : 0);
+        int fl = 0;
+        for (int e = tid; e < ny + nz; e += k3::NT) {
+            int i, j, k, a;
+            if (e < ny) { i = e % T0; k = e / T0; j = 0; a = 1; }
+            else { i = (e - ny) % T0; j = (e - ny) / T0; k = 0; a = 2; }
+            const int m = (i == 0 ? (cb & 1) : 0) | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
+            if (__popc(m) != 1) continue;                         // sets of two or more faces: step 3
+            const int w = wof(i, j, k), q = w - st[a];
+            const double m11 = fma(CC(a, w), -CC(a, q), 1.0);
+            fl |= !(fabs(m11) >= 1e-14);
+            X[q - st[a]] = div_rn(1.0, m11);
+        }
+        if (fl) atomicOr(A.flag, 1);
+        __syncthreads();
+    }
     SW_TMARK(t_prologue);
     // ---------------------------------------------------------------- 3. corner and edge sets
     const int ncpl = __popc(cb);
@@ -242,14 +383,13 @@ __global__ void __launch_bounds__(k3::NT, 2)
                 default: solve_set3<6>(X, WS, w, st, sb, A.flag); break;
             }
         }
-        __syncthreads();
-        // the edge chains (independent of each other), one per warp
-        if (tid == 0 && (cb & 6) == 6)
-            for (int t = 1; t < T0; ++t) solve_set3<6>(X, WS, wof(t, 0, 0), st, sb, A.flag);
-        if (tid == 32 && (cb & 5) == 5)
-            for (int t = 1; t < T1; ++t) solve_set3<5>(X, WS, wof(0, t, 0), st, sb, A.flag);
-        if (tid == 64 && (cb & 3) == 3)
-            for (int t = 1; t < T2; ++t) solve_set3<3>(X, WS, wof(0, 0, t), st, sb, A.flag);
+        // the edge chains (independent of each other), one per warp: x-edge in warp 1, y-edge in
+        // warp 2, z-edge in warp 3 (factored in parallel with the corner, substituted in order)
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp == 1) edge_chain<6>(X, WS, lane, T0, wof(1, 0, 0), st[0], st, sb, A.flag, (cb & 6) == 6);
+        else if (warp == 2) edge_chain<5>(X, WS, lane, T1, wof(0, 1, 0), st[1], st, sb, A.flag, (cb & 5) == 5);
+        else if (warp == 3) edge_chain<3>(X, WS, lane, T2, wof(0, 0, 1), st[2], st, sb, A.flag, (cb & 3) == 3);
+        else __syncthreads();
         __syncthreads();
     }
 
@@ -262,6 +402,108 @@ __global__ void __launch_bounds__(k3::NT, 2)
 #endif
     SW_TMARK(t_sets);
     // ---------------------------------------------------------------- 4. level loop (warp 0)
+    if (fast_lines) {
+        // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over (j, k)
+        if (tid < 32 && (cb & 1)) {
+            const int j = tid % T1, k = tid / T1;
+            const bool on = tid < T1 * T2;
+            const int m = 1 | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
+            const int w = on ? wof(0, j, k) : 0, q = w - st[0];
+            int fl = 0;
+            for (int d = 0; d <= T1 + T2 - 2; ++d) {
+                if (on && j + k == d && m == 1) {
+                    const double rp = fma(CC(2, w), X[w - st[2]], fma(CC(1, w), X[w - st[1]], X[w]));
+                    const double rq = fma(CC(2, q), X[q - st[2]], fma(CC(1, q), X[q - st[1]], X[q]));
+                    const bool qfirst = (sb & 1) == 0;
+                    const double ra = qfirst ? rq : rp, rb = qfirst ? rp : rq;
+                    const double cw = CC(0, w), cq = CC(0, q);
+                    const double mab = qfirst ? cq : cw, mba = qfirst ? cw : cq;
+                    const double m11 = fma(mba, -mab, 1.0);
+                    fl |= !(fabs(m11) >= 1e-14);
+                    const double ub = fma(mba, ra, rb) * div_rn(1.0, m11);
+                    const double ua = fma(mab, ub, ra) * 1.0;
+                    X[w] = qfirst ? ub : ua;
+                    X[q] = qfirst ? ua : ub;
+                }
+                __syncwarp();
+            }
+            if (fl) atomicOr(A.flag, 1);
+        }
+        // (b) all other nodes: lane (j, k) owns the x-line and updates node i = s - j - k at step
+        //     s; S and B arrive from lanes l-1 and l-T1 by shuffles, and so do the partner values
+        //     of the y- and z-face sheets (which each lane on such a face carries in registers).
+        //     One branch-free instruction stream for every kind of lane: a plain lane is a "pair"
+        //     with zero couplings and unit pivot, which leaves its node formula exact; the x-edge
+        //     lane (solved in step 3) only reloads and forwards its values.
+        if (tid < 32) {
+            const int lane = tid, nl = T1 * T2;
+            const bool on = lane < nl;
+            const int j = on ? lane % T1 : 0, k = on ? lane / T1 : 0;
+            const bool yc = j == 0 && (cb & 2), zc = k == 0 && (cb & 4);
+            const bool edge = yc && zc, ypair = yc && !zc, zpair = zc && !yc, pair = ypair || zpair;
+            const int i0 = (cb & 1) ? 1 : 0;
+            const int sx = st[0], sy = st[1], sz = st[2];
+            const int sa = ypair ? sy : (zpair ? sz : 0);                 // step toward the pair partner
+            const int wl = wof(0, j, k);
+            const bool qf = pair ? (((sb >> (ypair ? 1 : 2)) & 1) == 0) : true;   // partner first in index order
+            // addresses of the other transverse coupling of the partner: z for y-pairs, y for z-pairs
+            const int oq_arr = ypair ? 3 : 2;                             // (axis + 1) of that coupling
+            const int pa_arr = ypair ? 2 : 3;                             // (axis + 1) of the pair coupling
+            double W = i0 ? X[wl] : 0.0;
+            double Wq = (i0 && pair) ? X[wl - sa] : 0.0;                 // partner value at i0 - 1
+            double u = 0.0, py = 0.0, pz = 0.0;
+            const int NS = T0 + T1 + T2 - 2;
+            auto ld = [&](int s, double (&v)[11]) {
+                int i = s - j - k;
+                i = i < 0 ? 0 : (i >= T0 ? T0 - 1 : i);                   // clamp idle lanes' addresses
+                const int w = wl + i * sx, q = pair ? w - sa : w;
+                v[0] = X[w];                    // r0 (edge lane: its solved value)
+                v[1] = sm[WS + w];              // C_x
+                v[2] = sm[2 * WS + w];          // C_y
+                v[3] = sm[3 * WS + w];          // C_z
+                v[4] = X[q];                    // partner r0
+                v[5] = sm[WS + q];              // partner C_x
+                v[6] = sm[oq_arr * WS + q];     // partner other transverse coupling
+                v[7] = sm[pa_arr * WS + q];     // partner pair coupling
+                v[8] = pair ? X[q - sa] : 1.0;  // pivot inverse (prologue)
+                v[9] = edge ? X[w - sy] : 0.0;  // edge: its y-partner value
+                v[10] = edge ? X[w - sz] : 0.0; //       its z-partner value
+            };
+            double nv[11];
+            ld(0, nv);
+            for (int s = 0; s < NS; ++s) {
+                const double Sv = shfl_up_f64(u, 1), Bv = shfl_up_f64(u, T1);
+                const double Sq = shfl_up_f64(pz, 1), Bq = shfl_up_f64(py, T1);
+                double v[11];
+#pragma unroll
+                for (int t = 0; t < 11; ++t) v[t] = nv[t];
+                if (s + 1 < NS) ld(s + 1, nv);
+                const int i = s - j - k;
+                const bool act = on && i >= i0 && i < T0;
+                const int w = wl + (i < 0 ? 0 : (i >= T0 ? T0 - 1 : i)) * sx;
+                // own row: x, y (unless the y pair), z (unless the z pair), in axis order
+                const double cyE = ypair ? 0.0 : v[2], czE = zpair ? 0.0 : v[3];
+                const double rp = fma(czE, Bv, fma(cyE, Sv, fma(v[1], W, v[0])));
+                // partner row: x, then the other transverse axis
+                const double Oq = ypair ? Bq : Sq;
+                const double rq = fma(pair ? v[6] : 0.0, Oq, fma(pair ? v[5] : 0.0, Wq, v[4]));
+                const double cw = ypair ? v[2] : (zpair ? v[3] : 0.0), cq = pair ? v[7] : 0.0;
+                const double ra = qf ? rq : rp, rb = qf ? rp : rq;
+                const double mab = qf ? cq : cw, mba = qf ? cw : cq;
+                const double ub = fma(mba, ra, rb) * v[8];
+                const double ua = fma(mab, ub, ra) * 1.0;
+                double un = qf ? ub : ua;
+                const double pv = qf ? ua : ub;
+                un = edge ? v[0] : un;
+                st_shared_if(X + w, un, act && !edge);
+                u = sel_f64(act, un, u);
+                W = sel_f64(act, un, W);              // idle (joining) lanes keep W = value at i0 - 1
+                Wq = sel_f64(act && pair, pv, Wq);
+                py = sel_f64(act, ypair ? pv : (edge ? v[9] : py), py);
+                pz = sel_f64(act, zpair ? pv : (edge ? v[10] : pz), pz);
+            }
+        }
+    } else
     if (tid < 32) {
         const int nl = T1 * T2, nlev = T0 + T1 + T2 - 2;
         // per-lane lines (at most two): offset j + k of the level, window word of node i = 0,
@@ -362,6 +604,7 @@ inline bool sweep3_supported(const Geo &G) {
     const int64_t ne = (int64_t)(G.T[0] + 1) * (G.T[1] + 1) * (G.T[2] + 1);
     return (G.T[0] % 2 == 0) && G.T[0] + 4 <= 256 && G.T[1] + 4 <= 256 && G.T[2] + 4 <= 256 &&
            sweep3_smem(G) <= 227 * 1024 && ne <= (int64_t)k3::NT * k3::KMAX && G.T[1] * G.T[2] <= k3::MAXLINES &&
+           G.T[0] <= 33 && G.T[1] <= 33 && G.T[2] <= 33 &&
            G.off[0] == 0 && G.off[1] == 0;
 }
 
