@@ -195,6 +195,59 @@ __device__ __forceinline__ void subst4(double *X, int WS, int w, const int st[3]
     for (int r = 0; r < 4; ++r) X[wi[r]] = u[r];
 }
 
+// The corner set of three coupled faces (8 members), eliminated by lanes 0..7 of one warp (lane
+// q owns row q; step p: every lane below p updates its row) in a shared scratch of >= 80
+// doubles; the same operations in the same order as ge_solve_k<8>, then lane 0 back-substitutes.
+__device__ __forceinline__ void corner8_coop(double *X, int WS, double *scr, int lane, int w, const int st[3], int sbits,
+                                             int *flag) {
+    double *M = scr, *rhs = scr + 64, *inv = scr + 72;
+    int m = 0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) m |= (((sbits >> t) & 1) == 0) << t;
+    int wS = w;
+    if (lane < 8) {
+        const int r = lane, S = r ^ m;
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if ((S >> t) & 1) wS -= st[t];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) M[r * 8 + q] = (r == q) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) M[r * 8 + (r ^ (1 << t))] = -X[(t + 1) * WS + wS];
+        rhs[r] = X[wS];
+    }
+    __syncwarp();
+    for (int p = 0; p < 8; ++p) {
+        const double piv = M[p * 8 + p];
+        const double ip = div_rn(1.0, piv);
+        if (lane == 0) {
+            inv[p] = ip;
+            if (!(fabs(piv) >= 1e-14)) atomicOr(flag, 1);
+        }
+        if (lane > p && lane < 8) {
+            const double l = M[lane * 8 + p] * ip;
+            for (int j = p + 1; j < 8; ++j) M[lane * 8 + j] = fma(-l, M[p * 8 + j], M[lane * 8 + j]);
+            rhs[lane] = fma(-l, rhs[p], rhs[lane]);
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        double u[8];
+#pragma unroll
+        for (int p = 7; p >= 0; --p) {
+            double sacc = rhs[p];
+#pragma unroll
+            for (int j = p + 1; j < 8; ++j) sacc = fma(-M[p * 8 + j], u[j], sacc);
+            u[p] = sacc * inv[p];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) rhs[r] = u[r];
+    }
+    __syncwarp();
+    if (lane < 8) X[wS] = rhs[lane];
+    __syncwarp();
+}
+
 // one edge chain: lane t-1 of the calling warp owns set t (t = 1 .. T-1 <= 32); every lane
 // factors its set while the corner is being solved, then the sets are substituted in order
 template <int AXES>
@@ -272,13 +325,10 @@ __global__ void __launch_bounds__(k3::NT, 2)
         }
     }
     __syncthreads();
-    mbar_wait(&bar, 0);
-    SW_TMARK(t_staged);
-
-    // ---------------------------------------------------------------- 2. prologue
+    // right-hand sides (SOR: b) or 1/D~ (ILU) of the active nodes: issued before waiting for the window
     const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1, NE = E0 * E1 * E2;   // local [-1, T) per axis
-    // pass 1: every active node's r0 and couplings into registers (reads faces from the coupling
-    // arrays and x_old from the window); pass 2, after a barrier: write them in place
+    // pass 1 (below): every active node's r0 and couplings into registers (reads faces from the
+    // coupling arrays and x_old from the window); pass 2, after a barrier: write them in place
     double r0v[k3::KMAX], cv[k3::KMAX][3];
     int wv[k3::KMAX];
     double auxv[k3::KMAX];
@@ -291,13 +341,17 @@ __global__ void __launch_bounds__(k3::NT, 2)
         const int l0 = e % E0 - 1, l1 = (e / E0) % E1 - 1, l2 = e / (E0 * E1) - 1;
         const int L = (l0 < 0 ? 1 : 0) | (l1 < 0 ? 2 : 0) | (l2 < 0 ? 4 : 0);
         if ((L & cb) != L) continue;                      // not an active node
-        const int w = wof(l0, l1, l2);
-        wv[it] = w;
-        if (!A.tri || A.invd_mode) {
-            const int64_t g = gbase + (w % W0) + (int64_t)((w / W0) % W1) * P0 + (int64_t)(w / (W0 * W1)) * P01;
-            auxv[it] = A.aux[g];
-        }
+        const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - l0 : l0);
+        const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - l1 : l1);
+        const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - l2 : l2);
+        wv[it] = w0 + W0 * (w1 + W1 * w2);
+        if (!A.tri || A.invd_mode) auxv[it] = A.aux[gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01];
     }
+    mbar_wait(&bar, 0);
+    SW_TMARK(t_staged);
+
+    // ---------------------------------------------------------------- 2. prologue
+    SW_TMARK(t_p1);
 #pragma unroll
     for (int it = 0; it < k3::KMAX; ++it) {
         const int w = wv[it];
@@ -338,6 +392,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
         }
         r0v[it] = r0;
     }
+    SW_TMARK(t_p2);
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < k3::KMAX; ++it)
@@ -350,6 +405,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
     __syncthreads();
     // pivots 1 / (1 - m m') of the face pairs that the level loop solves (y- and z-face sheets),
     // stored in the free second halo layer at local y = -2 / z = -2 of the pair
+    SW_TMARK(t_p3);
     const bool fast_lines = T1 * T2 <= 32;
     if (fast_lines) {
         const int ny = ((cb & 2) ? T0 * T2 : 0), nz = ((cb & 4) ? T0 * T1 : 0);
@@ -374,7 +430,11 @@ __global__ void __launch_bounds__(k3::NT, 2)
     if (ncpl >= 2) {
         // one thread: the corner set, then the edge chains (a chain of 4-sets along axis c where
         // the two other axes are coupled; its only outside dependency is the previous set)
-        if (tid == 0) {
+        // scratch: the second halo plane beyond the end z face (never read)
+        double *zscr = X + ((((sb >> 2) & 1) ? 0 : W2 - 1) * W0 * W1);
+        if (cb == 7 && W0 * W1 >= 80) {
+            if (tid < 32) corner8_coop(X, WS, zscr, tid, wof(0, 0, 0), st, sb, A.flag);
+        } else if (tid == 0) {
             const int w = wof(0, 0, 0);
             switch (cb) {
                 case 7: solve_set3<7>(X, WS, w, st, sb, A.flag); break;
@@ -383,6 +443,8 @@ __global__ void __launch_bounds__(k3::NT, 2)
                 default: solve_set3<6>(X, WS, w, st, sb, A.flag); break;
             }
         }
+        SW_TMARK(t_corner);
+        SW_TADD(12, t_prologue, t_corner);
         // the edge chains (independent of each other), one per warp: x-edge in warp 1, y-edge in
         // warp 2, z-edge in warp 3 (factored in parallel with the corner, substituted in order)
         const int warp = tid >> 5, lane = tid & 31;
@@ -429,6 +491,8 @@ __global__ void __launch_bounds__(k3::NT, 2)
             }
             if (fl) atomicOr(A.flag, 1);
         }
+        SW_TMARK(t_xs);
+        SW_TADD(13, t_sets, t_xs);
         // (b) all other nodes: lane (j, k) owns the x-line and updates node i = s - j - k at step
         //     s; S and B arrive from lanes l-1 and l-T1 by shuffles, and so do the partner values
         //     of the y- and z-face sheets (which each lane on such a face carries in registers).
@@ -579,6 +643,10 @@ __global__ void __launch_bounds__(k3::NT, 2)
     SW_TADD(3, t_sets, t_levels);
     SW_TADD(4, t_levels, t_end);
     SW_TADD(5, 0, 1);
+    SW_TADD(8, t_staged, t_p1);
+    SW_TADD(9, t_p1, t_p2);
+    SW_TADD(10, t_p2, t_p3);
+    SW_TADD(11, t_p3, t_prologue);
 }
 
 inline bool encode_3d(CUtensorMap *m, const double *base, const int64_t pad[3], int b0, int b1, int b2) {
