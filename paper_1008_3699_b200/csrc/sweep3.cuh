@@ -324,29 +324,44 @@ __global__ void __launch_bounds__(k3::NT, 2)
             tma_load_3d(C2, &tf2, tx * T0, ty * T1, tz * T2, &bar);
         }
     }
-    __syncthreads();
-    // right-hand sides (SOR: b) or 1/D~ (ILU) of the active nodes: issued before waiting for the window
+    // right-hand sides (SOR: b) or 1/D~ (ILU) of the active nodes: issued before waiting for the
+    // window (and before the barrier that publishes the mbarrier, so thread 0's TMA issue overlaps)
     const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1, NE = E0 * E1 * E2;   // local [-1, T) per axis
     // pass 1 (below): every active node's r0 and couplings into registers (reads faces from the
     // coupling arrays and x_old from the window); pass 2, after a barrier: write them in place
     double r0v[k3::KMAX], cv[k3::KMAX][3];
-    int wv[k3::KMAX];
+    int wv[k3::KMAX], lp[k3::KMAX];             // window word (-1: none) and packed local coordinates
     double auxv[k3::KMAX];
+    {
+        // e = tid + it * NT walks the extended box; (l0, l1, l2) advance by the constant step
+        // (a0, a1, a2) = NT in mixed radix (E0, E1, E2) -- no divisions inside the loop
+        int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
+        const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
 #pragma unroll
-    for (int it = 0; it < k3::KMAX; ++it) {     // aux loads first (coalesced along x)
-        const int e = tid + it * k3::NT;
-        auxv[it] = 0.0;
-        wv[it] = -1;
-        if (e >= NE) continue;
-        const int l0 = e % E0 - 1, l1 = (e / E0) % E1 - 1, l2 = e / (E0 * E1) - 1;
-        const int L = (l0 < 0 ? 1 : 0) | (l1 < 0 ? 2 : 0) | (l2 < 0 ? 4 : 0);
-        if ((L & cb) != L) continue;                      // not an active node
-        const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - l0 : l0);
-        const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - l1 : l1);
-        const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - l2 : l2);
-        wv[it] = w0 + W0 * (w1 + W1 * w2);
-        if (!A.tri || A.invd_mode) auxv[it] = A.aux[gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01];
+        for (int it = 0; it < k3::KMAX; ++it) {     // aux loads first (coalesced along x)
+            auxv[it] = 0.0;
+            wv[it] = -1;
+            lp[it] = l0 | (l1 << 8) | (l2 << 16);
+            const int m0 = l0 - 1, m1 = l1 - 1, m2 = l2 - 1;
+            const int L = (m0 < 0 ? 1 : 0) | (m1 < 0 ? 2 : 0) | (m2 < 0 ? 4 : 0);
+            if (l2 < E2 && (L & cb) == L) {                      // an active node
+                const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - m0 : m0);
+                const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - m1 : m1);
+                const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - m2 : m2);
+                wv[it] = w0 + W0 * (w1 + W1 * w2);
+                if (!A.tri || A.invd_mode) auxv[it] = A.aux[gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01];
+            }
+            l0 += a0;
+            const int c0 = l0 >= E0;
+            l0 -= c0 ? E0 : 0;
+            l1 += a1 + c0;
+            const int c1 = l1 >= E1;
+            l1 -= c1 ? E1 : 0;
+            l2 += a2 + c1;
+        }
     }
+    (void)NE;
+    __syncthreads();                              // the mbarrier is initialised
     mbar_wait(&bar, 0);
     SW_TMARK(t_staged);
 
@@ -356,8 +371,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
     for (int it = 0; it < k3::KMAX; ++it) {
         const int w = wv[it];
         if (w < 0) continue;
-        const int e = tid + it * k3::NT;
-        const int lv[3] = {e % E0 - 1, (e / E0) % E1 - 1, e / (E0 * E1) - 1};
+        const int lv[3] = {(lp[it] & 255) - 1, ((lp[it] >> 8) & 255) - 1, (lp[it] >> 16) - 1};
         const int L = (lv[0] < 0 ? 1 : 0) | (lv[1] < 0 ? 2 : 0) | (lv[2] < 0 ? 4 : 0);
         double f[3][2];
 #pragma unroll
