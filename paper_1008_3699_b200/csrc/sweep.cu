@@ -75,8 +75,7 @@ static const CUtensorMap *get_map(sw_grid *g, const double *ptr, int box) {
     sw_grid::MapEntry e;
     e.ptr = ptr;
     e.box = box;
-    const bool ok = (g->dim == 3) ? encode_3d(&e.map, ptr, g->pad, g->tile[0] + 4, g->tile[1] + 4, g->tile[2] + 4)
-                                  : encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box);
+    const bool ok = g->dim == 2 && encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box);
     if (!ok) return nullptr;
     if (g->mapcache.size() > 32) g->mapcache.pop_front();   // never one of the (<= 3) maps of the current call
     g->mapcache.push_back(e);
@@ -437,15 +436,11 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2v launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
-            const CUtensorMap *mx = get_map(g, xo, 0);
-            const CUtensorMap *m0 = g->G.poisson ? mx : get_map(g, g->F[0], 0);
-            const CUtensorMap *m1 = g->G.poisson ? mx : get_map(g, g->F[1], 0);
-            const CUtensorMap *m2 = g->G.poisson ? mx : get_map(g, g->F[2], 0);
-            if (!mx || !m0 || !m1 || !m2) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
             Sweep3Args A3{};
             A3.G = g->G;
             A3.base = base;
             for (int i = 0; i < 8; ++i) A3.omega[i] = w8[i];
+            A3.xin = xo;
             A3.aux = g->B;
             A3.f0 = g->G.poisson ? nullptr : g->F[0];
             A3.f1 = g->G.poisson ? nullptr : g->F[1];
@@ -453,7 +448,7 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             A3.out = xn;
             A3.flag = g->flag;
             A3.couple = 1;
-            cudaError_t e = launch_sweep3(*mx, *m0, *m1, *m2, A3, cs);
+            cudaError_t e = launch_sweep3(A3, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
         } else if (g->dim == 2 && g->fast2d && g->maps.ok) {
@@ -578,14 +573,10 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     if (stage <= 1 && g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
         // 3D engine for the two forward-type solves
         const double *src = stage == 0 ? r : g->Y;
-        const CUtensorMap *ms = get_map(g, src, 0);
-        const CUtensorMap *m0 = g->G.poisson ? ms : get_map(g, g->F[0], 0);
-        const CUtensorMap *m1 = g->G.poisson ? ms : get_map(g, g->F[1], 0);
-        const CUtensorMap *m2 = g->G.poisson ? ms : get_map(g, g->F[2], 0);
-        if (!ms || !m0 || !m1 || !m2) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
         Sweep3Args A3{};
         A3.G = g->G;
         for (int i = 0; i < 8; ++i) A3.omega[i] = omega;
+        A3.xin = src;
         A3.aux = invd;
         A3.f0 = g->G.poisson ? nullptr : g->F[0];
         A3.f1 = g->G.poisson ? nullptr : g->F[1];
@@ -598,7 +589,7 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
         } else {
             A3.base = rev; A3.rscale = 0; A3.coef = coef; A3.couple = pairing == SW_PAIR_PAPER; A3.out = z;
         }
-        cudaError_t e = launch_sweep3(*ms, *m0, *m1, *m2, A3, s);
+        cudaError_t e = launch_sweep3(A3, s);
         g->launches++;
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
         return SW_OK;

@@ -1,32 +1,33 @@
 // sweep3.cuh -- 3D decomposed SOR sweep and block-triangular solves (7-point stencil), any box
 // T0 x T1 x T2 whose window fits in shared memory, sm_100a.
 //
-// One CTA (4 warps) per box.  Shared memory holds four arrays over the (T+4)^3 window (global
-// orientation): X (x_old / src, then r0, then the results, in place) and C0, C1, C2, the coupling
-// alpha c of every active node toward its implicit side along x, y, z.  Active nodes are the
-// box's own nodes and the partner layers across its coupled start faces (the other members of
-// the coupled 2x2 / 4x4 / 8x8 systems), recomputed redundantly by both boxes.
-//  1. Stage-in: one 3D TMA load of the window of x_old (SOR) or src (triangular solves).
-//  2. Prologue (all warps): r0 and the three couplings of every active node (DESIGN R-7), one
-//     branch-free correctly rounded division per node.
-//  3. Sets of two or more coupled faces (thread 0 the corner, then one thread per edge chain):
-//     Gaussian elimination without pivoting in ascending global index (DESIGN R-8).
-//  4. Level loop (warp 0): at level d every line (j, k) updates its node (d - j - k, j, k); a node
-//     on one coupled face solves its 2 x 2 pair with the partner layer.  __syncwarp per level.
-//  5. Write-back of the box.
+// One CTA (4 warps) per box, four CTAs per SM.  Shared memory holds four compact arrays over
+// the extended box [-1, T) per axis in LOCAL coordinates (local +a points away from the box's
+// start corner): X (r0, then the results, in place) and C0, C1, C2, the coupling alpha c of
+// every active node toward its implicit side along x, y, z.  Active nodes are the box's own
+// nodes and the partner layers across its coupled start faces (the other members of the coupled
+// 2x2 / 4x4 / 8x8 systems), recomputed redundantly by both boxes.
+//  1. Prologue (all warps): r0 and the three couplings of every active node (DESIGN R-7) from
+//     x_old / src, b / 1/D~ and the faces read straight from global memory (no halo window: the
+//     3D halo is 3.4x the box), one branch-free correctly rounded division per node; pair pivots.
+//  2. Sets of two or more coupled faces: the 8 x 8 corner by 8 lanes, the 4 x 4 edge chains by
+//     one warp each (factored in parallel, substituted in order); Gaussian elimination without
+//     pivoting in ascending global index (DESIGN R-8).
+//  3. Level loop (warp 0): the x-face sheet, then a branch-free shuffle wavefront in which lane
+//     (j, k) owns the x-line and updates node (s - j - k, j, k) at step s; a node on one coupled
+//     face solves its 2 x 2 pair with the partner layer.
+//  4. Write-back of the box, coalesced along x.
 // Same operations and order as the oracle, so the result is bitwise identical to it.
 #pragma once
 #include <cuda.h>
 
 #include "common.cuh"
 #include "sweep2p.cuh"
-#include "tma.cuh"
 
 namespace sw {
 
 namespace k3 {
-constexpr int NT = 256;        // threads per CTA
-constexpr int KMAX = 8;        // prologue nodes per thread: (T0+1)(T1+1)(T2+1) <= NT * KMAX
+constexpr int NT = 128;        // threads per CTA
 constexpr int MAXLINES = 64;   // T1 * T2
 }  // namespace k3
 
@@ -34,6 +35,7 @@ struct Sweep3Args {
     Geo G;
     int base;
     double omega[8];
+    const double *xin;          // x_old (SOR) or the solve's source array
     const double *aux;          // b (SOR) or 1/D~ (ILU) or null
     const double *f0, *f1, *f2; // face arrays or null (unit)
     double *out;
@@ -41,14 +43,6 @@ struct Sweep3Args {
     double coef;
     int tri, invd_mode, rscale, couple;
 };
-
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-            smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // Solve one coupled set on the axes AXES (K = 2^popcount members) whose own member sits at
 // window word w.  Member S (bit t set = across the t-th set axis) is w - sum_t st[ax_t]; in
@@ -272,17 +266,18 @@ __device__ int sw_dbg3_block = -1;
 #endif
 
 template <bool FACES>
-__global__ void __launch_bounds__(k3::NT, 2)
-    k_sweep3(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tf0,
-             const __grid_constant__ CUtensorMap tf1, const __grid_constant__ CUtensorMap tf2, Sweep3Args A) {
+__global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     extern __shared__ __align__(128) double sm[];
-    __shared__ uint64_t bar;
     const Geo &G = A.G;
     const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
-    const int W0 = T0 + 4, W1 = T1 + 4, W2 = T2 + 4;
-    const int WS = W0 * W1 * W2;
-    double *X = sm;
+    // compact arrays over the extended box [-1, T) per axis in LOCAL coordinates (sweep order:
+    // local +a points away from the box's start corner), so every step below is positive
+    const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1;
+    const int WS = E0 * E1 * E2;
+    double *const X = sm;                               // r0 of the active nodes, then their results
     double *const C0 = sm + WS, *const C1 = sm + 2 * WS, *const C2 = sm + 3 * WS;
+    double *const PV = sm + 4 * WS;                     // pair pivots: y-face sheet [T2][T0], z-face [T1][T0]
+    double *const SCR = PV + T0 * (T1 + T2);            // corner elimination scratch (80 doubles)
     auto CC = [&](int a, int w) -> double & { return sm[(a + 1) * WS + w]; };   // coupling of axis a
     const int tid = threadIdx.x;
     // box, direction bits, coupled start faces
@@ -298,59 +293,77 @@ __global__ void __launch_bounds__(k3::NT, 2)
         sb |= s << a;
         cb |= (int)c << a;
     }
-    const int Tv[3] = {T0, T1, T2}, Sv[3] = {1, W0, W0 * W1};
-    int st[3];          // window step of local +a
-#pragma unroll
-    for (int a = 0; a < 3; ++a) st[a] = ((sb >> a) & 1) ? -Sv[a] : Sv[a];
-    auto wof = [&](int l0, int l1, int l2) {   // window word of local coordinates
-        const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - l0 : l0);
-        const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - l1 : l1);
-        const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - l2 : l2);
-        return w0 + W0 * (w1 + W1 * w2);
-    };
+    const int st[3] = {1, E0, E0 * E1};               // compact step of local +a
+    auto wof = [&](int l0, int l1, int l2) { return (l0 + 1) + E0 * ((l1 + 1) + E1 * (l2 + 1)); };
     const int64_t P0 = G.P0, P01 = G.P01;
-    const int64_t gbase = (int64_t)tz * T2 * P01 + (int64_t)ty * T1 * P0 + (int64_t)tx * T0;   // padded index of window word 0
+    const int64_t gbase = (int64_t)tz * T2 * P01 + (int64_t)ty * T1 * P0 + (int64_t)tx * T0;   // padded (box min - 2)
+    const int64_t Sg[3] = {1, P0, P01};
 
     SW_TMARK(t_start);
-    // ---------------------------------------------------------------- 1. stage-in
-    if (tid == 0) {
-        mbar_init(&bar, 1);
-        fence_mbar_init();
-        mbar_expect_tx(&bar, (uint32_t)(sizeof(double) * WS * (FACES ? 4 : 1)));
-        tma_load_3d(X, &tmx, tx * T0, ty * T1, tz * T2, &bar);
-        if (FACES) {   // face windows land in the coupling arrays and are converted in place
-            tma_load_3d(C0, &tf0, tx * T0, ty * T1, tz * T2, &bar);
-            tma_load_3d(C1, &tf1, tx * T0, ty * T1, tz * T2, &bar);
-            tma_load_3d(C2, &tf2, tx * T0, ty * T1, tz * T2, &bar);
-        }
-    }
-    // right-hand sides (SOR: b) or 1/D~ (ILU) of the active nodes: issued before waiting for the
-    // window (and before the barrier that publishes the mbarrier, so thread 0's TMA issue overlaps)
-    const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1, NE = E0 * E1 * E2;   // local [-1, T) per axis
-    // pass 1 (below): every active node's r0 and couplings into registers (reads faces from the
-    // coupling arrays and x_old from the window); pass 2, after a barrier: write them in place
-    double r0v[k3::KMAX], cv[k3::KMAX][3];
-    int wv[k3::KMAX], lp[k3::KMAX];             // window word (-1: none) and packed local coordinates
-    double auxv[k3::KMAX];
+    // ---------------------------------------------------------------- 1. prologue
+    // Every node of the extended box: r0 and the couplings alpha c toward its implicit side of the
+    // active nodes (own nodes and the partner layers across coupled start faces, DESIGN R-7), zero
+    // for the rest (the layers across uncoupled faces are read only through zero couplings).
+    // x_old / src, b / 1/D~ and the faces come straight from global memory (L1/L2: neighbouring
+    // boxes share their halos), coalesced along x; the loop walks e = (l0, l1, l2) in mixed radix.
     {
-        // e = tid + it * NT walks the extended box; (l0, l1, l2) advance by the constant step
-        // (a0, a1, a2) = NT in mixed radix (E0, E1, E2) -- no divisions inside the loop
+        const double *__restrict__ xin = A.xin;
+        const double *__restrict__ aux = A.aux;
+        const double *__restrict__ F0 = A.f0, *__restrict__ F1 = A.f1, *__restrict__ F2 = A.f2;
         int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
         const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
+#pragma unroll 3
+        for (int e = tid; e < WS; e += k3::NT) {
+            const int lv[3] = {l0 - 1, l1 - 1, l2 - 1};
+            const int L = (lv[0] < 0 ? 1 : 0) | (lv[1] < 0 ? 2 : 0) | (lv[2] < 0 ? 4 : 0);
+            double r0 = 0.0, c[3] = {0.0, 0.0, 0.0};
+            if ((L & cb) == L) {
+                const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - lv[0] : lv[0]);
+                const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - lv[1] : lv[1]);
+                const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - lv[2] : lv[2]);
+                const int64_t g = gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01;
+                double f[3][2];
+                if (FACES) {
+                    f[0][0] = __ldg(F0 + g); f[0][1] = __ldg(F0 + g + 1);
+                    f[1][0] = __ldg(F1 + g); f[1][1] = __ldg(F1 + g + P0);
+                    f[2][0] = __ldg(F2 + g); f[2][1] = __ldg(F2 + g + P01);
+                } else {
 #pragma unroll
-        for (int it = 0; it < k3::KMAX; ++it) {     // aux loads first (coalesced along x)
-            auxv[it] = 0.0;
-            wv[it] = -1;
-            lp[it] = l0 | (l1 << 8) | (l2 << 16);
-            const int m0 = l0 - 1, m1 = l1 - 1, m2 = l2 - 1;
-            const int L = (m0 < 0 ? 1 : 0) | (m1 < 0 ? 2 : 0) | (m2 < 0 ? 4 : 0);
-            if (l2 < E2 && (L & cb) == L) {                      // an active node
-                const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - m0 : m0);
-                const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - m1 : m1);
-                const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - m2 : m2);
-                wv[it] = w0 + W0 * (w1 + W1 * w2);
-                if (!A.tri || A.invd_mode) auxv[it] = A.aux[gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01];
+                    for (int a = 0; a < 3; ++a) f[a][0] = f[a][1] = 1.0;
+                }
+                const double ap = (((f[0][0] + f[0][1]) + (f[1][0] + f[1][1])) + (f[2][0] + f[2][1])) + G.beta;
+                bool hi[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) hi[a] = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
+                double al;
+                if (!A.tri) {
+                    const double w_ = A.omega[sb ^ L];                 // the node's own box's direction bits
+                    double xn[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) xn[a] = __ldg(xin + (hi[a] ? g - Sg[a] : g + Sg[a]));
+                    const double xo = __ldg(xin + g);
+                    double ev = __ldg(aux + g);
+                    al = div_rn(w_, ap);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) ev = fma(hi[a] ? f[a][0] : f[a][1], xn[a], ev);
+                    r0 = fma(al, ev, (1.0 - w_) * xo);
+                } else {
+                    const double sv = __ldg(xin + g);
+                    al = A.invd_mode ? __ldg(aux + g) : div_rn(A.omega[0], ap);
+                    r0 = A.rscale ? al * sv : A.coef * sv;
+                }
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    // no coupling across an uncoupled start face: the oracle omits the term (physical
+                    // boundary) and the first pass of the transposed solve must not see the neighbour box
+                    const bool cut = !((L >> a) & 1) && lv[a] == 0 && !((cb >> a) & 1);
+                    c[a] = cut ? 0.0 : al * (hi[a] ? f[a][1] : f[a][0]);
+                }
             }
+            X[e] = r0;
+            C0[e] = c[0];
+            C1[e] = c[1];
+            C2[e] = c[2];
             l0 += a0;
             const int c0 = l0 >= E0;
             l0 -= c0 ? E0 : 0;
@@ -360,98 +373,35 @@ __global__ void __launch_bounds__(k3::NT, 2)
             l2 += a2 + c1;
         }
     }
-    (void)NE;
-    __syncthreads();                              // the mbarrier is initialised
-    mbar_wait(&bar, 0);
-    SW_TMARK(t_staged);
-
-    // ---------------------------------------------------------------- 2. prologue
-    SW_TMARK(t_p1);
-#pragma unroll
-    for (int it = 0; it < k3::KMAX; ++it) {
-        const int w = wv[it];
-        if (w < 0) continue;
-        const int lv[3] = {(lp[it] & 255) - 1, ((lp[it] >> 8) & 255) - 1, (lp[it] >> 16) - 1};
-        const int L = (lv[0] < 0 ? 1 : 0) | (lv[1] < 0 ? 2 : 0) | (lv[2] < 0 ? 4 : 0);
-        double f[3][2];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            f[a][0] = FACES ? CC(a, w) : 1.0;
-            f[a][1] = FACES ? CC(a, w + Sv[a]) : 1.0;
-        }
-        const double ap = (((f[0][0] + f[0][1]) + (f[1][0] + f[1][1])) + (f[2][0] + f[2][1])) + G.beta;
-        const int db = sb ^ L;                             // direction bits of the node's box
-        double al, r0;
-        if (!A.tri) {
-            const double w_ = A.omega[db];
-            al = div_rn(w_, ap);
-            double ev = auxv[it];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
-                ev = fma(hi ? f[a][0] : f[a][1], X[hi ? w - Sv[a] : w + Sv[a]], ev);
-            }
-            r0 = fma(al, ev, (1.0 - w_) * X[w]);
-        } else {
-            al = A.invd_mode ? auxv[it] : div_rn(A.omega[0], ap);
-            r0 = A.rscale ? al * X[w] : A.coef * X[w];
-        }
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);
-            // no coupling across an uncoupled start face: the oracle omits the term (physical
-            // boundary) and the first pass of the transposed solve must not see the neighbour box
-            const bool cut = !((L >> a) & 1) && lv[a] == 0 && !((cb >> a) & 1);
-            cv[it][a] = cut ? 0.0 : al * (hi ? f[a][1] : f[a][0]);
-        }
-        r0v[it] = r0;
-    }
-    SW_TMARK(t_p2);
     __syncthreads();
-#pragma unroll
-    for (int it = 0; it < k3::KMAX; ++it)
-        if (wv[it] >= 0) {
-            X[wv[it]] = r0v[it];
-            C0[wv[it]] = cv[it][0];
-            C1[wv[it]] = cv[it][1];
-            C2[wv[it]] = cv[it][2];
-        }
-    __syncthreads();
-    // pivots 1 / (1 - m m') of the face pairs that the level loop solves (y- and z-face sheets),
-    // stored in the free second halo layer at local y = -2 / z = -2 of the pair
-    SW_TMARK(t_p3);
+    // pivots 1 / (1 - m m') of the face pairs that the level loop solves (y- and z-face sheets)
     const bool fast_lines = T1 * T2 <= 32;
     if (fast_lines) {
         const int ny = ((cb & 2) ? T0 * T2 : 0), nz = ((cb & 4) ? T0 * T1 : 0);
         int fl = 0;
         for (int e = tid; e < ny + nz; e += k3::NT) {
-            int i, j, k, a;
-            if (e < ny) { i = e % T0; k = e / T0; j = 0; a = 1; }
-            else { i = (e - ny) % T0; j = (e - ny) / T0; k = 0; a = 2; }
+            int i, j, k, a, pi;
+            if (e < ny) { i = e % T0; k = e / T0; j = 0; a = 1; pi = e; }
+            else { i = (e - ny) % T0; j = (e - ny) / T0; k = 0; a = 2; pi = T0 * T2 + (e - ny); }
             const int m = (i == 0 ? (cb & 1) : 0) | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
             if (__popc(m) != 1) continue;                         // sets of two or more faces: step 3
             const int w = wof(i, j, k), q = w - st[a];
             const double m11 = fma(CC(a, w), -CC(a, q), 1.0);
             fl |= !(fabs(m11) >= 1e-14);
-            X[q - st[a]] = div_rn(1.0, m11);
+            PV[pi] = div_rn(1.0, m11);
         }
         if (fl) atomicOr(A.flag, 1);
         __syncthreads();
     }
     SW_TMARK(t_prologue);
-    // ---------------------------------------------------------------- 3. corner and edge sets
+    // ---------------------------------------------------------------- 2. corner and edge sets
     const int ncpl = __popc(cb);
     if (ncpl >= 2) {
-        // one thread: the corner set, then the edge chains (a chain of 4-sets along axis c where
-        // the two other axes are coupled; its only outside dependency is the previous set)
-        // scratch: the second halo plane beyond the end z face (never read)
-        double *zscr = X + ((((sb >> 2) & 1) ? 0 : W2 - 1) * W0 * W1);
-        if (cb == 7 && W0 * W1 >= 80) {
-            if (tid < 32) corner8_coop(X, WS, zscr, tid, wof(0, 0, 0), st, sb, A.flag);
+        if (cb == 7) {
+            if (tid < 32) corner8_coop(X, WS, SCR, tid, wof(0, 0, 0), st, sb, A.flag);
         } else if (tid == 0) {
             const int w = wof(0, 0, 0);
             switch (cb) {
-                case 7: solve_set3<7>(X, WS, w, st, sb, A.flag); break;
                 case 3: solve_set3<3>(X, WS, w, st, sb, A.flag); break;
                 case 5: solve_set3<5>(X, WS, w, st, sb, A.flag); break;
                 default: solve_set3<6>(X, WS, w, st, sb, A.flag); break;
@@ -477,7 +427,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
         }
 #endif
     SW_TMARK(t_sets);
-    // ---------------------------------------------------------------- 4. level loop (warp 0)
+    // ---------------------------------------------------------------- 3. level loop (warp 0)
     if (fast_lines) {
         // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over (j, k)
         if (tid < 32 && (cb & 1)) {
@@ -512,7 +462,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
         //     of the y- and z-face sheets (which each lane on such a face carries in registers).
         //     One branch-free instruction stream for every kind of lane: a plain lane is a "pair"
         //     with zero couplings and unit pivot, which leaves its node formula exact; the x-edge
-        //     lane (solved in step 3) only reloads and forwards its values.
+        //     lane (solved in step 2) only reloads and forwards its values.
         if (tid < 32) {
             const int lane = tid, nl = T1 * T2;
             const bool on = lane < nl;
@@ -523,6 +473,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
             const int sx = st[0], sy = st[1], sz = st[2];
             const int sa = ypair ? sy : (zpair ? sz : 0);                 // step toward the pair partner
             const int wl = wof(0, j, k);
+            const int pvb = ypair ? T0 * k : T0 * T2 + T0 * j;           // pivots of the lane's pairs
             const bool qf = pair ? (((sb >> (ypair ? 1 : 2)) & 1) == 0) : true;   // partner first in index order
             // addresses of the other transverse coupling of the partner: z for y-pairs, y for z-pairs
             const int oq_arr = ypair ? 3 : 2;                             // (axis + 1) of that coupling
@@ -543,7 +494,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
                 v[5] = sm[WS + q];              // partner C_x
                 v[6] = sm[oq_arr * WS + q];     // partner other transverse coupling
                 v[7] = sm[pa_arr * WS + q];     // partner pair coupling
-                v[8] = pair ? X[q - sa] : 1.0;  // pivot inverse (prologue)
+                v[8] = pair ? PV[pvb + i] : 1.0;  // pivot inverse (prologue)
                 v[9] = edge ? X[w - sy] : 0.0;  // edge: its y-partner value
                 v[10] = edge ? X[w - sz] : 0.0; //       its z-partner value
             };
@@ -581,11 +532,10 @@ __global__ void __launch_bounds__(k3::NT, 2)
                 pz = sel_f64(act, zpair ? pv : (edge ? v[10] : pz), pz);
             }
         }
-    } else
-    if (tid < 32) {
+    } else if (tid < 32) {
         const int nl = T1 * T2, nlev = T0 + T1 + T2 - 2;
-        // per-lane lines (at most two): offset j + k of the level, window word of node i = 0,
-        // coupled-face mask of the line (y-face if j == 0, z-face if k == 0)
+        // per-lane lines (at most two): offset j + k of the level, word of node i = 0, coupled-face
+        // mask of the line (y-face if j == 0, z-face if k == 0)
         int jk[2], wl[2], lm[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -633,7 +583,7 @@ __global__ void __launch_bounds__(k3::NT, 2)
                     X[w] = qfirst ? ub : ua;
                     X[q] = qfirst ? ua : ub;
                 }
-                // (sets on two or three faces were solved in step 3)
+                // (sets on two or three faces were solved in step 2)
             }
             __syncwarp();
         }
@@ -642,63 +592,53 @@ __global__ void __launch_bounds__(k3::NT, 2)
     __syncthreads();
     SW_TMARK(t_levels);
 
-    // ---------------------------------------------------------------- 5. write-back
-    const int nrow = T1 * T2;
-    for (int e = tid; e < nrow * T0; e += k3::NT) {
-        const int x = e % T0, row = e / T0;
-        const int w1 = 2 + row % T1, w2 = 2 + row / T1;
-        const int w = 2 + x + W0 * (w1 + W1 * w2);
-        A.out[gbase + 2 + x + (int64_t)w1 * P0 + (int64_t)w2 * P01] = X[w];
+    // ---------------------------------------------------------------- 4. write-back of the box
+    {
+        const int n = T0 * T1 * T2;
+        int l0 = tid % T0, l1 = (tid / T0) % T1, l2 = tid / (T0 * T1);
+        const int a0 = k3::NT % T0, a1 = (k3::NT / T0) % T1, a2 = k3::NT / (T0 * T1);
+        for (int e = tid; e < n; e += k3::NT) {
+            const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - l0 : l0);
+            const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - l1 : l1);
+            const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - l2 : l2);
+            A.out[gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01] = X[wof(l0, l1, l2)];
+            l0 += a0;
+            const int c0 = l0 >= T0;
+            l0 -= c0 ? T0 : 0;
+            l1 += a1 + c0;
+            const int c1 = l1 >= T1;
+            l1 -= c1 ? T1 : 0;
+            l2 += a2 + c1;
+        }
     }
     SW_TMARK(t_end);
-    SW_TADD(0, t_start, t_staged);
-    SW_TADD(1, t_staged, t_prologue);
+    SW_TADD(1, t_start, t_prologue);
     SW_TADD(2, t_prologue, t_sets);
     SW_TADD(3, t_sets, t_levels);
     SW_TADD(4, t_levels, t_end);
     SW_TADD(5, 0, 1);
-    SW_TADD(8, t_staged, t_p1);
-    SW_TADD(9, t_p1, t_p2);
-    SW_TADD(10, t_p2, t_p3);
-    SW_TADD(11, t_p3, t_prologue);
-}
-
-inline bool encode_3d(CUtensorMap *m, const double *base, const int64_t pad[3], int b0, int b1, int b2) {
-    EncodeTiledFn enc = get_encode();
-    if (!enc || !base) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)pad[0], (cuuint64_t)pad[1], (cuuint64_t)pad[2]};
-    cuuint64_t strides[2] = {(cuuint64_t)(pad[0] * sizeof(double)), (cuuint64_t)(pad[0] * pad[1] * sizeof(double))};
-    cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
 }
 
 inline size_t sweep3_smem(const Geo &G) {
-    return sizeof(double) * 4 * (size_t)(G.T[0] + 4) * (G.T[1] + 4) * (G.T[2] + 4);
+    const size_t ws = (size_t)(G.T[0] + 1) * (G.T[1] + 1) * (G.T[2] + 1);
+    return sizeof(double) * (4 * ws + (size_t)G.T[0] * (G.T[1] + G.T[2]) + 80);
 }
 
-// the fast 3D path handles boxes whose window fits and whose extended box fits the prologue
+// the fast 3D path handles boxes whose compact arrays fit in shared memory
 inline bool sweep3_supported(const Geo &G) {
     if (G.dim != 3) return false;
-    const int64_t ne = (int64_t)(G.T[0] + 1) * (G.T[1] + 1) * (G.T[2] + 1);
-    return (G.T[0] % 2 == 0) && G.T[0] + 4 <= 256 && G.T[1] + 4 <= 256 && G.T[2] + 4 <= 256 &&
-           sweep3_smem(G) <= 227 * 1024 && ne <= (int64_t)k3::NT * k3::KMAX && G.T[1] * G.T[2] <= k3::MAXLINES &&
-           G.T[0] <= 33 && G.T[1] <= 33 && G.T[2] <= 33 &&
-           G.off[0] == 0 && G.off[1] == 0;
+    return (G.T[0] % 2 == 0) && sweep3_smem(G) <= 227 * 1024 && G.T[1] * G.T[2] <= k3::MAXLINES &&
+           G.T[0] <= 33 && G.T[1] <= 33 && G.T[2] <= 33 && G.off[0] == 0 && G.off[1] == 0;
 }
 
-inline cudaError_t launch_sweep3(const CUtensorMap &tmx, const CUtensorMap &tf0, const CUtensorMap &tf1,
-                                 const CUtensorMap &tf2, const Sweep3Args &A, cudaStream_t s) {
+inline cudaError_t launch_sweep3(const Sweep3Args &A, cudaStream_t s) {
     const size_t smem = sweep3_smem(A.G);
     const bool faces = A.f0 != nullptr;
     if (faces) cudaFuncSetAttribute(k_sweep3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     else cudaFuncSetAttribute(k_sweep3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1] * A.G.nt[2]);
-    if (faces) k_sweep3<true><<<tiles, k3::NT, smem, s>>>(tmx, tf0, tf1, tf2, A);
-    else k_sweep3<false><<<tiles, k3::NT, smem, s>>>(tmx, tf0, tf1, tf2, A);
+    if (faces) k_sweep3<true><<<tiles, k3::NT, smem, s>>>(A);
+    else k_sweep3<false><<<tiles, k3::NT, smem, s>>>(A);
     return cudaGetLastError();
 }
 
