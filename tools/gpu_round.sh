@@ -12,7 +12,7 @@ timeout 900 python -m pytest tests -m gpu -x -q --timeout 180 > $OUT/pytest_gpu.
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?"; tail -2 $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?"; cat $OUT/bench.json
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref exit $?"; cat $OUT/bench_ref.json
-CMD="python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu"
+CMD="python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu --no-secondary"
 timeout 300 $CMD > $OUT/plain_launch.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "ncu launches exit $?"

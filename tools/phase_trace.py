@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1008_3699_b200 import binding, gen  # noqa: E402
 
 NAMES = ["stage-in wait", "partner+prologue", "corner+chains", "wavefront", "write-back", "", "chains (warp 1)",
-         "wavefront (warp 0)", "3D: aux loads", "3D: prologue pass 1", "3D: write-back of r0/C", "3D: pivots",
+         "wavefront (warp 0)", "3D: prologue (thr 0, own part)", "3D: wavefront (thr 0, no barrier)", "", "",
          "3D: corner (thr 0)", "3D: x-sheet"]
 
 
