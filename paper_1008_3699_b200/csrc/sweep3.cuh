@@ -312,67 +312,92 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         const double *__restrict__ F0 = A.f0, *__restrict__ F1 = A.f1, *__restrict__ F2 = A.f2;
         int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
         const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
-#pragma unroll 3
-        for (int e = tid; e < WS; e += k3::NT) {
-            const int lv[3] = {l0 - 1, l1 - 1, l2 - 1};
-            const int L = (lv[0] < 0 ? 1 : 0) | (lv[1] < 0 ? 2 : 0) | (lv[2] < 0 ? 4 : 0);
-            double r0 = 0.0, c[3] = {0.0, 0.0, 0.0};
-            if ((L & cb) == L) {
-                const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - lv[0] : lv[0]);
-                const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - lv[1] : lv[1]);
-                const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - lv[2] : lv[2]);
-                const int64_t g = gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01;
-                double f[3][2];
+        const bool need_x = !A.tri, need_aux = !A.tri || A.invd_mode;
+        constexpr int KB = 3;      // nodes per batch: all their loads are issued before any use
+        for (int e0 = tid; e0 < WS; e0 += KB * k3::NT) {
+            int lvv[KB][3], Lm[KB];
+            bool on[KB];
+            int64_t gg[KB];
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+                lvv[kb][0] = l0 - 1; lvv[kb][1] = l1 - 1; lvv[kb][2] = l2 - 1;
+                const int L = (l0 < 1 ? 1 : 0) | (l1 < 1 ? 2 : 0) | (l2 < 1 ? 4 : 0);
+                Lm[kb] = L;
+                on[kb] = l2 < E2 && (L & cb) == L;
+                const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - lvv[kb][0] : lvv[kb][0]);
+                const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - lvv[kb][1] : lvv[kb][1]);
+                const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - lvv[kb][2] : lvv[kb][2]);
+                // inactive nodes load from the box's first node (always inside the padded array)
+                gg[kb] = on[kb] ? gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01 : gbase + 2 + 2 * P0 + 2 * P01;
+                l0 += a0;
+                const int c0 = l0 >= E0;
+                l0 -= c0 ? E0 : 0;
+                l1 += a1 + c0;
+                const int c1 = l1 >= E1;
+                l1 -= c1 ? E1 : 0;
+                l2 += a2 + c1;
+            }
+            double f[KB][3][2], xn[KB][3], xo[KB], av[KB];
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+                const int64_t g = gg[kb];
                 if (FACES) {
-                    f[0][0] = __ldg(F0 + g); f[0][1] = __ldg(F0 + g + 1);
-                    f[1][0] = __ldg(F1 + g); f[1][1] = __ldg(F1 + g + P0);
-                    f[2][0] = __ldg(F2 + g); f[2][1] = __ldg(F2 + g + P01);
+                    f[kb][0][0] = __ldg(F0 + g); f[kb][0][1] = __ldg(F0 + g + 1);
+                    f[kb][1][0] = __ldg(F1 + g); f[kb][1][1] = __ldg(F1 + g + P0);
+                    f[kb][2][0] = __ldg(F2 + g); f[kb][2][1] = __ldg(F2 + g + P01);
                 } else {
 #pragma unroll
-                    for (int a = 0; a < 3; ++a) f[a][0] = f[a][1] = 1.0;
+                    for (int a = 0; a < 3; ++a) f[kb][a][0] = f[kb][a][1] = 1.0;
                 }
-                const double ap = (((f[0][0] + f[0][1]) + (f[1][0] + f[1][1])) + (f[2][0] + f[2][1])) + G.beta;
-                bool hi[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) hi[a] = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
-                double al;
-                if (!A.tri) {
-                    const double w_ = A.omega[sb ^ L];                 // the node's own box's direction bits
-                    double xn[3];
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) xn[a] = __ldg(xin + (hi[a] ? g - Sg[a] : g + Sg[a]));
-                    const double xo = __ldg(xin + g);
-                    double ev = __ldg(aux + g);
-                    al = div_rn(w_, ap);
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) ev = fma(hi[a] ? f[a][0] : f[a][1], xn[a], ev);
-                    r0 = fma(al, ev, (1.0 - w_) * xo);
-                } else {
-                    const double sv = __ldg(xin + g);
-                    al = A.invd_mode ? __ldg(aux + g) : div_rn(A.omega[0], ap);
-                    r0 = A.rscale ? al * sv : A.coef * sv;
-                }
+                xo[kb] = __ldg(xin + g);
+                av[kb] = need_aux ? __ldg(aux + g) : 0.0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    // no coupling across an uncoupled start face: the oracle omits the term (physical
-                    // boundary) and the first pass of the transposed solve must not see the neighbour box
-                    const bool cut = !((L >> a) & 1) && lv[a] == 0 && !((cb >> a) & 1);
-                    c[a] = cut ? 0.0 : al * (hi[a] ? f[a][1] : f[a][0]);
+                    const bool hi = (((Lm[kb] >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
+                    xn[kb][a] = need_x ? __ldg(xin + (hi ? g - Sg[a] : g + Sg[a])) : 0.0;
                 }
             }
-            X[e] = r0;
-            C0[e] = c[0];
-            C1[e] = c[1];
-            C2[e] = c[2];
-            l0 += a0;
-            const int c0 = l0 >= E0;
-            l0 -= c0 ? E0 : 0;
-            l1 += a1 + c0;
-            const int c1 = l1 >= E1;
-            l1 -= c1 ? E1 : 0;
-            l2 += a2 + c1;
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+                const int e = e0 + kb * k3::NT;
+                if (e >= WS) break;
+                const int L = Lm[kb];
+                double r0 = 0.0, c[3] = {0.0, 0.0, 0.0};
+                if (on[kb]) {
+                    const double(&fk)[3][2] = f[kb];
+                    const double ap = (((fk[0][0] + fk[0][1]) + (fk[1][0] + fk[1][1])) + (fk[2][0] + fk[2][1])) + G.beta;
+                    bool hi[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) hi[a] = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);
+                    double al;
+                    if (!A.tri) {
+                        const double w_ = A.omega[sb ^ L];             // the node's own box's direction bits
+                        al = div_rn(w_, ap);
+                        double ev = av[kb];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) ev = fma(hi[a] ? fk[a][0] : fk[a][1], xn[kb][a], ev);
+                        r0 = fma(al, ev, (1.0 - w_) * xo[kb]);
+                    } else {
+                        al = A.invd_mode ? av[kb] : div_rn(A.omega[0], ap);
+                        r0 = A.rscale ? al * xo[kb] : A.coef * xo[kb];
+                    }
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        // no coupling across an uncoupled start face: the oracle omits the term (physical
+                        // boundary) and the first pass of the transposed solve must not see the neighbour box
+                        const bool cut = !((L >> a) & 1) && lvv[kb][a] == 0 && !((cb >> a) & 1);
+                        c[a] = cut ? 0.0 : al * (hi[a] ? fk[a][1] : fk[a][0]);
+                    }
+                }
+                X[e] = r0;
+                C0[e] = c[0];
+                C1[e] = c[1];
+                C2[e] = c[2];
+            }
         }
     }
+    SW_TMARK(t_pro_own);
+    SW_TADD(8, t_start, t_pro_own);
     __syncthreads();
     // pivots 1 / (1 - m m') of the face pairs that the level loop solves (y- and z-face sheets)
     const bool fast_lines = T1 * T2 <= 32;
@@ -394,12 +419,13 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         __syncthreads();
     }
     SW_TMARK(t_prologue);
+    const int lt = tid;
     // ---------------------------------------------------------------- 2. corner and edge sets
     const int ncpl = __popc(cb);
     if (ncpl >= 2) {
         if (cb == 7) {
-            if (tid < 32) corner8_coop(X, WS, SCR, tid, wof(0, 0, 0), st, sb, A.flag);
-        } else if (tid == 0) {
+            if (lt < 32) corner8_coop(X, WS, SCR, lt, wof(0, 0, 0), st, sb, A.flag);
+        } else if (lt == 0) {
             const int w = wof(0, 0, 0);
             switch (cb) {
                 case 3: solve_set3<3>(X, WS, w, st, sb, A.flag); break;
@@ -408,10 +434,10 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
             }
         }
         SW_TMARK(t_corner);
-        SW_TADD(12, t_prologue, t_corner);
+        SW_TADDT(12, t_prologue, t_corner, 0);
         // the edge chains (independent of each other), one per warp: x-edge in warp 1, y-edge in
         // warp 2, z-edge in warp 3 (factored in parallel with the corner, substituted in order)
-        const int warp = tid >> 5, lane = tid & 31;
+        const int warp = lt >> 5, lane = lt & 31;
         if (warp == 1) edge_chain<6>(X, WS, lane, T0, wof(1, 0, 0), st[0], st, sb, A.flag, (cb & 6) == 6);
         else if (warp == 2) edge_chain<5>(X, WS, lane, T1, wof(0, 1, 0), st[1], st, sb, A.flag, (cb & 5) == 5);
         else if (warp == 3) edge_chain<3>(X, WS, lane, T2, wof(0, 0, 1), st[2], st, sb, A.flag, (cb & 3) == 3);
@@ -430,9 +456,9 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     // ---------------------------------------------------------------- 3. level loop (warp 0)
     if (fast_lines) {
         // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over (j, k)
-        if (tid < 32 && (cb & 1)) {
-            const int j = tid % T1, k = tid / T1;
-            const bool on = tid < T1 * T2;
+        if (lt < 32 && (cb & 1)) {
+            const int j = lt % T1, k = lt / T1;
+            const bool on = lt < T1 * T2;
             const int m = 1 | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
             const int w = on ? wof(0, j, k) : 0, q = w - st[0];
             int fl = 0;
@@ -456,15 +482,15 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
             if (fl) atomicOr(A.flag, 1);
         }
         SW_TMARK(t_xs);
-        SW_TADD(13, t_sets, t_xs);
+        SW_TADDT(13, t_sets, t_xs, 0);
         // (b) all other nodes: lane (j, k) owns the x-line and updates node i = s - j - k at step
         //     s; S and B arrive from lanes l-1 and l-T1 by shuffles, and so do the partner values
         //     of the y- and z-face sheets (which each lane on such a face carries in registers).
         //     One branch-free instruction stream for every kind of lane: a plain lane is a "pair"
         //     with zero couplings and unit pivot, which leaves its node formula exact; the x-edge
         //     lane (solved in step 2) only reloads and forwards its values.
-        if (tid < 32) {
-            const int lane = tid, nl = T1 * T2;
+        if (lt < 32) {
+            const int lane = lt, nl = T1 * T2;
             const bool on = lane < nl;
             const int j = on ? lane % T1 : 0, k = on ? lane / T1 : 0;
             const bool yc = j == 0 && (cb & 2), zc = k == 0 && (cb & 4);
@@ -531,15 +557,17 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                 py = sel_f64(act, ypair ? pv : (edge ? v[9] : py), py);
                 pz = sel_f64(act, zpair ? pv : (edge ? v[10] : pz), pz);
             }
+            SW_TMARK(t_wf);
+            SW_TADDT(9, t_xs, t_wf, 0);
         }
-    } else if (tid < 32) {
+    } else if (lt < 32) {
         const int nl = T1 * T2, nlev = T0 + T1 + T2 - 2;
         // per-lane lines (at most two): offset j + k of the level, word of node i = 0, coupled-face
         // mask of the line (y-face if j == 0, z-face if k == 0)
         int jk[2], wl[2], lm[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int ln = tid + 32 * h;
+            const int ln = lt + 32 * h;
             const int j = ln % T1, k = ln / T1;
             jk[h] = (ln < nl) ? j + k : (1 << 20);          // never active
             wl[h] = wof(0, ln < nl ? j : 0, ln < nl ? k : 0);
