@@ -42,6 +42,25 @@ struct Sweep3Args {
     int *flag;
     double coef;
     int tri, invd_mode, rscale, couple;
+    int RS, PS;                 // compact-array strides of local +y and +z (host: sweep3_layout)
+};
+
+// Compile-time box shapes: SHAPE 1 = 32 x 8 x 4 (config 5), SHAPE 0 = any box (runtime values).
+template <int SHAPE>
+struct Shape3 {
+    __device__ static int t0(const Sweep3Args &A) { return A.G.T[0]; }
+    __device__ static int t1(const Sweep3Args &A) { return A.G.T[1]; }
+    __device__ static int t2(const Sweep3Args &A) { return A.G.T[2]; }
+    __device__ static int rs(const Sweep3Args &A) { return A.RS; }
+    __device__ static int ps(const Sweep3Args &A) { return A.PS; }
+};
+template <>
+struct Shape3<1> {
+    __device__ static constexpr int t0(const Sweep3Args &) { return 32; }
+    __device__ static constexpr int t1(const Sweep3Args &) { return 8; }
+    __device__ static constexpr int t2(const Sweep3Args &) { return 4; }
+    __device__ static constexpr int rs(const Sweep3Args &) { return 34; }
+    __device__ static constexpr int ps(const Sweep3Args &) { return 307; }
 };
 
 // Solve one coupled set on the axes AXES (K = 2^popcount members) whose own member sits at
@@ -265,19 +284,28 @@ __device__ double sw_dbg3[4 * 8192];
 __device__ int sw_dbg3_block = -1;
 #endif
 
-template <bool FACES>
+template <bool FACES, int SHAPE>
 __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     extern __shared__ __align__(128) double sm[];
     const Geo &G = A.G;
-    const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
+    using SH = Shape3<SHAPE>;
+    const int T0 = SH::t0(A), T1 = SH::t1(A), T2 = SH::t2(A);
     // compact arrays over the extended box [-1, T) per axis in LOCAL coordinates (sweep order:
-    // local +a points away from the box's start corner), so every step below is positive
+    // local +a points away from the box's start corner), so every step below is positive; the
+    // y / z strides RS / PS are padded so that the wavefront's 32 lanes hit distinct banks
     const int E0 = T0 + 1, E1 = T1 + 1, E2 = T2 + 1;
-    const int WS = E0 * E1 * E2;
+    const int RS = SH::rs(A), PS = SH::ps(A);
+    const int WS = PS * E2;
     double *const X = sm;                               // r0 of the active nodes, then their results
     double *const C0 = sm + WS, *const C1 = sm + 2 * WS, *const C2 = sm + 3 * WS;
-    double *const PV = sm + 4 * WS;                     // pair pivots: y-face sheet [T2][T0], z-face [T1][T0]
-    double *const SCR = PV + T0 * (T1 + T2);            // corner elimination scratch (80 doubles)
+    // pair data of the 2 x 2 face pairs, a = the member of lower global index: x-face sheet
+    // (1 / pivot, m_ab, m_ba) [k][j]; y-face sheet (m_ab, m_ba) [k][i], z-face sheet [j][i] (line
+    // stride T0 + 1); then (0, 0) for the lanes without a pair
+    double *const PVX = sm + 4 * WS;
+    double *const PVY = PVX + 3 * T1 * T2;
+    double *const PVZ = PVY + 2 * (T0 + 1) * T2;
+    double *const PV1 = PVZ + 2 * (T0 + 1) * T1;
+    double *const SCR = PV1 + 4;                        // corner elimination scratch (80 doubles)
     auto CC = [&](int a, int w) -> double & { return sm[(a + 1) * WS + w]; };   // coupling of axis a
     const int tid = threadIdx.x;
     // box, direction bits, coupled start faces
@@ -293,49 +321,47 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         sb |= s << a;
         cb |= (int)c << a;
     }
-    const int st[3] = {1, E0, E0 * E1};               // compact step of local +a
-    auto wof = [&](int l0, int l1, int l2) { return (l0 + 1) + E0 * ((l1 + 1) + E1 * (l2 + 1)); };
+    const int st[3] = {1, RS, PS};                      // compact step of local +a
+    auto wof = [&](int l0, int l1, int l2) { return (l0 + 1) + RS * (l1 + 1) + PS * (l2 + 1); };
     const int64_t P0 = G.P0, P01 = G.P01;
     const int64_t gbase = (int64_t)tz * T2 * P01 + (int64_t)ty * T1 * P0 + (int64_t)tx * T0;   // padded (box min - 2)
     const int64_t Sg[3] = {1, P0, P01};
 
     SW_TMARK(t_start);
     // ---------------------------------------------------------------- 1. prologue
-    // Every node of the extended box: r0 and the couplings alpha c toward its implicit side of the
-    // active nodes (own nodes and the partner layers across coupled start faces, DESIGN R-7), zero
-    // for the rest (the layers across uncoupled faces are read only through zero couplings).
-    // x_old / src, b / 1/D~ and the faces come straight from global memory (L1/L2: neighbouring
-    // boxes share their halos), coalesced along x; the loop walks e = (l0, l1, l2) in mixed radix.
+    // Every slot of the compact arrays: r0 and the couplings alpha c toward its implicit side of
+    // the active nodes (own nodes and the partner layers across coupled start faces, DESIGN R-7),
+    // zero for the rest (the layers across uncoupled faces and the padding are read only through
+    // zero couplings).  x_old / src, b / 1/D~ and the faces come straight from global memory
+    // (L1/L2: neighbouring boxes share their halos), coalesced along x.
     {
         const double *__restrict__ xin = A.xin;
         const double *__restrict__ aux = A.aux;
         const double *__restrict__ F0 = A.f0, *__restrict__ F1 = A.f1, *__restrict__ F2 = A.f2;
-        int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
-        const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
+        const float invPS = 1.0f / (float)PS, invRS = 1.0f / (float)RS;
         const bool need_x = !A.tri, need_aux = !A.tri || A.invd_mode;
-        constexpr int KB = 3;      // nodes per batch: all their loads are issued before any use
+        constexpr int KB = 3;      // slots per batch: all their loads are issued before any use
         for (int e0 = tid; e0 < WS; e0 += KB * k3::NT) {
             int lvv[KB][3], Lm[KB];
             bool on[KB];
             int64_t gg[KB];
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
+                const int c = e0 + kb * k3::NT;
+                // c = l0 + RS l1 + PS l2 (exact float quotients: c < 2^22)
+                const int l2 = __float2int_rz(((float)c + 0.5f) * invPS);
+                const int r = c - l2 * PS;
+                const int l1 = __float2int_rz(((float)r + 0.5f) * invRS);
+                const int l0 = r - l1 * RS;
                 lvv[kb][0] = l0 - 1; lvv[kb][1] = l1 - 1; lvv[kb][2] = l2 - 1;
                 const int L = (l0 < 1 ? 1 : 0) | (l1 < 1 ? 2 : 0) | (l2 < 1 ? 4 : 0);
                 Lm[kb] = L;
-                on[kb] = l2 < E2 && (L & cb) == L;
+                on[kb] = c < WS && l0 < E0 && l1 < E1 && (L & cb) == L;
                 const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - lvv[kb][0] : lvv[kb][0]);
                 const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - lvv[kb][1] : lvv[kb][1]);
                 const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - lvv[kb][2] : lvv[kb][2]);
-                // inactive nodes load from the box's first node (always inside the padded array)
+                // inactive slots load from the box's first node (always inside the padded array)
                 gg[kb] = on[kb] ? gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01 : gbase + 2 + 2 * P0 + 2 * P01;
-                l0 += a0;
-                const int c0 = l0 >= E0;
-                l0 -= c0 ? E0 : 0;
-                l1 += a1 + c0;
-                const int c1 = l1 >= E1;
-                l1 -= c1 ? E1 : 0;
-                l2 += a2 + c1;
             }
             double f[KB][3][2], xn[KB][3], xo[KB], av[KB];
 #pragma unroll
@@ -396,24 +422,44 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
             }
         }
     }
+    // the pair data and the scratch start as zeros: idle wavefront lanes read them out of range,
+    // and every value anyone reads must be finite (a zero coupling times garbage must stay zero)
+    for (int e = tid; e < (int)(SCR + 80 - PVX); e += k3::NT) PVX[e] = 0.0;
     SW_TMARK(t_pro_own);
     SW_TADD(8, t_start, t_pro_own);
     __syncthreads();
-    // pivots 1 / (1 - m m') of the face pairs that the level loop solves (y- and z-face sheets)
+    // pair data of the 2 x 2 face pairs the level loop solves (one coupled face; sets on two or
+    // three faces are step 2): 1 / (1 - m_ba m_ab), m_ab, m_ba with a the member of lower global
+    // index.  The y- and z-sheet pairs' own couplings toward each other are then zeroed in the
+    // arrays, so that the wavefront evaluates every row with the same three-term formula.
     const bool fast_lines = T1 * T2 <= 32;
     if (fast_lines) {
-        const int ny = ((cb & 2) ? T0 * T2 : 0), nz = ((cb & 4) ? T0 * T1 : 0);
+        const int nx = T1 * T2, ny = T0 * T2, nz = T0 * T1;
         int fl = 0;
-        for (int e = tid; e < ny + nz; e += k3::NT) {
-            int i, j, k, a, pi;
-            if (e < ny) { i = e % T0; k = e / T0; j = 0; a = 1; pi = e; }
-            else { i = (e - ny) % T0; j = (e - ny) / T0; k = 0; a = 2; pi = T0 * T2 + (e - ny); }
+        for (int e = tid; e < nx + ny + nz; e += k3::NT) {
+            int i, j, k, a;
+            double *dst;
+            if (e < nx) { i = 0; j = e % T1; k = e / T1; a = 0; dst = PVX + 3 * e; }
+            else if (e < nx + ny) { const int f = e - nx; i = f % T0; k = f / T0; j = 0; a = 1; dst = PVY + 2 * (k * (T0 + 1) + i); }
+            else { const int f = e - nx - ny; i = f % T0; j = f / T0; k = 0; a = 2; dst = PVZ + 2 * (j * (T0 + 1) + i); }
             const int m = (i == 0 ? (cb & 1) : 0) | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
-            if (__popc(m) != 1) continue;                         // sets of two or more faces: step 3
+            if (m != (1 << a)) continue;                          // not a pair on exactly this face
             const int w = wof(i, j, k), q = w - st[a];
-            const double m11 = fma(CC(a, w), -CC(a, q), 1.0);
+            const double cw = CC(a, w), cq = CC(a, q);
+            const bool qfirst = ((sb >> a) & 1) == 0;             // partner has the lower global index
+            const double mab = qfirst ? cq : cw, mba = qfirst ? cw : cq;
+            const double m11 = fma(mba, -mab, 1.0);
             fl |= !(fabs(m11) >= 1e-14);
-            PV[pi] = div_rn(1.0, m11);
+            if (a == 0) {
+                dst[0] = div_rn(1.0, m11);
+                dst[1] = mab;
+                dst[2] = mba;
+            } else {        // the wavefront recomputes the pivot off its critical path
+                dst[0] = mab;
+                dst[1] = mba;
+                CC(a, w) = 0.0;
+                CC(a, q) = 0.0;
+            }
         }
         if (fl) atomicOr(A.flag, 1);
         __syncthreads();
@@ -455,108 +501,98 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     SW_TMARK(t_sets);
     // ---------------------------------------------------------------- 3. level loop (warp 0)
     if (fast_lines) {
-        // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over (j, k)
+        // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over d = j + k
         if (lt < 32 && (cb & 1)) {
             const int j = lt % T1, k = lt / T1;
             const bool on = lt < T1 * T2;
             const int m = 1 | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
-            const int w = on ? wof(0, j, k) : 0, q = w - st[0];
-            int fl = 0;
+            const int w = on ? wof(0, j, k) : wof(0, 0, 0), q = w - st[0];
+            const bool qfirst = (sb & 1) == 0;
+            const double *pd = PVX + 3 * (on ? lt : 0);
+            const double piv = pd[0], mab = pd[1], mba = pd[2];
+            const double cyw = CC(1, w), czw = CC(2, w), cyq = CC(1, q), czq = CC(2, q), r0w = X[w], r0q = X[q];
             for (int d = 0; d <= T1 + T2 - 2; ++d) {
                 if (on && j + k == d && m == 1) {
-                    const double rp = fma(CC(2, w), X[w - st[2]], fma(CC(1, w), X[w - st[1]], X[w]));
-                    const double rq = fma(CC(2, q), X[q - st[2]], fma(CC(1, q), X[q - st[1]], X[q]));
-                    const bool qfirst = (sb & 1) == 0;
+                    const double rp = fma(czw, X[w - st[2]], fma(cyw, X[w - st[1]], r0w));
+                    const double rq = fma(czq, X[q - st[2]], fma(cyq, X[q - st[1]], r0q));
                     const double ra = qfirst ? rq : rp, rb = qfirst ? rp : rq;
-                    const double cw = CC(0, w), cq = CC(0, q);
-                    const double mab = qfirst ? cq : cw, mba = qfirst ? cw : cq;
-                    const double m11 = fma(mba, -mab, 1.0);
-                    fl |= !(fabs(m11) >= 1e-14);
-                    const double ub = fma(mba, ra, rb) * div_rn(1.0, m11);
-                    const double ua = fma(mab, ub, ra) * 1.0;
+                    const double ub = fma(mba, ra, rb) * piv;
+                    const double ua = fma(mab, ub, ra);
                     X[w] = qfirst ? ub : ua;
                     X[q] = qfirst ? ua : ub;
                 }
                 __syncwarp();
             }
-            if (fl) atomicOr(A.flag, 1);
         }
         SW_TMARK(t_xs);
         SW_TADDT(13, t_sets, t_xs, 0);
         // (b) all other nodes: lane (j, k) owns the x-line and updates node i = s - j - k at step
-        //     s; S and B arrive from lanes l-1 and l-T1 by shuffles, and so do the partner values
+        //     s.  S and B arrive from lanes l-1 and l-T1 by shuffles, and so do the partner values
         //     of the y- and z-face sheets (which each lane on such a face carries in registers).
-        //     One branch-free instruction stream for every kind of lane: a plain lane is a "pair"
-        //     with zero couplings and unit pivot, which leaves its node formula exact; the x-edge
-        //     lane (solved in step 2) only reloads and forwards its values.
+        //     One instruction stream for every kind of lane, each row the same three-term formula:
+        //     a pair's coupling toward its partner was moved into the pair data (zero in the row),
+        //     and a plain lane is a "pair" with its own node as partner and pair data (1, 0, 0),
+        //     which leaves its node formula exact; the x-edge lane (solved in step 2) only reloads
+        //     and forwards its values.  Idle lanes compute finite garbage that nobody reads.
         if (lt < 32) {
             const int lane = lt, nl = T1 * T2;
             const bool on = lane < nl;
             const int j = on ? lane % T1 : 0, k = on ? lane / T1 : 0;
             const bool yc = j == 0 && (cb & 2), zc = k == 0 && (cb & 4);
-            const bool edge = yc && zc, ypair = yc && !zc, zpair = zc && !yc, pair = ypair || zpair;
+            const bool edge = on && yc && zc, ypair = on && yc && !zc, zpair = on && zc && !yc, pair = ypair || zpair;
             const int i0 = (cb & 1) ? 1 : 0;
-            const int sx = st[0], sy = st[1], sz = st[2];
-            const int sa = ypair ? sy : (zpair ? sz : 0);                 // step toward the pair partner
+            const int sa = ypair ? RS : (zpair ? PS : 0);                  // step toward the pair partner
             const int wl = wof(0, j, k);
-            const int pvb = ypair ? T0 * k : T0 * T2 + T0 * j;           // pivots of the lane's pairs
             const bool qf = pair ? (((sb >> (ypair ? 1 : 2)) & 1) == 0) : true;   // partner first in index order
-            // addresses of the other transverse coupling of the partner: z for y-pairs, y for z-pairs
-            const int oq_arr = ypair ? 3 : 2;                             // (axis + 1) of that coupling
-            const int pa_arr = ypair ? 2 : 3;                             // (axis + 1) of the pair coupling
+            const double *const pdl = ypair ? PVY + 2 * k * (T0 + 1) : (zpair ? PVZ + 2 * j * (T0 + 1) : PV1);
+            const int pds = pair ? 2 : 0;
             double W = i0 ? X[wl] : 0.0;
             double Wq = (i0 && pair) ? X[wl - sa] : 0.0;                 // partner value at i0 - 1
             double u = 0.0, py = 0.0, pz = 0.0;
             const int NS = T0 + T1 + T2 - 2;
-            auto ld = [&](int s, double (&v)[11]) {
-                int i = s - j - k;
-                i = i < 0 ? 0 : (i >= T0 ? T0 - 1 : i);                   // clamp idle lanes' addresses
-                const int w = wl + i * sx, q = pair ? w - sa : w;
-                v[0] = X[w];                    // r0 (edge lane: its solved value)
-                v[1] = sm[WS + w];              // C_x
-                v[2] = sm[2 * WS + w];          // C_y
-                v[3] = sm[3 * WS + w];          // C_z
-                v[4] = X[q];                    // partner r0
-                v[5] = sm[WS + q];              // partner C_x
-                v[6] = sm[oq_arr * WS + q];     // partner other transverse coupling
-                v[7] = sm[pa_arr * WS + q];     // partner pair coupling
-                v[8] = pair ? PV[pvb + i] : 1.0;  // pivot inverse (prologue)
-                v[9] = edge ? X[w - sy] : 0.0;  // edge: its y-partner value
-                v[10] = edge ? X[w - sz] : 0.0; //       its z-partner value
+            struct Ld { double r0, cx, cy, cz, q0, qx, qy, qz, piv, mab, mba, ey, ez; };
+            auto ld = [&](int s, Ld &v) {
+                const int i = s - j - k;                          // any value: idle lanes read in-bounds garbage
+                const int w = wl + i, q = w - sa;
+                const double *pd = pdl + pds * i;
+                v.r0 = X[w]; v.cx = C0[w]; v.cy = C1[w]; v.cz = C2[w];
+                v.q0 = X[q]; v.qx = C0[q]; v.qy = C1[q]; v.qz = C2[q];
+                v.mab = pd[0]; v.mba = pd[1];
+                v.piv = div_rn(1.0, fma(v.mba, -v.mab, 1.0));    // (1 for lanes without a pair)
+                v.ey = X[w - RS]; v.ez = X[w - PS];               // the x-edge lane's solved partners
             };
-            double nv[11];
-            ld(0, nv);
-            for (int s = 0; s < NS; ++s) {
+            auto step = [&](int s, const Ld &v) {
                 const double Sv = shfl_up_f64(u, 1), Bv = shfl_up_f64(u, T1);
                 const double Sq = shfl_up_f64(pz, 1), Bq = shfl_up_f64(py, T1);
-                double v[11];
-#pragma unroll
-                for (int t = 0; t < 11; ++t) v[t] = nv[t];
-                if (s + 1 < NS) ld(s + 1, nv);
                 const int i = s - j - k;
                 const bool act = on && i >= i0 && i < T0;
-                const int w = wl + (i < 0 ? 0 : (i >= T0 ? T0 - 1 : i)) * sx;
-                // own row: x, y (unless the y pair), z (unless the z pair), in axis order
-                const double cyE = ypair ? 0.0 : v[2], czE = zpair ? 0.0 : v[3];
-                const double rp = fma(czE, Bv, fma(cyE, Sv, fma(v[1], W, v[0])));
-                // partner row: x, then the other transverse axis
-                const double Oq = ypair ? Bq : Sq;
-                const double rq = fma(pair ? v[6] : 0.0, Oq, fma(pair ? v[5] : 0.0, Wq, v[4]));
-                const double cw = ypair ? v[2] : (zpair ? v[3] : 0.0), cq = pair ? v[7] : 0.0;
+                // rows in axis order x, y, z (the pair axis has a zero coupling)
+                const double rp = fma(v.cz, Bv, fma(v.cy, Sv, fma(v.cx, W, v.r0)));
+                const double rq = fma(v.qz, Bq, fma(v.qy, Sq, fma(v.qx, Wq, v.q0)));
                 const double ra = qf ? rq : rp, rb = qf ? rp : rq;
-                const double mab = qf ? cq : cw, mba = qf ? cw : cq;
-                const double ub = fma(mba, ra, rb) * v[8];
-                const double ua = fma(mab, ub, ra) * 1.0;
+                const double ub = fma(v.mba, ra, rb) * v.piv;
+                const double ua = fma(v.mab, ub, ra);
                 double un = qf ? ub : ua;
                 const double pv = qf ? ua : ub;
-                un = edge ? v[0] : un;
-                st_shared_if(X + w, un, act && !edge);
-                u = sel_f64(act, un, u);
+                un = edge ? v.r0 : un;
+                st_shared_if(X + wl + i, un, act && !edge);
+                u = un;
                 W = sel_f64(act, un, W);              // idle (joining) lanes keep W = value at i0 - 1
-                Wq = sel_f64(act && pair, pv, Wq);
-                py = sel_f64(act, ypair ? pv : (edge ? v[9] : py), py);
-                pz = sel_f64(act, zpair ? pv : (edge ? v[10] : pz), pz);
+                Wq = sel_f64(act, pv, Wq);
+                py = ypair ? pv : v.ey;
+                pz = zpair ? pv : v.ez;
+            };
+            Ld va, vb;
+            ld(0, va);
+            int s = 0;
+#pragma unroll 1
+            for (; s + 1 < NS; s += 2) {
+                ld(s + 1, vb);
+                step(s, va);
+                ld(s + 2, va);
+                step(s + 1, vb);
             }
+            if (s < NS) step(s, va);
             SW_TMARK(t_wf);
             SW_TADDT(9, t_xs, t_wf, 0);
         }
@@ -647,9 +683,35 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     SW_TADD(5, 0, 1);
 }
 
+// Strides of the compact arrays: the smallest padded (RS, PS) for which the 64-bit accesses of the
+// wavefront's lanes (j, k) = (l % T1, l / T1), l < T1 T2, are free of bank conflicts within each
+// half-warp (or have the fewest conflicts).
+inline void sweep3_layout(const int T[3], int *RS, int *PS) {
+    if (T[0] == 32 && T[1] == 8 && T[2] == 4) { *RS = 34; *PS = 307; return; }   // Shape3<1>
+    const int E0 = T[0] + 1, E1 = T[1] + 1, nl = T[1] * T[2];
+    int best = 1 << 30;
+    for (int rs = E0; rs < E0 + 16; ++rs)
+        for (int ps = rs * E1; ps < rs * E1 + 16; ++ps) {
+            int worst = 0;
+            for (int h = 0; h < 2; ++h) {
+                int cnt[16] = {0};
+                for (int l = 16 * h; l < 16 * h + 16 && l < nl; ++l) {
+                    const int off = rs * (l % T[1]) + ps * (l / T[1]);
+                    const int c = ++cnt[off & 15];
+                    if (c > worst) worst = c;
+                }
+            }
+            const int score = worst * (1 << 20) + ps;       // fewest conflicts, then least memory
+            if (score < best) { best = score; *RS = rs; *PS = ps; }
+        }
+}
+
 inline size_t sweep3_smem(const Geo &G) {
-    const size_t ws = (size_t)(G.T[0] + 1) * (G.T[1] + 1) * (G.T[2] + 1);
-    return sizeof(double) * (4 * ws + (size_t)G.T[0] * (G.T[1] + G.T[2]) + 80);
+    int rs, ps;
+    sweep3_layout(G.T, &rs, &ps);
+    const size_t ws = (size_t)ps * (G.T[2] + 1);
+    const size_t pv = 3 * (size_t)G.T[1] * G.T[2] + 2 * (size_t)(G.T[0] + 1) * (G.T[1] + G.T[2]) + 4;
+    return sizeof(double) * (4 * ws + pv + 80);
 }
 
 // the fast 3D path handles boxes whose compact arrays fit in shared memory
@@ -659,14 +721,26 @@ inline bool sweep3_supported(const Geo &G) {
            G.T[0] <= 33 && G.T[1] <= 33 && G.T[2] <= 33 && G.off[0] == 0 && G.off[1] == 0;
 }
 
-inline cudaError_t launch_sweep3(const Sweep3Args &A, cudaStream_t s) {
+template <bool FACES, int SHAPE>
+inline void launch_sweep3_t(const Sweep3Args &A, size_t smem, unsigned tiles, cudaStream_t s) {
+    cudaFuncSetAttribute(k_sweep3<FACES, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sweep3<FACES, SHAPE><<<tiles, k3::NT, smem, s>>>(A);
+}
+
+inline cudaError_t launch_sweep3(const Sweep3Args &A0, cudaStream_t s) {
+    Sweep3Args A = A0;
+    sweep3_layout(A.G.T, &A.RS, &A.PS);
     const size_t smem = sweep3_smem(A.G);
     const bool faces = A.f0 != nullptr;
-    if (faces) cudaFuncSetAttribute(k_sweep3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else cudaFuncSetAttribute(k_sweep3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool c5 = A.G.T[0] == 32 && A.G.T[1] == 8 && A.G.T[2] == 4;
     const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1] * A.G.nt[2]);
-    if (faces) k_sweep3<true><<<tiles, k3::NT, smem, s>>>(A);
-    else k_sweep3<false><<<tiles, k3::NT, smem, s>>>(A);
+    if (faces) {
+        if (c5) launch_sweep3_t<true, 1>(A, smem, tiles, s);
+        else launch_sweep3_t<true, 0>(A, smem, tiles, s);
+    } else {
+        if (c5) launch_sweep3_t<false, 1>(A, smem, tiles, s);
+        else launch_sweep3_t<false, 0>(A, smem, tiles, s);
+    }
     return cudaGetLastError();
 }
 
