@@ -265,7 +265,7 @@ __device__ __forceinline__ void corner8_coop(double *X, int WS, double *scr, int
 // factors its set while the corner is being solved, then the sets are substituted in order
 template <int AXES>
 __device__ __forceinline__ void edge_chain(double *X, int WS, int lane, int T, int w1, int step, const int st[3],
-                                           int sbits, int *flag, bool run) {
+                                           int sbits, int *flag, bool run, int *done = nullptr) {
     Fac4 F;
     int fl = 0;
     const bool mine = run && lane + 1 < T;
@@ -274,7 +274,11 @@ __device__ __forceinline__ void edge_chain(double *X, int WS, int lane, int T, i
     __syncthreads();                          // the corner set is in place
     if (run)
         for (int t = 1; t < T; ++t) {
-            if (lane == t - 1) subst4<AXES>(X, WS, w1 + (t - 1) * step, st, sbits, F);
+            if (lane == t - 1) {
+                subst4<AXES>(X, WS, w1 + (t - 1) * step, st, sbits, F);
+                if (done)                     // publish: set t is in place (read by the wavefront warp)
+                    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(done)), "r"(t) : "memory");
+            }
             __syncwarp();
         }
 }
@@ -329,64 +333,77 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
 
     SW_TMARK(t_start);
     // ---------------------------------------------------------------- 1. prologue
-    // Every slot of the compact arrays: r0 and the couplings alpha c toward its implicit side of
-    // the active nodes (own nodes and the partner layers across coupled start faces, DESIGN R-7),
-    // zero for the rest (the layers across uncoupled faces and the padding are read only through
-    // zero couplings).  x_old / src, b / 1/D~ and the faces come straight from global memory
-    // (L1/L2: neighbouring boxes share their halos), coalesced along x.
+    // Every node of the extended box: r0 and the couplings alpha c toward its implicit side of the
+    // active nodes (own nodes and the partner layers across coupled start faces, DESIGN R-7), zero
+    // for the rest (the layers across uncoupled faces and the padding are read only through zero
+    // couplings).  x_old / src, b / 1/D~ and the faces come straight from global memory (L1/L2:
+    // neighbouring boxes share their halos), coalesced along x, addressed by 32-bit offsets from
+    // the box's base: local (m0, m1, m2) sits at o = O0 + m0 d0 + m1 d1 + m2 d2.
     {
-        const double *__restrict__ xin = A.xin;
-        const double *__restrict__ aux = A.aux;
-        const double *__restrict__ F0 = A.f0, *__restrict__ F1 = A.f1, *__restrict__ F2 = A.f2;
-        const float invPS = 1.0f / (float)PS, invRS = 1.0f / (float)RS;
+        const int P0i = (int)P0, P01i = (int)P01;
+        const int Sgi[3] = {1, P0i, P01i};
+        int O0 = 0, d[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int Ta = a == 0 ? T0 : (a == 1 ? T1 : T2);
+            const bool sa_ = (sb >> a) & 1;
+            O0 += (2 + (sa_ ? Ta - 1 : 0)) * Sgi[a];
+            d[a] = sa_ ? -Sgi[a] : Sgi[a];
+        }
+        const double *__restrict__ xb = A.xin + gbase;
+        const double *__restrict__ ab = (A.aux ? A.aux : A.xin) + gbase;
+        const double *__restrict__ f0b = (FACES ? A.f0 : A.xin) + gbase;
+        const double *__restrict__ f1b = (FACES ? A.f1 : A.xin) + gbase;
+        const double *__restrict__ f2b = (FACES ? A.f2 : A.xin) + gbase;
         const bool need_x = !A.tri, need_aux = !A.tri || A.invd_mode;
-        constexpr int KB = 3;      // slots per batch: all their loads are issued before any use
-        for (int e0 = tid; e0 < WS; e0 += KB * k3::NT) {
-            int lvv[KB][3], Lm[KB];
+        const int NE = E0 * E1 * E2;
+        int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
+        const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
+        constexpr int KB = 3;      // nodes per batch: all their loads are issued before any use
+        for (int e0 = tid; e0 < NE; e0 += KB * k3::NT) {
+            int cw_[KB], Lm[KB], o_[KB], mz[KB];
             bool on[KB];
-            int64_t gg[KB];
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
-                const int c = e0 + kb * k3::NT;
-                // c = l0 + RS l1 + PS l2 (exact float quotients: c < 2^22)
-                const int l2 = __float2int_rz(((float)c + 0.5f) * invPS);
-                const int r = c - l2 * PS;
-                const int l1 = __float2int_rz(((float)r + 0.5f) * invRS);
-                const int l0 = r - l1 * RS;
-                lvv[kb][0] = l0 - 1; lvv[kb][1] = l1 - 1; lvv[kb][2] = l2 - 1;
                 const int L = (l0 < 1 ? 1 : 0) | (l1 < 1 ? 2 : 0) | (l2 < 1 ? 4 : 0);
                 Lm[kb] = L;
-                on[kb] = c < WS && l0 < E0 && l1 < E1 && (L & cb) == L;
-                const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - lvv[kb][0] : lvv[kb][0]);
-                const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - lvv[kb][1] : lvv[kb][1]);
-                const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - lvv[kb][2] : lvv[kb][2]);
-                // inactive slots load from the box's first node (always inside the padded array)
-                gg[kb] = on[kb] ? gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01 : gbase + 2 + 2 * P0 + 2 * P01;
+                on[kb] = l2 < E2 && (L & cb) == L;
+                cw_[kb] = l2 < E2 ? l0 + RS * l1 + PS * l2 : -1;
+                // which coordinates are 0 (cut test) packed in 3 bits
+                mz[kb] = (l0 == 1 ? 1 : 0) | (l1 == 1 ? 2 : 0) | (l2 == 1 ? 4 : 0);
+                o_[kb] = on[kb] ? O0 + (l0 - 1) * d[0] + (l1 - 1) * d[1] + (l2 - 1) * d[2] : O0;
+                l0 += a0;
+                const int c0 = l0 >= E0;
+                l0 -= c0 ? E0 : 0;
+                l1 += a1 + c0;
+                const int c1 = l1 >= E1;
+                l1 -= c1 ? E1 : 0;
+                l2 += a2 + c1;
             }
             double f[KB][3][2], xn[KB][3], xo[KB], av[KB];
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
-                const int64_t g = gg[kb];
+                const int o = o_[kb];
                 if (FACES) {
-                    f[kb][0][0] = __ldg(F0 + g); f[kb][0][1] = __ldg(F0 + g + 1);
-                    f[kb][1][0] = __ldg(F1 + g); f[kb][1][1] = __ldg(F1 + g + P0);
-                    f[kb][2][0] = __ldg(F2 + g); f[kb][2][1] = __ldg(F2 + g + P01);
+                    f[kb][0][0] = __ldg(f0b + o); f[kb][0][1] = __ldg(f0b + o + 1);
+                    f[kb][1][0] = __ldg(f1b + o); f[kb][1][1] = __ldg(f1b + o + P0i);
+                    f[kb][2][0] = __ldg(f2b + o); f[kb][2][1] = __ldg(f2b + o + P01i);
                 } else {
 #pragma unroll
                     for (int a = 0; a < 3; ++a) f[kb][a][0] = f[kb][a][1] = 1.0;
                 }
-                xo[kb] = __ldg(xin + g);
-                av[kb] = need_aux ? __ldg(aux + g) : 0.0;
+                xo[kb] = __ldg(xb + o);
+                av[kb] = need_aux ? __ldg(ab + o) : 0.0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     const bool hi = (((Lm[kb] >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
-                    xn[kb][a] = need_x ? __ldg(xin + (hi ? g - Sg[a] : g + Sg[a])) : 0.0;
+                    xn[kb][a] = need_x ? __ldg(xb + (hi ? o - Sgi[a] : o + Sgi[a])) : 0.0;
                 }
             }
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
-                const int e = e0 + kb * k3::NT;
-                if (e >= WS) break;
+                const int e = cw_[kb];
+                if (e < 0) break;
                 const int L = Lm[kb];
                 double r0 = 0.0, c[3] = {0.0, 0.0, 0.0};
                 if (on[kb]) {
@@ -411,7 +428,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                     for (int a = 0; a < 3; ++a) {
                         // no coupling across an uncoupled start face: the oracle omits the term (physical
                         // boundary) and the first pass of the transposed solve must not see the neighbour box
-                        const bool cut = !((L >> a) & 1) && lvv[kb][a] == 0 && !((cb >> a) & 1);
+                        const bool cut = !((L >> a) & 1) && ((mz[kb] >> a) & 1) && !((cb >> a) & 1);
                         c[a] = cut ? 0.0 : al * (hi[a] ? fk[a][1] : fk[a][0]);
                     }
                 }
@@ -421,7 +438,22 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                 C2[e] = c[2];
             }
         }
+        // the padding slots (x beyond E0 in every row, rows beyond E1 in every plane): zeros
+        const int rp = RS - E0, pp = PS - RS * E1;
+        for (int q = tid; q < rp * E1 * E2 + pp * E2; q += k3::NT) {
+            int c;
+            if (q < rp * E1 * E2) { const int row = q / rp; c = (row % E1) * RS + (row / E1) * PS + E0 + q % rp; }
+            else { const int r2 = q - rp * E1 * E2; c = (r2 / pp) * PS + RS * E1 + r2 % pp; }
+            X[c] = 0.0;
+            C0[c] = 0.0;
+            C1[c] = 0.0;
+            C2[c] = 0.0;
+        }
     }
+    // x-edge chain concurrent with the wavefront (lane wavefront, y and z start faces coupled)
+    __shared__ int s_edge_done;
+    const bool conc_x = (T1 * T2 <= 32) && __popc(cb) >= 2 && (cb & 6) == 6;
+    if (tid == 0) s_edge_done = 0;
     // the pair data and the scratch start as zeros: idle wavefront lanes read them out of range,
     // and every value anyone reads must be finite (a zero coupling times garbage must stay zero)
     for (int e = tid; e < (int)(SCR + 80 - PVX); e += k3::NT) PVX[e] = 0.0;
@@ -465,6 +497,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         __syncthreads();
     }
     SW_TMARK(t_prologue);
+    SW_TADD(1, t_start, t_prologue);
     const int lt = tid;
     // ---------------------------------------------------------------- 2. corner and edge sets
     const int ncpl = __popc(cb);
@@ -482,13 +515,18 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         SW_TMARK(t_corner);
         SW_TADDT(12, t_prologue, t_corner, 0);
         // the edge chains (independent of each other), one per warp: x-edge in warp 1, y-edge in
-        // warp 2, z-edge in warp 3 (factored in parallel with the corner, substituted in order)
+        // warp 2, z-edge in warp 3 (factored in parallel with the corner, substituted in order).
+        // With the lane wavefront, the long x-edge chain runs concurrently with the x-sheet and the
+        // wavefront, publishing its progress in s_edge_done; the other warps wait only for the
+        // y- and z-edge chains (named barrier 1).
         const int warp = lt >> 5, lane = lt & 31;
-        if (warp == 1) edge_chain<6>(X, WS, lane, T0, wof(1, 0, 0), st[0], st, sb, A.flag, (cb & 6) == 6);
+        if (warp == 1) edge_chain<6>(X, WS, lane, T0, wof(1, 0, 0), st[0], st, sb, A.flag, (cb & 6) == 6,
+                                     conc_x ? &s_edge_done : nullptr);
         else if (warp == 2) edge_chain<5>(X, WS, lane, T1, wof(0, 1, 0), st[1], st, sb, A.flag, (cb & 5) == 5);
         else if (warp == 3) edge_chain<3>(X, WS, lane, T2, wof(0, 0, 1), st[2], st, sb, A.flag, (cb & 3) == 3);
         else __syncthreads();
-        __syncthreads();
+        if (!conc_x) __syncthreads();
+        else if (warp != 1) asm volatile("bar.sync 1, %0;" ::"r"(k3::NT - 32) : "memory");
     }
 
 #ifdef SW_DEBUG3
@@ -499,6 +537,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         }
 #endif
     SW_TMARK(t_sets);
+    SW_TADD(2, t_prologue, t_sets);
     // ---------------------------------------------------------------- 3. level loop (warp 0)
     if (fast_lines) {
         // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over d = j + k
@@ -582,13 +621,25 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                 py = ypair ? pv : v.ey;
                 pz = zpair ? pv : v.ez;
             };
+            // the edge lane's loads of x-edge set `need` wait until warp 1 has stored it
+            auto wait_edge = [&](int need) {
+                if (conc_x && need < T0) {
+                    int got;
+                    do {
+                        asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(got) : "r"(smem_u32(&s_edge_done)) : "memory");
+                    } while (got < need);
+                }
+            };
             Ld va, vb;
+            __syncwarp();                             // converged (the shuffles' fast path)
             ld(0, va);
             int s = 0;
 #pragma unroll 1
             for (; s + 1 < NS; s += 2) {
+                wait_edge(s + 1);
                 ld(s + 1, vb);
                 step(s, va);
+                wait_edge(s + 2);
                 ld(s + 2, va);
                 step(s + 1, vb);
             }
@@ -655,6 +706,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     }
     __syncthreads();
     SW_TMARK(t_levels);
+    SW_TADD(3, t_sets, t_levels);
 
     // ---------------------------------------------------------------- 4. write-back of the box
     {
@@ -676,9 +728,6 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         }
     }
     SW_TMARK(t_end);
-    SW_TADD(1, t_start, t_prologue);
-    SW_TADD(2, t_prologue, t_sets);
-    SW_TADD(3, t_sets, t_levels);
     SW_TADD(4, t_levels, t_end);
     SW_TADD(5, 0, 1);
 }
