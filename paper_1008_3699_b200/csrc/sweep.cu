@@ -391,6 +391,19 @@ static sw_status launch_generic(sw_grid *g, const KParams &P, cudaStream_t s) {
     return SW_OK;
 }
 
+// 3D SYMMETRIC phase-2 stages: only the coupled sets of one degree (k_t2sets)
+static sw_status launch_t2sets(sw_grid *g, const KParams &P, int degree, cudaStream_t s) {
+    const unsigned tiles = (unsigned)((int64_t)g->G.nt[0] * g->G.nt[1] * g->G.nt[2]);
+    switch (degree) {
+        case 1: k_t2sets<1><<<tiles, 32, 0, s>>>(P); break;
+        case 2: k_t2sets<2><<<tiles, 32, 0, s>>>(P); break;
+        default: k_t2sets<3><<<tiles, 32, 0, s>>>(P); break;
+    }
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
 static KParams base_params(sw_grid *g) {
     KParams P;
     memset(&P, 0, sizeof(P));
@@ -619,6 +632,7 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     }
     P.mode = M_T2;                  // coupled sets of degree stage - 1
     P.j = stage - 1;
+    if (g->dim == 3 && g->fast2d) return launch_t2sets(g, P, P.j, s);
     return launch_generic(g, P, s);
 }
 
