@@ -134,82 +134,6 @@ __device__ void solve_set(const KParams &P, bool transpose, const int64_t gl[3],
     for (int m = 0; m < k; ++m) P.out[gidx(G, gm[m][0], gm[m][1], gm[m][2])] = u[m];
 }
 
-// The same solve with the set size NA = popcount(mask) known at compile time: every index is a
-// constant or a select, so the member arrays stay in registers (k_t2sets).
-template <int NA>
-__device__ __forceinline__ void solve_set_t(const KParams &P, bool transpose, const int64_t gl[3], int mask) {
-    const Geo &G = P.G;
-    constexpr int k = 1 << NA;
-    int bitof[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) bitof[a] = __popc(mask & ((1 << a) - 1));
-    int64_t gm[k][3];
-#pragma unroll
-    for (int m = 0; m < k; ++m)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) gm[m][a] = gl[a] + (((mask >> a) & 1) ? ((m >> bitof[a]) & 1) : 0);
-    double M[k][k], rhs[k], u[k];
-#pragma unroll
-    for (int p = 0; p < k; ++p) {
-#pragma unroll
-        for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
-        double al = node_alpha(P, gm[p]);
-        double acc = node_r0(P, gm[p], al);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            if (a >= G.dim) break;
-#pragma unroll
-            for (int sd = -1; sd <= 1; sd += 2) {
-                int64_t q[3] = {gm[p][0], gm[p][1], gm[p][2]};
-                q[a] += sd;
-                if (!in_domain(G, q) || !depends(G, P.base, transpose, gm[p], a, sd)) continue;
-                double m = al * face(G, P.F, gm[p], a, sd);
-                int in = -1;
-                if ((mask >> a) & 1) {
-                    const int bit = bitof[a];
-                    const int64_t other = gl[a] + (((p >> bit) & 1) ^ 1);   // the partner's coordinate
-                    if (other == q[a]) in = p ^ (1 << bit);
-                }
-                if (in >= 0) {
-#pragma unroll
-                    for (int c = 0; c < k; ++c)
-                        if (c == in) M[p][c] = -m;
-                } else {
-                    acc = fma(m, P.out[gidx(G, q[0], q[1], q[2])], acc);
-                }
-            }
-        }
-        rhs[p] = acc;
-    }
-    if (k == 1) {
-        u[0] = rhs[0];
-    } else {
-        double inv[k];
-#pragma unroll
-        for (int p = 0; p < k; ++p) {
-            double piv = M[p][p];
-            if (!(fabs(piv) >= 1e-14)) atomicOr(P.flag, 1);
-            inv[p] = 1.0 / piv;
-#pragma unroll
-            for (int q = p + 1; q < k; ++q) {
-                double l = M[q][p] * inv[p];
-#pragma unroll
-                for (int j = p + 1; j < k; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
-                rhs[q] = fma(-l, rhs[p], rhs[q]);
-            }
-        }
-#pragma unroll
-        for (int p = k - 1; p >= 0; --p) {
-            double s = rhs[p];
-#pragma unroll
-            for (int j = p + 1; j < k; ++j) s = fma(-M[p][j], u[j], s);
-            u[p] = s * inv[p];
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < k; ++m) P.out[gidx(G, gm[m][0], gm[m][1], gm[m][2])] = u[m];
-}
-
 // D-ILU(0) factor of one node (DESIGN R-C): dd = a_P - sum_{implicit q, same box} c^2 invD_q
 __device__ void factor_node(const KParams &P, const int64_t g[3]) {
     const Geo &G = P.G;
@@ -307,81 +231,5 @@ __global__ void __launch_bounds__(128) k_generic(KParams P) {
     }
 }
 
-
-// Second phase of the SYMMETRIC transposed solve in 3D, coupled sets of degree NA only (the
-// M_T2 pass of k_generic without its scan over every level and line): NA = 1 the pairs of the
-// three start-face sheets, a reverse 2D wavefront per sheet (a pair depends on the pairs at
-// +1 along the sheet's two axes); NA = 2 the three edge chains of 4-sets, reversed; NA = 3 the
-// corner set.  Sheets (edges) never depend on each other.  One warp per box; identical
-// arithmetic to k_generic (solve_set).
-template <int NA>
-__global__ void __launch_bounds__(32) k_t2sets(KParams P) {
-    const Geo &G = P.G;
-    const int64_t t = blockIdx.x;
-    int64_t R[3] = {t % G.nt[0], (t / G.nt[0]) % G.nt[1], t / ((int64_t)G.nt[0] * G.nt[1])};
-    int s[3], cpl[3];
-    int64_t lo_g[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        R[a] += G.toff[a];
-        s[a] = ((P.base >> a) & 1) ^ (int)(R[a] & 1);
-        cpl[a] = s[a] ? (R[a] < G.ntg[a] - 1) : (R[a] > 0);
-        lo_g[a] = R[a] * G.T[a];
-    }
-    const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
-    // this lane's line: (axis of the coupled face(s), fixed coordinate) and the walked axis
-    int fa = -1, fixv = 0, walk = 0, fixax = 0;
-    {
-        int ln = threadIdx.x;
-        if (NA == 1) {
-            const int n0 = cpl[0] ? T2 : 0, n1 = cpl[1] ? T2 : 0, n2 = cpl[2] ? T1 : 0;
-            if (ln < n0) { fa = 0; fixax = 2; fixv = ln; walk = 1; }
-            else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
-            else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
-        } else if (NA == 2) {
-            // edge along `walk` where the two other faces are coupled
-            if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; }
-        } else {
-            if (ln == 0 && cpl[0] && cpl[1] && cpl[2]) { fa = 0; walk = 0; }
-        }
-    }
-    const int dmax = (NA == 3) ? 0 : (NA == 2 ? (T0 > T1 ? (T0 > T2 ? T0 : T2) : (T1 > T2 ? T1 : T2)) - 1
-                                              : T0 - 1 + (T1 > T2 ? T1 : T2) - 1);
-    for (int d = dmax; d >= 0; --d) {
-        if (fa >= 0) {
-            int l[3] = {0, 0, 0};
-            bool ok = true;
-            if (NA == 1) {
-                l[fixax] = fixv;
-                l[walk] = d - fixv;
-                l[fa] = 0;
-                // the other two coordinates must be off the coupled start faces (else a set of
-                // higher degree) and inside the box
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-                    if (a != fa && (l[a] < (cpl[a] ? 1 : 0) || l[a] >= G.T[a])) ok = false;
-            } else if (NA == 2) {
-                l[walk] = d;
-                if (d < (cpl[walk] ? 1 : 0) || d >= G.T[walk]) ok = false;
-            }
-            if (ok) {
-                int64_t g[3], gl[3];
-                int mask = 0;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    g[a] = s[a] ? (lo_g[a] + G.T[a] - 1 - l[a]) : (lo_g[a] + l[a]);
-                    gl[a] = g[a];
-                    if (cpl[a] && l[a] == 0) {
-                        mask |= 1 << a;
-                        const int64_t other = s[a] ? (lo_g[a] + G.T[a]) : (lo_g[a] - 1);
-                        if (other < gl[a]) gl[a] = other;
-                    }
-                }
-                solve_set_t<NA>(P, true, gl, mask);
-            }
-        }
-        __syncwarp();
-    }
-}
 
 }  // namespace sw

@@ -18,6 +18,7 @@
 #include "sweep2v.cuh"
 #include "tri2t.cuh"
 #include "sweep3.cuh"
+#include "tri3t.cuh"
 
 using namespace sw;
 
@@ -391,19 +392,6 @@ static sw_status launch_generic(sw_grid *g, const KParams &P, cudaStream_t s) {
     return SW_OK;
 }
 
-// 3D SYMMETRIC phase-2 stages: only the coupled sets of one degree (k_t2sets)
-static sw_status launch_t2sets(sw_grid *g, const KParams &P, int degree, cudaStream_t s) {
-    const unsigned tiles = (unsigned)((int64_t)g->G.nt[0] * g->G.nt[1] * g->G.nt[2]);
-    switch (degree) {
-        case 1: k_t2sets<1><<<tiles, 32, 0, s>>>(P); break;
-        case 2: k_t2sets<2><<<tiles, 32, 0, s>>>(P); break;
-        default: k_t2sets<3><<<tiles, 32, 0, s>>>(P); break;
-    }
-    g->launches++;
-    CK(cudaGetLastError());
-    return SW_OK;
-}
-
 static KParams base_params(sw_grid *g) {
     KParams P;
     memset(&P, 0, sizeof(P));
@@ -632,7 +620,24 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     }
     P.mode = M_T2;                  // coupled sets of degree stage - 1
     P.j = stage - 1;
-    if (g->dim == 3 && g->fast2d) return launch_t2sets(g, P, P.j, s);
+    if (g->dim == 3 && g->fast2d) {
+        Tri3tArgs T3{};
+        T3.G = g->G;
+        T3.base = base;
+        T3.omega = omega;
+        T3.coef = coef;
+        T3.invd = invd;
+        T3.src = g->Y;
+        T3.f0 = g->G.poisson ? nullptr : g->F[0];
+        T3.f1 = g->G.poisson ? nullptr : g->F[1];
+        T3.f2 = g->G.poisson ? nullptr : g->F[2];
+        T3.z = z;
+        T3.flag = g->flag;
+        cudaError_t e = launch_tri3t(T3, P.j, s);
+        g->launches++;
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("tri3t launch: ") + cudaGetErrorString(e));
+        return SW_OK;
+    }
     return launch_generic(g, P, s);
 }
 

@@ -1,0 +1,201 @@
+// tri3t.cuh -- second phase of the transposed (SYMMETRIC-pairing) triangular solve in 3D, sm_100a
+// (DESIGN R-C; SURVEY §8(a) a11-a12, §8(c) C-ILU).
+//
+// The backward factor of the SYMMETRIC pairing solves (D/alpha + A_I^T) z = r0:
+//     z_p = coef src_p + sum_{q : p implicit for q} alpha_p c_pq z_q .
+// Phase 1 (k_sweep3 run from the far corner with the coupling off) is exact for every node outside
+// a coupled set.  The coupled sets are recomputed here by degree, one launch each, because a set
+// of degree j reads sets of degree j - 1 that neighbouring boxes compute:
+//   NA = 1: the pairs of the three start-face sheets, a reverse 2D wavefront per sheet;
+//   NA = 2: the three edge chains of 4-sets, reversed;
+//   NA = 3: the corner set.
+// One warp per box, one lane per sheet line / edge.  The member rows are built in the order of
+// the oracle's transposed solve (axes ascending, global -1 side before +1; the partner across a
+// coupled face goes into the matrix) and eliminated without pivoting in ascending global index
+// (DESIGN R-8), so the results are bitwise those of the oracle (and of k_generic's M_T2 pass).
+#pragma once
+#include "common.cuh"
+
+namespace sw {
+
+struct Tri3tArgs {
+    Geo G;
+    int base;                   // direction bits of the forward pass (phase k0)
+    double omega;               // SSOR: alpha = omega / a_P
+    double coef;                // r0 = coef src
+    const double *invd;         // ILU: alpha = 1/D~ (null for SSOR)
+    const double *src;          // phase-1 right-hand side (y)
+    const double *f0, *f1, *f2; // faces (null: Poisson)
+    double *z;                  // phase-1 result, coupled sets corrected in place
+    int *flag;
+};
+
+// box parity bit of global coordinate c along axis a (global coordinates fit in 32 bits)
+__device__ __forceinline__ int box_bit(const Tri3tArgs &A, int a, int64_t c) { return ((int)c / A.G.T[a]) & 1; }
+
+template <int NA>
+__device__ __forceinline__ void tri3t_solve(const Tri3tArgs &A, const int64_t gl[3], int mask) {
+    const Geo &G = A.G;
+    constexpr int k = 1 << NA;
+    int bitof[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) bitof[a] = __popc(mask & ((1 << a) - 1));
+    const int64_t S[3] = {1, G.P0, G.P01};
+    const double *const F[3] = {A.f0, A.f1, A.f2};
+    double M[k][k], rhs[k], u[k];
+    int64_t ix[k];
+#pragma unroll
+    for (int p = 0; p < k; ++p) {
+        int64_t g[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g[a] = gl[a] + (((mask >> a) & 1) ? ((p >> bitof[a]) & 1) : 0);
+        const int64_t i = gidx(G, g[0], g[1], g[2]);
+        ix[p] = i;
+        // faces toward -a and +a of this member
+        double fm[3], fp[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            fm[a] = G.poisson ? 1.0 : F[a][i];
+            fp[a] = G.poisson ? 1.0 : F[a][i + S[a]];
+        }
+        double al;
+        if (A.invd) {
+            al = A.invd[i];
+        } else {
+            const double ap = (((fm[0] + fp[0]) + (fm[1] + fp[1])) + (fm[2] + fp[2])) + G.beta;
+            al = A.omega / ap;
+        }
+        double acc = A.coef * A.src[i];
+#pragma unroll
+        for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+#pragma unroll
+            for (int sd = -1; sd <= 1; sd += 2) {
+                const int64_t qa = g[a] + sd;
+                if (qa < 0 || qa >= G.ng[a]) continue;              // outside the domain
+                // p is implicit for q = p + sd e_a iff q's box starts at the side facing p
+                const int sq = ((A.base >> a) & 1) ^ box_bit(A, a, qa);
+                if (sq != (sd < 0 ? 1 : 0)) continue;
+                const double m = al * (sd < 0 ? fm[a] : fp[a]);
+                int in = -1;
+                if ((mask >> a) & 1) {
+                    const int bit = bitof[a];
+                    const int64_t other = gl[a] + (((p >> bit) & 1) ^ 1);   // the partner's coordinate
+                    if (other == qa) in = p ^ (1 << bit);
+                }
+                if (in >= 0) {
+#pragma unroll
+                    for (int c = 0; c < k; ++c)
+                        if (c == in) M[p][c] = -m;
+                } else {
+                    acc = fma(m, A.z[i + sd * S[a]], acc);
+                }
+            }
+        }
+        rhs[p] = acc;
+    }
+    double inv[k];
+#pragma unroll
+    for (int p = 0; p < k; ++p) {
+        const double piv = M[p][p];
+        if (!(fabs(piv) >= 1e-14)) atomicOr(A.flag, 1);
+        inv[p] = 1.0 / piv;
+#pragma unroll
+        for (int q = p + 1; q < k; ++q) {
+            const double l = M[q][p] * inv[p];
+#pragma unroll
+            for (int j = p + 1; j < k; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
+            rhs[q] = fma(-l, rhs[p], rhs[q]);
+        }
+    }
+#pragma unroll
+    for (int p = k - 1; p >= 0; --p) {
+        double s = rhs[p];
+#pragma unroll
+        for (int j = p + 1; j < k; ++j) s = fma(-M[p][j], u[j], s);
+        u[p] = s * inv[p];
+    }
+#pragma unroll
+    for (int p = 0; p < k; ++p) A.z[ix[p]] = u[p];
+}
+
+template <int NA>
+__global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
+    const Geo &G = A.G;
+    const int64_t t = blockIdx.x;
+    int64_t R[3] = {t % G.nt[0], (t / G.nt[0]) % G.nt[1], t / ((int64_t)G.nt[0] * G.nt[1])};
+    int s[3], cpl[3];
+    int64_t lo_g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        R[a] += G.toff[a];
+        s[a] = ((A.base >> a) & 1) ^ (int)(R[a] & 1);
+        cpl[a] = s[a] ? (R[a] < G.ntg[a] - 1) : (R[a] > 0);
+        lo_g[a] = R[a] * G.T[a];
+    }
+    const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
+    // this lane's line: the face (NA = 1) or edge axis (NA = 2), the fixed and the walked axes
+    int fa = -1, fixv = 0, walk = 0, fixax = 0;
+    {
+        int ln = threadIdx.x;
+        if (NA == 1) {
+            const int n0 = cpl[0] ? T2 : 0, n1 = cpl[1] ? T2 : 0, n2 = cpl[2] ? T1 : 0;
+            if (ln < n0) { fa = 0; fixax = 2; fixv = ln; walk = 1; }
+            else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
+            else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
+        } else if (NA == 2) {
+            if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; }
+        } else {
+            if (ln == 0 && cpl[0] && cpl[1] && cpl[2]) fa = 0;
+        }
+    }
+    const int tmax = T0 > T1 ? (T0 > T2 ? T0 : T2) : (T1 > T2 ? T1 : T2);
+    const int dmax = (NA == 3) ? 0 : (NA == 2 ? tmax - 1 : T0 - 1 + (T1 > T2 ? T1 : T2) - 1);
+    for (int d = dmax; d >= 0; --d) {
+        if (fa >= 0) {
+            int l[3] = {0, 0, 0};
+            bool ok = true;
+            if (NA == 1) {
+                l[fixax] = fixv;
+                l[walk] = d - fixv;
+                // the other two coordinates off the coupled start faces (else a set of higher
+                // degree) and inside the box
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    if (a != fa && (l[a] < (cpl[a] ? 1 : 0) || l[a] >= G.T[a])) ok = false;
+            } else if (NA == 2) {
+                l[walk] = d;
+                if (d < (cpl[walk] ? 1 : 0) || d >= G.T[walk]) ok = false;
+            }
+            if (ok) {
+                int64_t gl[3];
+                int mask = 0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const int64_t g = s[a] ? (lo_g[a] + G.T[a] - 1 - l[a]) : (lo_g[a] + l[a]);
+                    gl[a] = g;
+                    if (cpl[a] && l[a] == 0) {
+                        mask |= 1 << a;
+                        const int64_t other = s[a] ? (lo_g[a] + G.T[a]) : (lo_g[a] - 1);
+                        if (other < gl[a]) gl[a] = other;
+                    }
+                }
+                tri3t_solve<NA>(A, gl, mask);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+inline cudaError_t launch_tri3t(const Tri3tArgs &A, int degree, cudaStream_t s) {
+    const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1] * A.G.nt[2]);
+    switch (degree) {
+        case 1: k_tri3t<1><<<tiles, 32, 0, s>>>(A); break;
+        case 2: k_tri3t<2><<<tiles, 32, 0, s>>>(A); break;
+        default: k_tri3t<3><<<tiles, 32, 0, s>>>(A); break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace sw
