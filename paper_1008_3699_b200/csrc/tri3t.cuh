@@ -120,6 +120,91 @@ __device__ __forceinline__ void tri3t_solve(const Tri3tArgs &A, const int64_t gl
     for (int p = 0; p < k; ++p) A.z[ix[p]] = u[p];
 }
 
+// Row of member p alone (the same operations as tri3t_solve's member loop): rhs and the matrix row.
+template <int NA>
+__device__ __forceinline__ void tri3t_row(const Tri3tArgs &A, const int64_t gl[3], int mask, int p, double &rhs,
+                                          double (&Mr)[1 << NA], int64_t &ix) {
+    const Geo &G = A.G;
+    constexpr int k = 1 << NA;
+    int bitof[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) bitof[a] = __popc(mask & ((1 << a) - 1));
+    const int64_t S[3] = {1, G.P0, G.P01};
+    const double *const F[3] = {A.f0, A.f1, A.f2};
+    int64_t g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = gl[a] + (((mask >> a) & 1) ? ((p >> bitof[a]) & 1) : 0);
+    const int64_t i = gidx(G, g[0], g[1], g[2]);
+    ix = i;
+    double fm[3], fp[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        fm[a] = G.poisson ? 1.0 : F[a][i];
+        fp[a] = G.poisson ? 1.0 : F[a][i + S[a]];
+    }
+    double al;
+    if (A.invd) {
+        al = A.invd[i];
+    } else {
+        const double ap = (((fm[0] + fp[0]) + (fm[1] + fp[1])) + (fm[2] + fp[2])) + G.beta;
+        al = A.omega / ap;
+    }
+    double acc = A.coef * A.src[i];
+#pragma unroll
+    for (int q = 0; q < k; ++q) Mr[q] = (p == q) ? 1.0 : 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int sd = -1; sd <= 1; sd += 2) {
+            const int64_t qa = g[a] + sd;
+            if (qa < 0 || qa >= G.ng[a]) continue;
+            const int sq = ((A.base >> a) & 1) ^ box_bit(A, a, qa);
+            if (sq != (sd < 0 ? 1 : 0)) continue;
+            const double m = al * (sd < 0 ? fm[a] : fp[a]);
+            int in = -1;
+            if ((mask >> a) & 1) {
+                const int bit = bitof[a];
+                const int64_t other = gl[a] + (((p >> bit) & 1) ^ 1);
+                if (other == qa) in = p ^ (1 << bit);
+            }
+            if (in >= 0) {
+#pragma unroll
+                for (int c = 0; c < k; ++c)
+                    if (c == in) Mr[c] = -m;
+            } else {
+                acc = fma(m, A.z[i + sd * S[a]], acc);
+            }
+        }
+    }
+    rhs = acc;
+}
+
+// Gaussian elimination of a gathered k x k set (rows in rank order) as in tri3t_solve.
+template <int K>
+__device__ __forceinline__ void tri3t_ge(double (&M)[K][K], double (&rhs)[K], double (&u)[K], int *flag, bool report) {
+    double inv[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+        const double piv = M[p][p];
+        if (report && !(fabs(piv) >= 1e-14)) atomicOr(flag, 1);
+        inv[p] = 1.0 / piv;
+#pragma unroll
+        for (int q = p + 1; q < K; ++q) {
+            const double l = M[q][p] * inv[p];
+#pragma unroll
+            for (int j = p + 1; j < K; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
+            rhs[q] = fma(-l, rhs[p], rhs[q]);
+        }
+    }
+#pragma unroll
+    for (int p = K - 1; p >= 0; --p) {
+        double s = rhs[p];
+#pragma unroll
+        for (int j = p + 1; j < K; ++j) s = fma(-M[p][j], u[j], s);
+        u[p] = s * inv[p];
+    }
+}
+
 template <int NA>
 __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
     const Geo &G = A.G;
@@ -135,28 +220,43 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
         lo_g[a] = R[a] * G.T[a];
     }
     const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
-    // this lane's line: the face (NA = 1) or edge axis (NA = 2), the fixed and the walked axes
-    int fa = -1, fixv = 0, walk = 0, fixax = 0;
-    {
-        int ln = threadIdx.x;
-        if (NA == 1) {
-            const int n0 = cpl[0] ? T2 : 0, n1 = cpl[1] ? T2 : 0, n2 = cpl[2] ? T1 : 0;
-            if (ln < n0) { fa = 0; fixax = 2; fixv = ln; walk = 1; }
-            else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
-            else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
-        } else if (NA == 2) {
-            if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; }
-        } else {
-            if (ln == 0 && cpl[0] && cpl[1] && cpl[2]) fa = 0;
-        }
-    }
     const int tmax = T0 > T1 ? (T0 > T2 ? T0 : T2) : (T1 > T2 ? T1 : T2);
-    const int dmax = (NA == 3) ? 0 : (NA == 2 ? tmax - 1 : T0 - 1 + (T1 > T2 ? T1 : T2) - 1);
+    if (NA == 3) {                                   // the corner set: one lane
+        if (threadIdx.x == 0 && cpl[0] && cpl[1] && cpl[2]) {
+            int64_t gl[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int64_t g = s[a] ? (lo_g[a] + G.T[a] - 1) : lo_g[a];
+                const int64_t other = s[a] ? (lo_g[a] + G.T[a]) : (lo_g[a] - 1);
+                gl[a] = other < g ? other : g;
+            }
+            tri3t_solve<3>(A, gl, 7);
+        }
+        return;
+    }
+    // NA = 1: lane pairs (2 members) per sheet line; NA = 2: lane quads (4 members) per edge.  Every
+    // lane builds its member's row, the group gathers the rows by shuffles and eliminates them
+    // redundantly, and each lane writes its member.
+    constexpr int K = 1 << NA;
+    const int p = threadIdx.x & (K - 1);
+    const int grp = threadIdx.x / K;                    // 16 sheet lines / 8 edge groups per pass
+    const int n0 = cpl[0] ? T2 : 0, n1 = cpl[1] ? T2 : 0, n2 = cpl[2] ? T1 : 0;
+    const int nlines = NA == 1 ? n0 + n1 + n2 : 3;
+    const int dmax = NA == 2 ? tmax - 1 : T0 - 1 + (T1 > T2 ? T1 : T2) - 1;
     for (int d = dmax; d >= 0; --d) {
-        if (fa >= 0) {
-            int l[3] = {0, 0, 0};
-            bool ok = true;
+        for (int base_ln = 0; base_ln < nlines; base_ln += 32 / K) {
+            int ln = base_ln + grp;
+            int fa = -1, fixv = 0, walk = 0, fixax = 0;
             if (NA == 1) {
+                if (ln < n0) { fa = 0; fixax = 2; fixv = ln; walk = 1; }
+                else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
+                else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
+            } else {
+                if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; }
+            }
+            bool ok = fa >= 0;
+            int l[3] = {0, 0, 0};
+            if (ok && NA == 1) {
                 l[fixax] = fixv;
                 l[walk] = d - fixv;
                 // the other two coordinates off the coupled start faces (else a set of higher
@@ -164,13 +264,13 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
                     if (a != fa && (l[a] < (cpl[a] ? 1 : 0) || l[a] >= G.T[a])) ok = false;
-            } else if (NA == 2) {
+            } else if (ok) {
                 l[walk] = d;
                 if (d < (cpl[walk] ? 1 : 0) || d >= G.T[walk]) ok = false;
             }
+            int64_t gl[3] = {0, 0, 0};
+            int mask = 0;
             if (ok) {
-                int64_t gl[3];
-                int mask = 0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     const int64_t g = s[a] ? (lo_g[a] + G.T[a] - 1 - l[a]) : (lo_g[a] + l[a]);
@@ -181,7 +281,27 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
                         if (other < gl[a]) gl[a] = other;
                     }
                 }
-                tri3t_solve<NA>(A, gl, mask);
+            }
+            double rhs = 0.0, Mr[K];
+            int64_t ix = 0;
+#pragma unroll
+            for (int c = 0; c < K; ++c) Mr[c] = (c == p) ? 1.0 : 0.0;
+            if (ok) tri3t_row<NA>(A, gl, mask, p, rhs, Mr, ix);
+            double Mall[K][K], rall[K], u[K];
+            const int src0 = threadIdx.x & ~(K - 1);
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                rall[q] = __shfl_sync(0xffffffffu, rhs, src0 + q);
+#pragma unroll
+                for (int c = 0; c < K; ++c) Mall[q][c] = __shfl_sync(0xffffffffu, Mr[c], src0 + q);
+            }
+            if (ok) {
+                tri3t_ge<K>(Mall, rall, u, A.flag, p == 0);
+                double mine = u[0];
+#pragma unroll
+                for (int c = 1; c < K; ++c)
+                    if (c == p) mine = u[c];
+                A.z[ix] = mine;
             }
         }
         __syncwarp();
