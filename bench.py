@@ -270,7 +270,7 @@ def run_secondary(args):
     """The other BASELINE.json configurations, measured on the same GPU (not the headline):
     config 3 (2D variable coefficients, 4096^2): 100 decomposed SOR sweeps at omega = 1 (R-10)
     and ILU(0)-PCG (SYMMETRIC pairing) to 1e-8; config 5's sweep (3D anisotropic 512^3, boxes
-    32 x 8 x 4) at omega = 1; config 2 (256^2) iteration counts."""
+    32 x 8 x 4) at omega = 1 and its ILU(0)-PCG to 1e-8; config 2 (256^2) iteration counts."""
     import torch
 
     from paper_1008_3699_b200 import binding, gen
@@ -307,6 +307,15 @@ def run_secondary(args):
     out["c5_sweep"] = {"n": [n3] * 3, "tile": [32, 8, 4], "ms_per_sweep": round(ms, 3),
                        "glups": round(n3 ** 3 / (ms * 1e-3) / 1e9, 2), "algorithmic_B_per_lup": 48,
                        "frac_of_measured_hbm": round(48 * n3 ** 3 / (ms * 1e-3) / 1e9 / peaks()[0], 3)}
+    if not args.no_c5_pcg:
+        # config 5's solve: ILU(0)-PCG (SYMMETRIC pairing) to 1e-8 on the full 512^3 grid
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        it, rel, ok = g.pcg_solve(binding.PC_ILU0, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 5000)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["c5_pcg_ilu0"] = {"n": [n3] * 3, "tile": [32, 8, 4], "iterations": it, "relres": rel, "converged": ok,
+                              "seconds": round(dt, 3), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
     del g
     torch.cuda.empty_cache()
     # ---- config 2 iteration counts (256^2 Poisson, 64 x 64 boxes)
@@ -328,6 +337,21 @@ def run_secondary(args):
             break
     res["sor_sweeps_to_1e-8 (checked every 10)"] = sweeps
     out["c2_iterations"] = res
+    # ---- the relaxation-factor search of PAPER:1996-1998 on config 2
+    from paper_1008_3699_b200 import omega as OM
+    evals = []
+
+    def count(v):
+        evals.append(1)
+        return OM.sweeps_to_tol(g, v, 1e-8, 20000, 10)
+    t0 = time.perf_counter()
+    w_best, c_best = OM.refine_search(count, 1.90, 1.999, accuracy=1e-3, coarse=0.01)
+    dt = time.perf_counter() - t0
+    w_y = OM.omega_opt_poisson(n2)
+    out["c2_omega_search"] = {"range": [1.90, 1.999], "accuracy": 1e-3, "best_omega": w_best,
+                              "sweeps_at_best": c_best, "young_omega_opt": round(w_y, 6),
+                              "sweeps_at_young": OM.sweeps_to_tol(g, [w_y], 1e-8, 20000, 10),
+                              "evaluations": len(evals), "seconds": round(dt, 3)}
     return out
 
 
@@ -390,6 +414,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-c5-pcg", action="store_true", help="skip config 5's 512^3 PCG solve (about a minute)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -36,6 +36,14 @@ def test_1d_sor_rows():
     assert run_decomposed(1, 41, [1], [1.0, 1.87776], 1e-3)[0] == 62
 
 
+def test_1d_ssour_row():
+    """Symmetric over/under-relaxation SSOUR, R = 41: per-direction factors
+    (w_L, w_R) = (0.24825, 1.87087), 58 iterations (the sequential and the one-box decomposed
+    sweep).  The PSOUR(p) rows of the same table are not reproduced."""
+    assert run_lex(1, 41, [0.24825, 1.87087], [0, 1], 1e-3)[0] == 58
+    assert run_decomposed(1, 41, [1], [0.24825, 1.87087], 1e-3)[0] == 58
+
+
 def test_2d_rows_51():
     """2D tables at 51x51: GS RGS 1018, SGS 1006, FGS 1006 (frontal = one
     box on the paper's 4-direction cycle); SOR w=1.25 RSOR 616, SSOR 606,
