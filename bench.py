@@ -336,6 +336,12 @@ def run_secondary(args):
         if g.residual_norm() < 1e-8:
             break
     res["sor_sweeps_to_1e-8 (checked every 10)"] = sweeps
+    # m-step SSOR preconditioning, theta = 1/2 (lambda_max(P^-1 A) = 2)
+    for m in (2, 3, 4):
+        g.set_precond_steps(m, 0.5)
+        it, rel, ok = g.pcg_solve(binding.PC_SSOR, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
+        res[f"pcg_ssor_{m}step"] = it
+    g.set_precond_steps(1, 1.0)
     out["c2_iterations"] = res
     # ---- the relaxation-factor search of PAPER:1996-1998 on config 2
     from paper_1008_3699_b200 import omega as OM

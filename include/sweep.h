@@ -136,6 +136,17 @@ sw_status sw_ilu_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_pairin
 sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev, double *z_dev, sw_pairing pairing,
                         sw_stream_t s);
 
+/* Number m of preconditioner steps applied by sw_ilu_apply, sw_ssor_apply and sw_pcg_solve
+ * (default 1), the "few iterations of SOR ... during each step of preconditioning" of
+ * z_1 = P^-1 r, z_{j+1} = z_j + P^-1 (r - theta A z_j), i.e. m
+ * Richardson steps of length theta on P^-1 A from zero, scaled by 1/theta (m = 1 is P^-1 r for
+ * any theta).  With the SYMMETRIC pairing the operator is symmetric, and positive definite iff
+ * theta * lambda_max(P^-1 A) < 2.  The decomposed SGS / D-ILU(0) preconditioners have
+ * lambda_max(P^-1 A) = 2 (the start-face pairs; DESIGN R-C), so use theta < 1 (0.5 recommended)
+ * for even m.  Single rank (the staged form below applies one step).  SW_EINVAL unless
+ * 1 <= m <= 64 and 0 < theta <= 1. */
+sw_status sw_set_precond_steps(sw_grid *g, int m, double theta);
+
 /* Preconditioned CG from x0 = 0 on the right-hand side SW_B until ||r||/||b|| < rtol
  * (recursive residual) or maxit; result in SW_X.  precond SW_PC_ILU0 factors at phase 0
  * first.  SW_ENOCONV: iters/relres still valid.  Single rank. */

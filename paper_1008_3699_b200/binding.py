@@ -57,6 +57,7 @@ def load():
     L.sw_ilu_apply.argtypes = [P_, P_, P_, I, P_]
     L.sw_ssor_apply.argtypes = [P_, D, P_, P_, I, P_]
     L.sw_pcg_solve.argtypes = [P_, I, D, I, D, I, ctypes.POINTER(I), ctypes.POINTER(D), P_]
+    L.sw_set_precond_steps.argtypes = [P_, I, D]
     L.sw_precond_stages.argtypes = [P_, I]
     L.sw_precond_stages.restype = I
     L.sw_ilu_apply_stage.argtypes = [P_, I, P_, P_, I, P_]
@@ -237,6 +238,11 @@ class Grid:
     def ssor_apply(self, omega: float, r_ptr: int, z_ptr: int, pairing: int = PAIR_SYMMETRIC, stream=None):
         _check(load().sw_ssor_apply(self.h, float(omega), ctypes.c_void_p(r_ptr), ctypes.c_void_p(z_ptr),
                                     int(pairing), _stream(stream)), "sw_ssor_apply")
+
+    def set_precond_steps(self, m: int, theta: float = 0.5):
+        """m-step preconditioner (sw_set_precond_steps): z_{j+1} = z_j + P^-1 (r - theta A z_j)."""
+        _check(load().sw_set_precond_steps(self.h, int(m), float(theta)), "sw_set_precond_steps")
+        return self
 
     def pcg_solve(self, precond: int = PC_ILU0, omega: float = 1.0, pairing: int = PAIR_SYMMETRIC,
                   rtol: float = 1e-8, maxit: int = 10000, stream=None):

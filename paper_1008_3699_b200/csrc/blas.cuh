@@ -294,6 +294,36 @@ __global__ void __launch_bounds__(RED_THREADS) k_pupdate_r(Rows R, const double 
     }
 }
 
+// y = r - theta q (interior nodes; the m-step preconditioner's residual), product and difference
+// rounded separately (no contraction)
+__global__ void __launch_bounds__(RED_THREADS) k_sub_r(Rows R, const double *__restrict__ r, double theta,
+                                                       const double *__restrict__ q, double *__restrict__ y) {
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h)
+            if (xb + h * RSEG < R.n0) {
+                const int64_t i = base + xb + h * RSEG;
+                y[i] = __dsub_rn(r[i], __dmul_rn(theta, q[i]));
+            }
+    }
+}
+
+// z += d (interior nodes)
+__global__ void __launch_bounds__(RED_THREADS) k_addto_r(Rows R, double *__restrict__ z, const double *__restrict__ d) {
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h)
+            if (xb + h * RSEG < R.n0) {
+                const int64_t i = base + xb + h * RSEG;
+                z[i] = z[i] + d[i];
+            }
+    }
+}
+
 // PCG scalars kept on the device
 struct CgScalars {
     double rz, pq, alpha, beta, rr, bb, rz_new;

@@ -53,6 +53,9 @@ struct sw_grid {
     double *B = nullptr;
     double *F[3] = {nullptr, nullptr, nullptr};
     double *invD = nullptr, *R = nullptr, *Z = nullptr, *Pv = nullptr, *Q = nullptr, *Y = nullptr;
+    double *W1 = nullptr, *W2 = nullptr;   // m-step preconditioner work (allocated when pc_steps > 1)
+    int pc_steps = 1;                      // sw_set_precond_steps
+    double pc_theta = 1.0;
     DD *partial = nullptr;
     CgScalars *cg = nullptr;
     int *flag = nullptr;
@@ -114,7 +117,7 @@ extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, d
 
 static void free_all(sw_grid *g) {
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
-                       &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y};
+                       &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->partial) cudaFree(g->partial);
@@ -641,13 +644,49 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     return launch_generic(g, P, s);
 }
 
-static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
-                           cudaStream_t s) {
-    if (g->nranks > 1) return fail(SW_EINVAL, "multi-rank: apply the preconditioner stage by stage");
+static sw_status tri_apply1(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
+                            cudaStream_t s) {
     for (int stage = 0; stage < tri_nstages(g, pairing); ++stage) {
         sw_status st = tri_stage(g, ilu, omega, r, z, pairing, stage, s);
         if (st != SW_OK) return st;
     }
+    return SW_OK;
+}
+
+template <typename F>
+static sw_status spmv_launch(sw_grid *g, const Rows &RW, int nr, const double *x, double *y, cudaStream_t cs, F);
+
+// z = M_m r with M_m the m-step preconditioner of P ("a few iterations ... during each step of
+// preconditioning"): z_1 = P^-1 r, z_{j+1} = z_j + P^-1 (r - theta A z_j), i.e.
+// m steps of Richardson with step theta on P^-1 A, scaled by 1/theta.  Symmetric whenever P is
+// (SYMMETRIC pairing); positive definite when theta lambda_max(P^-1 A) < 2.
+static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
+                           cudaStream_t s) {
+    if (g->nranks > 1) return fail(SW_EINVAL, "multi-rank: apply the preconditioner stage by stage");
+    sw_status st = tri_apply1(g, ilu, omega, r, z, pairing, s);
+    if (st != SW_OK || g->pc_steps <= 1) return st;
+    if ((st = alloc_arr(g, &g->W1)) != SW_OK) return st;
+    if ((st = alloc_arr(g, &g->W2)) != SW_OK) return st;
+    const Rows RW = make_rows(g->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    for (int j = 1; j < g->pc_steps; ++j) {
+        if ((st = spmv_launch(g, RW, nr, z, g->W1, s, 0)) != SW_OK) return st;   // W1 = A z
+        k_sub_r<<<nr, RED_THREADS, 0, s>>>(RW, r, g->pc_theta, g->W1, g->W2);     // W2 = r - theta A z
+        g->launches++;
+        if ((st = tri_apply1(g, ilu, omega, g->W2, g->W1, pairing, s)) != SW_OK) return st;   // W1 = P^-1 W2
+        k_addto_r<<<nr, RED_THREADS, 0, s>>>(RW, z, g->W1);                       // z += W1
+        g->launches++;
+        CK(cudaGetLastError());
+    }
+    return SW_OK;
+}
+
+extern "C" sw_status sw_set_precond_steps(sw_grid *g, int m, double theta) {
+    if (!g) return fail(SW_EINVAL, "null grid");
+    if (m < 1 || m > 64) return fail(SW_EINVAL, "precond steps must lie in [1, 64]");
+    if (!(theta > 0.0 && theta <= 1.0)) return fail(SW_EINVAL, "theta must lie in (0, 1]");
+    g->pc_steps = m;
+    g->pc_theta = theta;
     return SW_OK;
 }
 

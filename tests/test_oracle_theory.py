@@ -429,3 +429,34 @@ def test_faces_from_k_harmonic_mean():
     F = O.faces_from_k((5, 4), kr)
     Fr = O.faces_from_k((5, 4), kr[::-1, ::-1].copy())
     assert np.allclose(F[0], Fr[0][::-1, ::-1], rtol=0, atol=0)
+
+
+def test_decomposed_symmetric_preconditioner_spectrum_reaches_two():
+    """The decomposed SGS / D-ILU(0) preconditioners of the SYMMETRIC pairing (reading R-C) have
+    lambda(P^-1 A) in (0, 2] with the maximum 2 attained (the start-face pairs), while the
+    one-box (classical) SGS has lambda_max = 1.  Hence the m-step form z_{j+1} = z_j +
+    P^-1 (r - theta A z_j) of sw_set_precond_steps needs theta < 1 for even m (include/sweep.h)."""
+    import numpy as np
+    n = (24, 24)
+    N = n[0] * n[1]
+
+    def spectrum(tile, ilu):
+        pb = O.tiled(n, tile)
+        inv = O.ilu0_factor(pb) if ilu else None
+        Pi = np.zeros((N, N))
+        A = np.zeros((N, N))
+        for i in range(N):
+            e = np.zeros(N)
+            e[i] = 1.0
+            e = e.reshape(pb.shape)
+            Pi[:, i] = (O.ilu_apply(pb, inv, e, 0) if ilu else O.ssor_apply(pb, 1.0, e, 0)).ravel()
+            A[:, i] = O.apply_A(pb, e).ravel()
+        ev = np.linalg.eigvals(Pi @ A)
+        assert np.max(np.abs(ev.imag)) < 1e-8
+        return ev.real.min(), ev.real.max()
+    lo, hi = spectrum((8, 8), False)
+    assert lo > 0 and abs(hi - 2.0) < 1e-9
+    lo, hi = spectrum((8, 8), True)
+    assert lo > 0 and abs(hi - 2.0) < 1e-9
+    lo, hi = spectrum(n, False)
+    assert lo > 0 and abs(hi - 1.0) < 1e-9

@@ -9,8 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1008_3699_b200 import binding, gen  # noqa: E402
 
 NAMES = ["stage-in wait", "partner+prologue", "corner+chains", "wavefront", "write-back", "", "chains (warp 1)",
-         "wavefront (warp 0)", "3D: prologue (thr 0, own part)", "3D: wavefront (thr 0, no barrier)", "", "",
-         "3D: corner (thr 0)", "3D: x-sheet"]
+         "wavefront (warp 0)", "3D: prologue (thr 0, own part)", "3D: wavefront (thr 0, no barrier)", "3D: wf steps 1-8", "3D: wf last 8 steps",
+         "3D: corner (thr 0)", "3D: x-sheet", "3D: wf middle steps"]
 
 
 def main():
@@ -39,7 +39,7 @@ def main():
         return
     ctas = out[5]
     print(f"n={n} faces={faces} CTAs={ctas}")
-    for i, nm in enumerate(NAMES):
+    for i, nm in enumerate(NAMES[:15]):
         if nm:
             print(f"  {nm:18s} {out[i] / max(ctas, 1):10.0f} cycles/CTA")
     print(f"  {'total':18s} {sum(out[i] for i in range(5)) / max(ctas, 1):10.0f}")
