@@ -54,7 +54,7 @@ typedef enum {
 } sw_status;
 
 typedef enum { SW_COEF_POISSON = 0, SW_COEF_FACES = 1 } sw_coef;
-typedef enum { SW_PC_NONE = 0, SW_PC_SSOR = 1, SW_PC_ILU0 = 2 } sw_precond;
+typedef enum { SW_PC_NONE = 0, SW_PC_SSOR = 1, SW_PC_ILU0 = 2, SW_PC_MG = 3 } sw_precond;
 /* SYMMETRIC: P = (D~+L) D~^-1 (D~+L)^T;  PAPER: P = (D~+L) D~^-1 (D~+U), U = A_E(k0) (R-C) */
 typedef enum { SW_PAIR_SYMMETRIC = 0, SW_PAIR_PAPER = 1 } sw_pairing;
 typedef enum { SW_X = 0, SW_B = 1, SW_R = 2, SW_Z = 3, SW_P = 4, SW_Q = 5, SW_INVD = 6, SW_Y = 7 } sw_vector;
@@ -146,6 +146,24 @@ sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev, double *z
  * for even m.  Single rank (the staged form below applies one step).  SW_EINVAL unless
  * 1 <= m <= 64 and 0 < theta <= 1. */
 sw_status sw_set_precond_steps(sw_grid *g, int m, double theta);
+
+/* Geometric multigrid preconditioner (the decomposed sweep as the smoother
+ * inside multigrid).  Builds `levels` - 1 coarse grids by halving the
+ * node count per axis (every level must have even counts): piecewise-constant aggregation of
+ * 2^d fine nodes, restriction R = P^T and the Galerkin operator R A P, which is again a
+ * face-coefficient operator (coarse face = sum of the 2^(d-1) fine faces it covers, beta_c =
+ * 2^d beta; DESIGN R-19).  Coarse boxes: the fine box shape, shrunk to divide the level.
+ * The symmetric V-cycle (sw_mg_apply, and SW_PC_MG in sw_pcg_solve): nu Richardson steps of length
+ * theta on P^-1 A from zero, P the decomposed SGS (SYMMETRIC pairing), i.e. theta times the m-step
+ * operator of sw_set_precond_steps, before and after the coarse correction, which is added scaled by coarse_scale (the usual
+ * over-correction of piecewise-constant interpolation; any value > 0 keeps the V-cycle symmetric
+ * positive definite); on the coarsest level nu_coarse steps.  Single rank.  SW_EINVAL for levels
+ * outside [2, 16], nu outside [1, 64], nu_coarse outside [1, 1024], theta outside (0, 1],
+ * coarse_scale outside (0, 4] or an odd count on a level to be coarsened. */
+sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale);
+
+/* z = B r, one V-cycle from zero (padded device arrays as for sw_ilu_apply; borrowed). */
+sw_status sw_mg_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_stream_t s);
 
 /* Preconditioned CG from x0 = 0 on the right-hand side SW_B until ||r||/||b|| < rtol
  * (recursive residual) or maxit; result in SW_X.  precond SW_PC_ILU0 factors at phase 0

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libsweep.so")
 
 SW_OK, SW_EINVAL, SW_ESINGULAR, SW_ENOCONV, SW_ECUDA, SW_ENOMEM, SW_ESTATE = 0, 1, 2, 3, 4, 6, 7
 COEF_POISSON, COEF_FACES = 0, 1
-PC_NONE, PC_SSOR, PC_ILU0 = 0, 1, 2
+PC_NONE, PC_SSOR, PC_ILU0, PC_MG = 0, 1, 2, 3
 PAIR_SYMMETRIC, PAIR_PAPER = 0, 1
 X, B, R, Z, P, Q, INVD, Y = range(8)
 
@@ -58,6 +58,8 @@ def load():
     L.sw_ssor_apply.argtypes = [P_, D, P_, P_, I, P_]
     L.sw_pcg_solve.argtypes = [P_, I, D, I, D, I, ctypes.POINTER(I), ctypes.POINTER(D), P_]
     L.sw_set_precond_steps.argtypes = [P_, I, D]
+    L.sw_mg_setup.argtypes = [P_, I, I, D, I, D]
+    L.sw_mg_apply.argtypes = [P_, P_, P_, P_]
     L.sw_precond_stages.argtypes = [P_, I]
     L.sw_precond_stages.restype = I
     L.sw_ilu_apply_stage.argtypes = [P_, I, P_, P_, I, P_]
@@ -243,6 +245,15 @@ class Grid:
         """m-step preconditioner (sw_set_precond_steps): z_{j+1} = z_j + P^-1 (r - theta A z_j)."""
         _check(load().sw_set_precond_steps(self.h, int(m), float(theta)), "sw_set_precond_steps")
         return self
+
+    def mg_setup(self, levels: int, nu: int = 1, theta: float = 0.5, nu_coarse: int = 8, coarse_scale: float = 1.0):
+        """Geometric multigrid preconditioner with the decomposed sweep as smoother (sw_mg_setup)."""
+        _check(load().sw_mg_setup(self.h, int(levels), int(nu), float(theta), int(nu_coarse), float(coarse_scale)),
+               "sw_mg_setup")
+        return self
+
+    def mg_apply(self, r_ptr: int, z_ptr: int, stream=None):
+        _check(load().sw_mg_apply(self.h, ctypes.c_void_p(r_ptr), ctypes.c_void_p(z_ptr), _stream(stream)), "sw_mg_apply")
 
     def pcg_solve(self, precond: int = PC_ILU0, omega: float = 1.0, pairing: int = PAIR_SYMMETRIC,
                   rtol: float = 1e-8, maxit: int = 10000, stream=None):

@@ -324,6 +324,20 @@ __global__ void __launch_bounds__(RED_THREADS) k_addto_r(Rows R, double *__restr
     }
 }
 
+// x = s x (interior nodes)
+__global__ void __launch_bounds__(RED_THREADS) k_scale_r(Rows R, double sc, double *__restrict__ x) {
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h)
+            if (xb + h * RSEG < R.n0) {
+                const int64_t i = base + xb + h * RSEG;
+                x[i] = sc * x[i];
+            }
+    }
+}
+
 // PCG scalars kept on the device
 struct CgScalars {
     double rz, pq, alpha, beta, rr, bb, rz_new;

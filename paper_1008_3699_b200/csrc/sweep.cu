@@ -19,6 +19,8 @@
 #include "tri2t.cuh"
 #include "sweep3.cuh"
 #include "tri3t.cuh"
+#include "mg.cuh"
+#include <vector>
 
 using namespace sw;
 
@@ -56,6 +58,12 @@ struct sw_grid {
     double *W1 = nullptr, *W2 = nullptr;   // m-step preconditioner work (allocated when pc_steps > 1)
     int pc_steps = 1;                      // sw_set_precond_steps
     double pc_theta = 1.0;
+    // geometric multigrid (sw_mg_setup): coarse levels 1.., and per level the V-cycle's right-hand
+    // side / correction (MGR, MGX, coarse levels) and two temporaries (MT1, MT2)
+    std::vector<sw_grid *> mg;
+    int mg_nu = 1, mg_nu_coarse = 8;
+    double mg_theta = 0.5, mg_scale = 1.0;
+    double *MGR = nullptr, *MGX = nullptr, *MT1 = nullptr, *MT2 = nullptr;
     DD *partial = nullptr;
     CgScalars *cg = nullptr;
     int *flag = nullptr;
@@ -115,9 +123,14 @@ extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, d
     return SW_OK;
 }
 
+extern "C" sw_status sw_destroy(sw_grid *g);
+
 static void free_all(sw_grid *g) {
+    for (sw_grid *c : g->mg) sw_destroy(c);
+    g->mg.clear();
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
-                       &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2};
+                       &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2,
+                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->partial) cudaFree(g->partial);
@@ -681,6 +694,142 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     return SW_OK;
 }
 
+// ---------------------------------------------------------------- geometric multigrid (N1)
+extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->nranks > 1) return fail(SW_EINVAL, "multigrid is single-rank in this build");
+    if (levels < 2 || levels > 16 || nu < 1 || nu > 64 || nu_coarse < 1 || nu_coarse > 1024 ||
+        !(theta > 0.0 && theta <= 1.0) || !(coarse_scale > 0.0 && coarse_scale <= 4.0))
+        return fail(SW_EINVAL, "bad multigrid parameters");
+    g->mg_scale = coarse_scale;
+    for (sw_grid *c : g->mg) sw_destroy(c);
+    g->mg.clear();
+    g->mg_nu = nu;
+    g->mg_theta = theta;
+    g->mg_nu_coarse = nu_coarse;
+    sw_status st;
+    if ((st = ensure_work(g)) != SW_OK) return st;
+    const double *const *src_faces = g->G.poisson ? nullptr : g->F;
+    sw_grid *fine = g;
+    for (int l = 1; l < levels; ++l) {
+        int64_t nc[3] = {1, 1, 1};
+        int tc[3] = {1, 1, 1};
+        for (int a = 0; a < g->dim; ++a) {
+            if (fine->ng[a] % 2) return fail(SW_EINVAL, "every level must have an even node count per axis");
+            nc[a] = fine->ng[a] / 2;
+            tc[a] = fine->tile[a] <= nc[a] ? fine->tile[a] : (int)nc[a];
+            while (nc[a] % tc[a]) --tc[a];
+        }
+        sw_grid *c = nullptr;
+        double bc = fine->beta * (double)(1 << g->dim);
+        if ((st = sw_create_grid(g->dim, nc, SW_COEF_FACES, bc, g->dev, &c)) != SW_OK) return st;
+        g->mg.push_back(c);
+        c->fast2d = g->fast2d;
+        if ((st = sw_decompose(c, tc, 0, 1)) != SW_OK) return st;
+        if ((st = ensure_work(c)) != SW_OK) return st;
+        for (int a = 0; a < g->dim; ++a) {
+            const double *ff = (fine == g) ? (src_faces ? src_faces[a] : nullptr) : fine->F[a];
+            const int64_t tot = (nc[0] + (a == 0)) * (nc[1] + (a == 1)) * (nc[2] + (a == 2));
+            const int nb = (int)std::min<int64_t>((tot + 255) / 256, 4096);
+            if (g->dim == 1) k_coarsen_faces<1><<<nb, 256>>>(fine->G, c->G, a, ff, c->F[a]);
+            else if (g->dim == 2) k_coarsen_faces<2><<<nb, 256>>>(fine->G, c->G, a, ff, c->F[a]);
+            else k_coarsen_faces<3><<<nb, 256>>>(fine->G, c->G, a, ff, c->F[a]);
+            CK(cudaGetLastError());
+        }
+        CK(cudaDeviceSynchronize());
+        double **ptrs[] = {&c->MGR, &c->MGX, &c->MT1, &c->MT2};
+        for (double **p : ptrs)
+            if ((st = alloc_arr(c, p)) != SW_OK) return st;
+        fine = c;
+    }
+    double **ptrs[] = {&g->MT1, &g->MT2};
+    for (double **p : ptrs)
+        if ((st = alloc_arr(g, p)) != SW_OK) return st;
+    return SW_OK;
+}
+
+static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
+                           cudaStream_t s);
+
+// x = S r with the level's smoother S = m Richardson steps of length theta on P^-1 A from zero, P
+// the decomposed SGS (SYMMETRIC pairing): S = theta M_m (the m-step operator of tri_apply).  A
+// damped step is needed because lambda_max(P^-1 A) = 2 (DESIGN R-C).
+static sw_status mg_smooth(sw_grid *l, const double *r, double *x, int m, double theta, cudaStream_t s) {
+    const int keep_m = l->pc_steps;
+    const double keep_t = l->pc_theta;
+    l->pc_steps = m;
+    l->pc_theta = theta;
+    l->factor_phase = 0;
+    sw_status st = tri_apply(l, false, 1.0, r, x, SW_PAIR_SYMMETRIC, s);
+    l->pc_steps = keep_m;
+    l->pc_theta = keep_t;
+    if (st != SW_OK || theta == 1.0) return st;
+    const Rows RW = make_rows(l->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    k_scale_r<<<nr, RED_THREADS, 0, s>>>(RW, theta, x);
+    l->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+static sw_status mg_residual(sw_grid *l, const double *r, const double *x, double *out, cudaStream_t s) {
+    const Rows RW = make_rows(l->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    sw_status st = spmv_launch(l, RW, nr, x, l->MT1, s, 0);   // MT1 = A x
+    if (st != SW_OK) return st;
+    k_sub_r<<<nr, RED_THREADS, 0, s>>>(RW, r, 1.0, l->MT1, out);
+    l->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+// One symmetric V-cycle on level `lev` (0 = g): x = B r.
+static sw_status mg_vcycle(sw_grid *g, int lev, const double *r, double *x, cudaStream_t s) {
+    sw_grid *l = lev == 0 ? g : g->mg[lev - 1];
+    const int nlev = (int)g->mg.size() + 1;
+    sw_status st;
+    if (lev == nlev - 1) return mg_smooth(l, r, x, g->mg_nu_coarse, g->mg_theta, s);
+    if ((st = mg_smooth(l, r, x, g->mg_nu, g->mg_theta, s)) != SW_OK) return st;          // pre-smoothing
+    if ((st = mg_residual(l, r, x, l->MT2, s)) != SW_OK) return st;                      // MT2 = r - A x
+    sw_grid *c = g->mg[lev];
+    const int64_t nct = c->G.n[0] * c->G.n[1] * c->G.n[2];
+    const int nbc = (int)std::min<int64_t>((nct + 255) / 256, 8192);
+    if (g->dim == 1) k_restrict<1><<<nbc, 256, 0, s>>>(l->G, c->G, l->MT2, c->MGR);
+    else if (g->dim == 2) k_restrict<2><<<nbc, 256, 0, s>>>(l->G, c->G, l->MT2, c->MGR);
+    else k_restrict<3><<<nbc, 256, 0, s>>>(l->G, c->G, l->MT2, c->MGR);
+    l->launches++;
+    CK(cudaGetLastError());
+    if ((st = mg_vcycle(g, lev + 1, c->MGR, c->MGX, s)) != SW_OK) return st;             // coarse correction
+    const int64_t nft = l->G.n[0] * l->G.n[1] * l->G.n[2];
+    const int nbf = (int)std::min<int64_t>((nft + 255) / 256, 8192);
+    if (g->dim == 1) k_prolong_add<1><<<nbf, 256, 0, s>>>(l->G, c->G, g->mg_scale, c->MGX, x);
+    else if (g->dim == 2) k_prolong_add<2><<<nbf, 256, 0, s>>>(l->G, c->G, g->mg_scale, c->MGX, x);
+    else k_prolong_add<3><<<nbf, 256, 0, s>>>(l->G, c->G, g->mg_scale, c->MGX, x);
+    l->launches++;
+    CK(cudaGetLastError());
+    if ((st = mg_residual(l, r, x, l->MT2, s)) != SW_OK) return st;                      // MT2 = r - A x
+    if ((st = mg_smooth(l, l->MT2, l->MT1, g->mg_nu, g->mg_theta, s)) != SW_OK) return st;   // post-smoothing
+    const Rows RW = make_rows(l->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    k_addto_r<<<nr, RED_THREADS, 0, s>>>(RW, x, l->MT1);
+    l->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+extern "C" sw_status sw_mg_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->mg.empty()) return fail(SW_ESTATE, "sw_mg_setup must precede sw_mg_apply");
+    if (!r_dev || !z_dev || r_dev == z_dev || z_dev == g->Y || z_dev == g->MT1 || z_dev == g->MT2)
+        return fail(SW_EINVAL, "bad r/z pointers");
+    sw_status st = mg_vcycle(g, 0, r_dev, z_dev, (cudaStream_t)s);
+    for (sw_grid *c : g->mg) {                     // one launch count and one status for the whole hierarchy
+        g->launches += c->launches;
+        c->launches = 0;
+    }
+    return st;
+}
+
 extern "C" sw_status sw_set_precond_steps(sw_grid *g, int m, double theta) {
     if (!g) return fail(SW_EINVAL, "null grid");
     if (m < 1 || m > 64) return fail(SW_EINVAL, "precond steps must lie in [1, 64]");
@@ -735,8 +884,10 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         g->factor_phase = 0;
     }
     double *z = (pc == SW_PC_NONE) ? g->R : g->Z;
+    if (pc == SW_PC_MG && g->mg.empty()) return fail(SW_ESTATE, "sw_mg_setup must precede SW_PC_MG");
     auto apply_pc = [&]() -> sw_status {
         if (pc == SW_PC_NONE) return SW_OK;
+        if (pc == SW_PC_MG) return sw_mg_apply(g, g->R, g->Z, s);
         return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, cs);
     };
     // row-segment kernels, launch shape fixed per grid (deterministic reductions)

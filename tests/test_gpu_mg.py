@@ -1,0 +1,133 @@
+"""Geometric multigrid with the decomposed sweep as smoother: one V-cycle
+through the C ABI (sw_mg_setup / sw_mg_apply) against the same V-cycle composed from oracle calls
+(piecewise-constant aggregation, Galerkin face sums, m-step SGS smoothing, DESIGN R-17/R-19), and
+MG-preconditioned CG."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_1008_3699_b200 import binding as B, gen
+from tests.gpu_helpers import make_grid, rand_faces, rel_maxdiff
+
+pytestmark = pytest.mark.gpu
+
+
+# ---- the oracle-side V-cycle (numpy + oracle calls; sums in the order DESIGN R-19 fixes)
+def coarsen_faces(faces, n):
+    dim = len(n)
+    out = []
+    for a in range(dim):
+        f = np.ones(O.face_shape(n, a)) if faces is None else np.asarray(faces[a])
+        ax = dim - 1 - a                                   # numpy axis of grid axis a
+        g = np.take(f, np.arange(0, f.shape[ax], 2), axis=ax)          # the faces at even positions along a
+        others = [b for b in range(dim) if b != a]         # ascending grid axes
+        if dim == 1:
+            out.append(g)
+            continue
+        b = others[0]
+        nb = dim - 1 - b
+        h = np.take(g, np.arange(0, g.shape[nb], 2), axis=nb) + np.take(g, np.arange(1, g.shape[nb], 2), axis=nb)
+        if dim == 3:
+            c = others[1]
+            nc = dim - 1 - c
+            h = np.take(h, np.arange(0, h.shape[nc], 2), axis=nc) + np.take(h, np.arange(1, h.shape[nc], 2), axis=nc)
+        out.append(h)
+    return tuple(out)
+
+
+def restrict(r):
+    dim = r.ndim
+    v = r[..., 0::2] + r[..., 1::2]
+    if dim > 1:
+        v = v[..., 0::2, :] + v[..., 1::2, :]
+    if dim > 2:
+        v = v[0::2] + v[1::2]
+    return v
+
+
+def prolong(xc):
+    for ax in range(xc.ndim):
+        xc = np.repeat(xc, 2, axis=ax)
+    return xc
+
+
+def coarse_tile(t, nc):
+    t = min(t, nc)
+    while nc % t:
+        t -= 1
+    return t
+
+
+def build_levels(n, tile, faces, beta, levels):
+    lv = [(tuple(n), tuple(tile), faces, beta)]
+    for _ in range(levels - 1):
+        n0, t0, f0, b0 = lv[-1]
+        nc = tuple(v // 2 for v in n0)
+        tc = tuple(coarse_tile(t, v) for t, v in zip(t0, nc))
+        lv.append((nc, tc, coarsen_faces(f0, n0), b0 * 2 ** len(n)))
+    return [O.tiled(nn, tt, faces=ff, beta=bb) for nn, tt, ff, bb in lv]
+
+
+def smooth(pb, r, m, theta):
+    z = O.ssor_apply(pb, 1.0, r, 0)
+    for _ in range(m - 1):
+        z = z + O.ssor_apply(pb, 1.0, r - theta * O.apply_A(pb, z), 0)
+    return theta * z
+
+
+def vcycle(pbs, lev, r, nu, theta, nu_c, sc=1.0):
+    pb = pbs[lev]
+    if lev == len(pbs) - 1:
+        return smooth(pb, r, nu_c, theta)
+    x = smooth(pb, r, nu, theta)
+    xc = vcycle(pbs, lev + 1, restrict(r - O.apply_A(pb, x)), nu, theta, nu_c, sc)
+    x = x + sc * prolong(xc)
+    return x + smooth(pb, r - O.apply_A(pb, x), nu, theta)
+
+
+CASES = [((256, 256), (64, 64), False, 0.0, 3), ((128, 128), (64, 64), True, 0.0, 4),
+         ((64, 32, 32), (32, 8, 4), True, 0.0, 3), ((32, 32, 32), (16, 8, 4), False, 0.1, 3)]
+
+
+@pytest.mark.parametrize("n,tile,var,beta,levels", CASES)
+@pytest.mark.parametrize("nu,theta,sc", [(1, 0.5, 1.0), (2, 0.6, 1.7)])
+def test_vcycle_matches_oracle(n, tile, var, beta, levels, nu, theta, sc):
+    faces = rand_faces(n, 17) if var else None
+    pbs = build_levels(n, tile, faces, beta, levels)
+    r = gen.uniform_field(8, gen.STREAM_TEST, pbs[0].shape)
+    g = make_grid(B, n, tile, faces, beta).mg_setup(levels, nu, theta, 6, sc)
+    g.set_vector(B.R, r)
+    g.mg_apply(g.ptr(B.R), g.ptr(B.Z))
+    torch.cuda.synchronize()
+    g.check()
+    want = vcycle(pbs, 0, r, nu, theta, 6, sc)
+    assert rel_maxdiff(g.get_vector(B.Z), want) <= 1e-12
+
+
+@pytest.mark.parametrize("n,tile,var,levels", [((256, 256), (64, 64), True, 4), ((64, 64, 64), (32, 8, 4), True, 3)])
+def test_mg_pcg_converges_in_few_iterations(n, tile, var, levels):
+    faces = rand_faces(n, 19) if var else None
+    pb = O.tiled(n, tile, faces=faces)
+    b = gen.uniform_field(0, gen.STREAM_RHS, pb.shape) / float((n[0] + 1) ** 2)
+    g = make_grid(B, n, tile, faces)
+    g.set_vector(B.B, b)
+    it_ilu, _, ok = g.pcg_solve(B.PC_ILU0, 1.0, B.PAIR_SYMMETRIC, 1e-8, 5000)
+    assert ok
+    g.mg_setup(levels, 1, 0.5, 16)
+    it_mg, rel, ok = g.pcg_solve(B.PC_MG, 1.0, B.PAIR_SYMMETRIC, 1e-8, 5000)
+    assert ok and it_mg < it_ilu / 2, (it_mg, it_ilu)
+    assert O.relres(pb, g.get_vector(B.X), b) < 2e-8
+
+
+def test_mg_setup_validation():
+    g = make_grid(B, (192, 192), (64, 64))
+    with pytest.raises(B.SweepError):
+        g.mg_setup(1)
+    with pytest.raises(B.SweepError):
+        g.mg_setup(8)            # 192 -> 96 -> 48 -> 24 -> 12 -> 6 -> 3, then an odd count
+    g2 = make_grid(B, (192, 192), (64, 64))
+    with pytest.raises(B.SweepError):
+        g2.mg_setup(3, 1, 1.5)
+    with pytest.raises(B.SweepError):
+        make_grid(B, (192, 192), (64, 64)).pcg_solve(B.PC_MG)
