@@ -64,6 +64,8 @@ struct sw_grid {
     int mg_nu = 1, mg_nu_coarse = 8;
     double mg_theta = 0.5, mg_scale = 1.0;
     double *MGR = nullptr, *MGX = nullptr, *MT1 = nullptr, *MT2 = nullptr;
+    CgScalars *hcg = nullptr;              // pinned host copy of the PCG scalars
+    cudaStream_t cap_stream = nullptr;     // private stream for CUDA-graph capture
     DD *partial = nullptr;
     CgScalars *cg = nullptr;
     int *flag = nullptr;
@@ -133,6 +135,10 @@ static void free_all(sw_grid *g) {
                        &g->MGR,  &g->MGX,  &g->MT1, &g->MT2};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
+    if (g->hcg) cudaFreeHost(g->hcg);
+    g->hcg = nullptr;
+    if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+    g->cap_stream = nullptr;
     if (g->partial) cudaFree(g->partial);
     if (g->cg) cudaFree(g->cg);
     if (g->flag) cudaFree(g->flag);
@@ -504,6 +510,12 @@ extern "C" sw_status sw_check_status(sw_grid *g, sw_stream_t s) {
     CK(cudaStreamSynchronize((cudaStream_t)s));
     int f = 0;
     CK(cudaMemcpy(&f, g->flag, sizeof(int), cudaMemcpyDeviceToHost));
+    for (sw_grid *c : g->mg) {                     // multigrid levels keep their own flags
+        int fc = 0;
+        CK(cudaMemcpy(&fc, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
+        if (fc) CK(cudaMemset(c->flag, 0, sizeof(int)));
+        f |= fc;
+    }
     if (f) {
         CK(cudaMemset(g->flag, 0, sizeof(int)));
         return fail(SW_ESINGULAR, "singular coupled system or non-positive ILU pivot");
@@ -871,10 +883,9 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     if (!iters_out || !relres_out || maxit < 1 || !(rtol > 0)) return fail(SW_EINVAL, "bad arguments");
     sw_status st = ensure_work(g);
     if (st != SW_OK) return st;
-    cudaStream_t cs = (cudaStream_t)s;
+    const cudaStream_t cs = (cudaStream_t)s;
+    cudaStream_t ws = cs;                       // the stream the iteration's work is issued on
     const Geo &G = g->G;
-    int64_t N = G.n[0] * G.n[1] * G.n[2];
-    int nb = grid_blocks(N, RED_THREADS);
     double *x = g->X[g->cur];
     CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)g->nelem, cs));
     CK(cudaMemcpyAsync(g->R, g->B, sizeof(double) * (size_t)g->nelem, cudaMemcpyDeviceToDevice, cs));
@@ -887,8 +898,8 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     if (pc == SW_PC_MG && g->mg.empty()) return fail(SW_ESTATE, "sw_mg_setup must precede SW_PC_MG");
     auto apply_pc = [&]() -> sw_status {
         if (pc == SW_PC_NONE) return SW_OK;
-        if (pc == SW_PC_MG) return sw_mg_apply(g, g->R, g->Z, s);
-        return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, cs);
+        if (pc == SW_PC_MG) return sw_mg_apply(g, g->R, g->Z, ws);
+        return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, ws);
     };
     // row-segment kernels, launch shape fixed per grid (deterministic reductions)
     const Rows RW = make_rows(G);
@@ -896,15 +907,17 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     const bool fc = !G.poisson;
     auto spmv = [&]() {
         const double *F0 = g->F[0], *F1 = g->F[1], *F2 = g->F[2];
-        if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
-                            : k_spmv_dot_r<1, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
-        else if (g->dim == 2) fc ? k_spmv_dot_r<2, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
-                                 : k_spmv_dot_r<2, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
-        else fc ? k_spmv_dot_r<3, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
-                : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
+                            : k_spmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        else if (g->dim == 2) fc ? k_spmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
+                                 : k_spmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        else fc ? k_spmv_dot_r<3, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
+                : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
         g->launches++;
     };
-    // b.b
+    if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars)));   // pinned: the readback is a graph node
+    CgScalars &h = *g->hcg;
+    // b.b, z0 = P^-1 r0, r.z, p = z
     k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->B, g->B, g->partial);
     g->launches++;
     if ((st = finish(g, nr, 1, 0, &g->cg->bb, cs)) != SW_OK) return st;
@@ -914,37 +927,97 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     if ((st = finish(g, nr, 1, 0, &g->cg->rz, cs)) != SW_OK) return st;
     k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 1, z, g->Pv);
     g->launches++;
-    CgScalars h;
     CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
     CK(cudaStreamSynchronize(cs));
-    double bnorm = sqrt(h.bb);
+    const double bnorm = sqrt(h.bb);
     *iters_out = 0;
     *relres_out = 1.0;
     if (bnorm == 0.0) { *relres_out = 0.0; return SW_OK; }
-    for (int it = 1; it <= maxit; ++it) {
+    // q = A p, alpha, x += alpha p, r -= alpha q (r.r), and the readback of the scalars
+    auto head = [&]() -> sw_status {
         spmv();
-        if ((st = finish(g, nr, 1, 0, &g->cg->pq, cs)) != SW_OK) return st;
-        k_cg_alpha<<<1, 1, 0, cs>>>(g->cg);
+        sw_status t = finish(g, nr, 1, 0, &g->cg->pq, ws);
+        if (t != SW_OK) return t;
+        k_cg_alpha<<<1, 1, 0, ws>>>(g->cg);
         g->launches++;
-        k_axpy2_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->alpha, x, g->R, g->Pv, g->Q, g->partial);
+        k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, g->Pv, g->Q, g->partial);
         g->launches++;
-        if ((st = finish(g, nr, 1, 0, &g->cg->rr, cs)) != SW_OK) return st;
-        CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
-        CK(cudaStreamSynchronize(cs));
-        *iters_out = it;
-        *relres_out = sqrt(h.rr) / bnorm;
-        if (*relres_out < rtol) return sw_check_status(g, s);
-        if (!(h.rr == h.rr)) return fail(SW_ENOCONV, "PCG produced NaN");
-        if ((st = apply_pc()) != SW_OK) return st;
-        k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->R, z, g->partial);
+        if ((t = finish(g, nr, 1, 0, &g->cg->rr, ws)) != SW_OK) return t;
+        CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, ws));
+        return SW_OK;
+    };
+    // z = P^-1 r, r.z, beta, p = z + beta p
+    auto tail = [&]() -> sw_status {
+        sw_status t = apply_pc();
+        if (t != SW_OK) return t;
+        k_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, g->R, z, g->partial);
         g->launches++;
-        if ((st = finish(g, nr, 1, 0, &g->cg->rz_new, cs)) != SW_OK) return st;
-        k_cg_beta<<<1, 1, 0, cs>>>(g->cg);
+        if ((t = finish(g, nr, 1, 0, &g->cg->rz_new, ws)) != SW_OK) return t;
+        k_cg_beta<<<1, 1, 0, ws>>>(g->cg);
         g->launches++;
-        k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 0, z, g->Pv);
+        k_pupdate_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->beta, 0, z, g->Pv);
         g->launches++;
         CK(cudaGetLastError());
+        return SW_OK;
+    };
+    // Iterations 2.. replay one CUDA graph of tail + head (tens of launches, hundreds with the
+    // multigrid preconditioner): one launch and one synchronisation per iteration.
+    static const bool no_graph = getenv("SW_NO_GRAPH") != nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t graph_launches = 0;
+    bool graph_ok = !no_graph;
+    auto cleanup = [&]() {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+    };
+    for (int it = 1; it <= maxit; ++it) {
+        if (it == 1) {
+            ws = cs;
+            if ((st = head()) != SW_OK) return st;
+        } else if (graph_ok && !exec) {
+            // capture on a private stream (the caller's may be the legacy default stream)
+            if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+            CK(cudaStreamSynchronize(cs));
+            const int64_t l0 = g->launches;
+            cudaGraph_t graph = nullptr;
+            ws = g->cap_stream;
+            bool ok = cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            sw_status t1 = ok ? tail() : SW_OK;
+            sw_status t2 = (ok && t1 == SW_OK) ? head() : SW_OK;
+            const cudaError_t ce = ok ? cudaStreamEndCapture(ws, &graph) : cudaErrorUnknown;
+            ws = cs;
+            graph_launches = g->launches - l0;
+            g->launches = l0;
+            if (ok && t1 == SW_OK && t2 == SW_OK && ce == cudaSuccess && graph &&
+                cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+                cudaGraphDestroy(graph);
+            } else {                                   // no graph: run the iteration as plain launches
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                graph_ok = false;
+                exec = nullptr;
+                if ((st = tail()) != SW_OK) return st;
+                if ((st = head()) != SW_OK) return st;
+            }
+            if (exec) {
+                if (cudaGraphLaunch(exec, cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "cudaGraphLaunch"); }
+                g->launches += graph_launches;
+            }
+        } else if (exec) {
+            if (cudaGraphLaunch(exec, cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "cudaGraphLaunch"); }
+            g->launches += graph_launches;
+        } else {
+            ws = cs;
+            if ((st = tail()) != SW_OK) return st;
+            if ((st = head()) != SW_OK) return st;
+        }
+        if (cudaStreamSynchronize(cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "PCG iteration failed"); }
+        *iters_out = it;
+        *relres_out = sqrt(h.rr) / bnorm;
+        if (*relres_out < rtol) { cleanup(); return sw_check_status(g, s); }
+        if (!(h.rr == h.rr)) { cleanup(); return fail(SW_ENOCONV, "PCG produced NaN"); }
     }
+    cleanup();
     st = sw_check_status(g, s);
     if (st != SW_OK) return st;
     return fail(SW_ENOCONV, "PCG reached maxit");
