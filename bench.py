@@ -294,6 +294,16 @@ def run_secondary(args):
     dt = time.perf_counter() - t0
     out["c3_pcg_ilu0"] = {"iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
                           "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
+    # multigrid-preconditioned CG with the decomposed sweep as smoother
+    g.mg_setup(5, 2, 0.6, 32, 1.5)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, rel, ok = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["c3_pcg_mg"] = {"levels": 5, "nu": 2, "theta": 0.6, "nu_coarse": 32, "coarse_scale": 1.5, "iterations": it,
+                        "relres": rel, "converged": ok, "seconds": round(dt, 3),
+                        "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
     del g, b
     torch.cuda.empty_cache()
     # ---- config 5 sweep
@@ -316,6 +326,15 @@ def run_secondary(args):
         dt = time.perf_counter() - t0
         out["c5_pcg_ilu0"] = {"n": [n3] * 3, "tile": [32, 8, 4], "iterations": it, "relres": rel, "converged": ok,
                               "seconds": round(dt, 3), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
+        g.mg_setup(4, 2, 0.5, 16, 1.5)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        it, rel, ok = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 5000)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["c5_pcg_mg"] = {"levels": 4, "nu": 2, "theta": 0.5, "nu_coarse": 16, "coarse_scale": 1.5,
+                            "iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
+                            "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
     del g
     torch.cuda.empty_cache()
     # ---- config 2 iteration counts (256^2 Poisson, 64 x 64 boxes)
