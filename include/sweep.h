@@ -57,7 +57,10 @@ typedef enum { SW_COEF_POISSON = 0, SW_COEF_FACES = 1 } sw_coef;
 typedef enum { SW_PC_NONE = 0, SW_PC_SSOR = 1, SW_PC_ILU0 = 2, SW_PC_MG = 3 } sw_precond;
 /* SYMMETRIC: P = (D~+L) D~^-1 (D~+L)^T;  PAPER: P = (D~+L) D~^-1 (D~+U), U = A_E(k0) (R-C) */
 typedef enum { SW_PAIR_SYMMETRIC = 0, SW_PAIR_PAPER = 1 } sw_pairing;
-typedef enum { SW_X = 0, SW_B = 1, SW_R = 2, SW_Z = 3, SW_P = 4, SW_Q = 5, SW_INVD = 6, SW_Y = 7 } sw_vector;
+typedef enum {
+    SW_X = 0, SW_B = 1, SW_R = 2, SW_Z = 3, SW_P = 4, SW_Q = 5, SW_INVD = 6, SW_Y = 7,
+    SW_W1 = 8, SW_W2 = 9 /* work vectors of the m-step preconditioner (multi-rank drivers) */
+} sw_vector;
 
 /* Create a grid of n[0..dim-1] GLOBAL interior nodes.  kind = SW_COEF_POISSON (unit
  * faces) or SW_COEF_FACES (coefficients supplied by sw_set_faces / sw_set_coefficients_k
@@ -197,6 +200,12 @@ sw_status sw_dot(sw_grid *g, const double *a_dev, const double *b_dev, double *d
 sw_status sw_axpy2(sw_grid *g, double alpha, double *x_dev, double *r_dev, const double *p_dev, const double *q_dev,
                    double *rr_dd, sw_stream_t s);
 sw_status sw_xpby(sw_grid *g, const double *z_dev, double beta, double *p_dev, sw_stream_t s);
+
+/* out = a x + b y on the local slab's interior nodes, products and sum rounded separately (the
+ * m-step preconditioner's r - theta A z and z + dz, sw_set_precond_steps, for drivers that apply
+ * it over several ranks).  Device pointers to padded arrays; out may alias x or y. */
+sw_status sw_axpby(sw_grid *g, double a, const double *x_dev, double b, const double *y_dev, double *out_dev,
+                   sw_stream_t s);
 
 /* Synchronise `s` and report a deferred device-side error (singular coupled system). */
 sw_status sw_check_status(sw_grid *g, sw_stream_t s);

@@ -20,7 +20,7 @@ SW_OK, SW_EINVAL, SW_ESINGULAR, SW_ENOCONV, SW_ECUDA, SW_ENOMEM, SW_ESTATE = 0, 
 COEF_POISSON, COEF_FACES = 0, 1
 PC_NONE, PC_SSOR, PC_ILU0, PC_MG = 0, 1, 2, 3
 PAIR_SYMMETRIC, PAIR_PAPER = 0, 1
-X, B, R, Z, P, Q, INVD, Y = range(8)
+X, B, R, Z, P, Q, INVD, Y, W1, W2 = range(10)
 
 _lib = None
 
@@ -68,6 +68,7 @@ def load():
     L.sw_dot.argtypes = [P_, P_, P_, P_, P_]
     L.sw_axpy2.argtypes = [P_, D, P_, P_, P_, P_, P_, P_]
     L.sw_xpby.argtypes = [P_, P_, D, P_, P_]
+    L.sw_axpby.argtypes = [P_, D, P_, D, P_, P_, P_]
     L.sw_check_status.argtypes = [P_, P_]
     L.sw_launch_count.argtypes = [P_]
     L.sw_launch_count.restype = I64
@@ -297,6 +298,11 @@ class Grid:
     def xpby(self, z_ptr: int, beta: float, p_ptr: int, stream=None):
         _check(load().sw_xpby(self.h, ctypes.c_void_p(z_ptr), float(beta), ctypes.c_void_p(p_ptr), _stream(stream)),
                "sw_xpby")
+
+    def axpby(self, a: float, x_ptr: int, b: float, y_ptr: int, out_ptr: int, stream=None):
+        """out = a x + b y (interior; products and sum rounded separately)."""
+        _check(load().sw_axpby(self.h, float(a), ctypes.c_void_p(x_ptr), float(b), ctypes.c_void_p(y_ptr),
+                               ctypes.c_void_p(out_ptr), _stream(stream)), "sw_axpby")
 
     def check(self, stream=None):
         _check(load().sw_check_status(self.h, _stream(stream)), "sw_check_status")

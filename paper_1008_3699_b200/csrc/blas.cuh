@@ -338,6 +338,21 @@ __global__ void __launch_bounds__(RED_THREADS) k_scale_r(Rows R, double sc, doub
     }
 }
 
+// out = a x + b y (interior nodes), products and sum rounded separately; out may alias x or y
+__global__ void __launch_bounds__(RED_THREADS) k_axpby_r(Rows R, double a, const double *x, double b, const double *y,
+                                                         double *out) {
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h)
+            if (xb + h * RSEG < R.n0) {
+                const int64_t i = base + xb + h * RSEG;
+                out[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
+            }
+    }
+}
+
 // PCG scalars kept on the device
 struct CgScalars {
     double rz, pq, alpha, beta, rr, bb, rz_new;

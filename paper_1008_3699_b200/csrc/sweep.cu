@@ -250,6 +250,8 @@ static double *vec_ptr(sw_grid *g, sw_vector which) {
         case SW_Q: return g->Q;
         case SW_INVD: return g->invD;
         case SW_Y: return g->Y;
+        case SW_W1: return alloc_arr(g, &g->W1) == SW_OK ? g->W1 : nullptr;
+        case SW_W2: return alloc_arr(g, &g->W2) == SW_OK ? g->W2 : nullptr;
     }
     return nullptr;
 }
@@ -1092,6 +1094,18 @@ extern "C" sw_status sw_xpby(sw_grid *g, const double *z, double beta, double *p
     k_set_scalar<<<1, 1, 0, cs>>>(&g->cg->beta, beta);
     k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 0, z, p);
     g->launches += 2;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+extern "C" sw_status sw_axpby(sw_grid *g, double a, const double *x, double b, const double *y, double *out,
+                              sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!x || !y || !out) return fail(SW_EINVAL, "bad pointers");
+    const Rows RW = make_rows(g->G);
+    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    k_axpby_r<<<nr, RED_THREADS, 0, (cudaStream_t)s>>>(RW, a, x, b, y, out);
+    g->launches++;
     CK(cudaGetLastError());
     return SW_OK;
 }

@@ -138,15 +138,18 @@ class DistComm:
 
 
 def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol: float = 1e-8,
-              maxit: int = 10000):
+              maxit: int = 10000, msteps: int = 1, theta: float = 0.5):
     """Preconditioned CG from x0 = 0 on the right-hand side SW_B of every slab grid of `comm`
-    (same algorithm and stop test as sw_pcg_solve).  Returns (iterations, relres, converged)."""
+    (same algorithm and stop test as sw_pcg_solve).  msteps > 1 applies the m-step form of the
+    preconditioner (sw_set_precond_steps: z_{j+1} = z_j + P^-1 (r - theta A z_j)) through the
+    staged solves, sw_apply_A and sw_axpby.  Returns (iterations, relres, converged)."""
     import torch
 
     from . import binding as B
     grids = comm.grids
     dev = f"cuda:{grids[0].device}"
-    V = {w: [g.view(w) for g in grids] for w in (B.X, B.B, B.R, B.Z, B.P, B.Q, B.Y, B.INVD)}
+    vecs = (B.X, B.B, B.R, B.Z, B.P, B.Q, B.Y, B.INVD) + ((B.W1, B.W2) if msteps > 1 else ())
+    V = {w: [g.view(w) for g in grids] for w in vecs}
     ptr = {w: [t.data_ptr() for t in V[w]] for w in V}
     dd = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in grids]
 
@@ -165,19 +168,30 @@ def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol
         comm.exchange(V[B.INVD], 1)
     z = B.R if precond == B.PC_NONE else B.Z
 
-    def apply_pc():
-        if precond == B.PC_NONE:
-            return
-        comm.exchange(V[B.R], 1)
+    def apply1(src, dst):                    # dst = P^-1 src, stage by stage
+        comm.exchange(V[src], 1)
         for st in range(grids[0].precond_stages(pairing)):
             if st == 1 and pairing == B.PAIR_PAPER:
                 comm.exchange(V[B.Y], 1)
             if st >= 2:
                 if st == 2:
                     comm.exchange(V[B.Y], 1)
-                comm.exchange(V[B.Z], 2)
+                comm.exchange(V[dst], 2)
             for i, g in enumerate(grids):
-                g.precond_apply_stage(precond, st, ptr[B.R][i], ptr[B.Z][i], omega, pairing)
+                g.precond_apply_stage(precond, st, ptr[src][i], ptr[dst][i], omega, pairing)
+
+    def apply_pc():
+        if precond == B.PC_NONE:
+            return
+        apply1(B.R, B.Z)
+        for _ in range(msteps - 1):             # z += P^-1 (r - theta A z)
+            comm.exchange(V[B.Z], 1)
+            for i, g in enumerate(grids):
+                g.apply_A(ptr[B.Z][i], ptr[B.W1][i], dd[i].data_ptr())
+                g.axpby(1.0, ptr[B.R][i], -theta, ptr[B.W1][i], ptr[B.W2][i])
+            apply1(B.W2, B.W1)
+            for i, g in enumerate(grids):
+                g.axpby(1.0, ptr[B.Z][i], 1.0, ptr[B.W1][i], ptr[B.Z][i])
 
     bb = reduce(lambda i, g: g.dot(ptr[B.B][i], ptr[B.B][i], dd[i].data_ptr()))
     bnorm = bb ** 0.5

@@ -145,3 +145,25 @@ def test_pcg_over_slabs_matches_single_grid(n, tile, nranks, var, pc):
     assert abs(it - it1) <= 1, (it, it1)
     x = gather(sl, B.X)
     assert O.relres(pb, x, b) < 2e-8
+
+
+@pytest.mark.parametrize("n,tile,nranks,var,pc", [((256, 256), (64, 64), 2, True, B.PC_SSOR),
+                                                  ((32, 16, 16), (16, 8, 4), 2, True, B.PC_ILU0)])
+def test_msteps_pcg_over_slabs_matches_single_grid(n, tile, nranks, var, pc):
+    """m-step preconditioning over slabs (staged solves + sw_apply_A + sw_axpby) reproduces the
+    single-grid m-step PCG (sw_set_precond_steps)."""
+    faces = None
+    if var:
+        ring = tuple(v + 2 for v in reversed(n))
+        faces = O.faces_from_k(n, gen.lognormal_k(0, ring, 1.0))
+    pb = O.tiled(n, tile, faces=faces)
+    b = gen.uniform_field(0, gen.STREAM_RHS, pb.shape) / float((n[0] + 1) ** 2)
+    one = make_grid(B, n, tile, faces).set_precond_steps(2, 0.5)
+    one.set_vector(B.B, b)
+    it1, rel1, ok1 = one.pcg_solve(pc, 1.0, 0, 1e-8, 5000)
+    sl = make_slabs(n, tile, nranks, faces)
+    scatter(sl, B.B, b)
+    it, rel, ok = parallel.pcg_slabs(parallel.LocalComm(sl), pc, 1.0, 0, 1e-8, 5000, msteps=2, theta=0.5)
+    assert ok and ok1
+    assert abs(it - it1) <= 1, (it, it1)
+    assert O.relres(pb, gather(sl, B.X), b) < 2e-8
