@@ -31,7 +31,11 @@ struct Tri3tArgs {
 };
 
 // box parity bit of global coordinate c along axis a (global coordinates fit in 32 bits)
-__device__ __forceinline__ int box_bit(const Tri3tArgs &A, int a, int64_t c) { return ((int)c / A.G.T[a]) & 1; }
+// (a float reciprocal instead of an integer division: the quotient (c + 1/2) / T is exact to the
+// integer part for c < 2^22)
+__device__ __forceinline__ int box_bit(const Tri3tArgs &A, int a, int64_t c) {
+    return __float2int_rz(((float)c + 0.5f) * __frcp_rn((float)A.G.T[a])) & 1;
+}
 
 template <int NA>
 __device__ __forceinline__ void tri3t_solve(const Tri3tArgs &A, const int64_t gl[3], int mask) {
@@ -289,11 +293,23 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
             if (ok) tri3t_row<NA>(A, gl, mask, p, rhs, Mr, ix);
             double Mall[K][K], rall[K], u[K];
             const int src0 = threadIdx.x & ~(K - 1);
+            // gather the rows: the right-hand side and the NA off-diagonal entries (to the partner
+            // across each set axis, p ^ (1 << t)); the rest of every row is the identity's
+            double off[NA];
+#pragma unroll
+            for (int t = 0; t < NA; ++t) {
+                off[t] = Mr[0];
+#pragma unroll
+                for (int c = 1; c < K; ++c)
+                    if (c == (p ^ (1 << t))) off[t] = Mr[c];
+            }
 #pragma unroll
             for (int q = 0; q < K; ++q) {
                 rall[q] = __shfl_sync(0xffffffffu, rhs, src0 + q);
 #pragma unroll
-                for (int c = 0; c < K; ++c) Mall[q][c] = __shfl_sync(0xffffffffu, Mr[c], src0 + q);
+                for (int c = 0; c < K; ++c) Mall[q][c] = (c == q) ? 1.0 : 0.0;
+#pragma unroll
+                for (int t = 0; t < NA; ++t) Mall[q][q ^ (1 << t)] = __shfl_sync(0xffffffffu, off[t], src0 + q);
             }
             if (ok) {
                 tri3t_ge<K>(Mall, rall, u, A.flag, p == 0);
