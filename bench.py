@@ -361,6 +361,14 @@ def run_secondary(args):
         it, rel, ok = g.pcg_solve(binding.PC_SSOR, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
         res[f"pcg_ssor_{m}step"] = it
     g.set_precond_steps(1, 1.0)
+    g.mg_setup(4, 1, 0.5, 16, 1.2)
+    res["pcg_mg"], _, _ = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
+    # the same V-cycle with one box per level (the sequential sweep as smoother): the paper's
+    # "no convergence decay" claim for smoothing
+    g1 = binding.Grid(2, (n2, n2)).decompose((n2, n2)).mg_setup(4, 1, 0.5, 16, 1.2)
+    g1.set_vector(binding.B, b)
+    res["pcg_mg_one_box_smoother"], _, _ = g1.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
+    del g1
     out["c2_iterations"] = res
     # ---- the relaxation-factor search of PAPER:1996-1998 on config 2
     from paper_1008_3699_b200 import omega as OM

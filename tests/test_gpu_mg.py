@@ -131,3 +131,26 @@ def test_mg_setup_validation():
         g2.mg_setup(3, 1, 1.5)
     with pytest.raises(B.SweepError):
         make_grid(B, (192, 192), (64, 64)).pcg_solve(B.PC_MG)
+
+
+@pytest.mark.parametrize("law", ["poisson", "lognormal"])
+def test_decomposed_smoother_loses_no_convergence(law):
+    """The paper's claim that parallelising the sweep costs no convergence rate (PAPER:378-380
+    "good smoothing properties", 2585-2588) measured where it matters most: the
+    MG-PCG iteration count with the decomposed sweep as smoother on 64^2 / 32^2 / 16^2 boxes stays
+    within 25 % of the same V-cycle with one box per level (the sequential sweep)."""
+    n = (256, 256)
+    b = gen.uniform_field(0, gen.STREAM_RHS, tuple(reversed(n))) / float((n[0] + 1) ** 2)
+    faces = None
+    if law == "lognormal":
+        ring = tuple(v + 2 for v in reversed(n))
+        faces = O.faces_from_k(n, gen.lognormal_k(0, ring, 1.0))
+    its = {}
+    for tile in [(256, 256), (64, 64), (32, 32), (16, 16)]:
+        g = make_grid(B, n, tile, faces).mg_setup(4, 1, 0.5, 16, 1.2)
+        g.set_vector(B.B, b)
+        it, rel, ok = g.pcg_solve(B.PC_MG, 1.0, B.PAIR_SYMMETRIC, 1e-8, 5000)
+        assert ok
+        its[tile[0]] = it
+    for t in (64, 32, 16):
+        assert its[t] <= 1.25 * its[256], its
