@@ -1133,14 +1133,3 @@ extern "C" int sw_debug_phase_times(unsigned long long out[16]) {
 #endif
 }
 
-// Tuning aid (not part of sweep.h): window of one 3D box after the set phase (SW_DEBUG3 builds).
-extern "C" int sw_debug3(int block, double *out, int n) {
-#ifdef SW_DEBUG3
-    if (block >= -1) cudaMemcpyToSymbol(sw_dbg3_block, &block, sizeof(int));
-    if (out) cudaMemcpyFromSymbol(out, sw_dbg3, sizeof(double) * (size_t)n);
-    return 1;
-#else
-    (void)block; (void)out; (void)n;
-    return 0;
-#endif
-}

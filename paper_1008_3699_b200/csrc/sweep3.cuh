@@ -283,10 +283,6 @@ __device__ __forceinline__ void edge_chain(double *X, int WS, int lane, int T, i
         }
 }
 
-#ifdef SW_DEBUG3
-__device__ double sw_dbg3[4 * 8192];
-__device__ int sw_dbg3_block = -1;
-#endif
 
 template <bool FACES, int SHAPE>
 __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
@@ -529,13 +525,6 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         else if (warp != 1) asm volatile("bar.sync 1, %0;" ::"r"(k3::NT - 32) : "memory");
     }
 
-#ifdef SW_DEBUG3
-    if ((int)blockIdx.x == sw_dbg3_block)
-        for (int i = tid; i < WS; i += k3::NT) {
-            sw_dbg3[i] = X[i];
-            sw_dbg3[8192 + i] = C0[i];
-        }
-#endif
     SW_TMARK(t_sets);
     SW_TADD(2, t_prologue, t_sets);
     // ---------------------------------------------------------------- 3. level loop (warp 0)
