@@ -355,6 +355,16 @@ def run_secondary(args):
                             "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
     del g
     torch.cuda.empty_cache()
+    # ---- config 1: 1D Poisson n = 1024, 4 boxes, SOR at omega_opt until relres < 1e-8
+    n1 = 1024
+    g1d = binding.Grid(1, (n1,)).decompose((256,))
+    g1d.set_vector(binding.B, gen.uniform_field(args.seed, gen.STREAM_RHS, (n1,)) / float((n1 + 1) ** 2))
+    from paper_1008_3699_b200 import omega as OM
+    t0 = time.perf_counter()
+    c1 = OM.sweeps_to_tol(g1d, [OM.omega_opt_poisson(n1)], 1e-8, 100000, 1)
+    out["c1_sweeps_to_1e-8"] = {"n": n1, "tile": 256, "omega": round(OM.omega_opt_poisson(n1), 6), "sweeps": c1,
+                                "seconds": round(time.perf_counter() - t0, 3)}
+    del g1d
     # ---- config 2 iteration counts (256^2 Poisson, 64 x 64 boxes)
     n2 = 256
     g = binding.Grid(2, (n2, n2)).decompose((64, 64))

@@ -50,3 +50,17 @@ def test_search_on_the_library_finds_the_oracle_optimum():
     w_or, c_or, t_or = OM.grid_search(lambda v: oracle_count(pb, b, v), 1.90, 1.98, 0.02)
     assert t_lib == t_or
     assert (w_lib, c_lib) == (w_or, c_or)
+
+
+def test_config1_sweep_count_equals_oracle():
+    """Config 1 (1D Poisson, n = 1024, 4 boxes of 256, omega_opt): the number of decomposed SOR
+    sweeps to a relative residual of 1e-8 (checked after every sweep) equals the oracle's."""
+    n, tile = (1024,), (256,)
+    w = [OM.omega_opt_poisson(n[0])]
+    pb = O.tiled(n, tile)
+    b = gen.uniform_field(0, gen.STREAM_RHS, pb.shape) / float((n[0] + 1) ** 2)
+    g = make_grid(B, n, tile)
+    g.set_vector(B.B, b)
+    got = OM.sweeps_to_tol(g, w, 1e-8, 100000, 1)
+    want = oracle_count(pb, b, w, 1e-8, 100000, 1)
+    assert got == want and got is not None
