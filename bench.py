@@ -50,7 +50,8 @@ class ClockSampler:
     def __init__(self, dev):
         self.dev = dev
         self.proc = None
-        self.lines = []
+        self.lines = []            # (monotonic time, line)
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -65,7 +66,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def start(self):
+        """Mark the start of the timed region (the sampler itself runs from before the warm-up,
+        so that samples already flow when the region begins)."""
+        self.t0 = time.monotonic()
+
+    def stop(self):
+        self.t1 = time.monotonic()
+        time.sleep(0.05)           # let the sample that covers the end arrive
 
     def __exit__(self, *a):
         if self.proc:
@@ -78,7 +88,15 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.t0 is not None and self.t1 is not None:
+            inside = [ln for t, ln in lines if self.t0 <= t <= self.t1 + 0.03]
+            if not inside:             # a region shorter than the sampling period: the next sample
+                inside = [ln for t, ln in lines if t >= self.t0][:1]
+            lines = inside
+        else:
+            lines = [ln for _, ln in lines]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -138,6 +156,8 @@ def run_ours(args):
         return g.sor_sweep([omega], 1, phase)
 
     phase = 0
+    clk = ClockSampler(local).__enter__()      # sampling from before the warm-up on
+    time.sleep(0.3)                            # nvidia-smi's first samples
     for _ in range(args.warmup):
         phase = step(phase)
     torch.cuda.synchronize()
@@ -147,12 +167,14 @@ def run_ours(args):
     l0 = g.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            phase = step(phase)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    clk.start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        phase = step(phase)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk.stop()
+    clk.__exit__(None, None, None)
     ms = ev0.elapsed_time(ev1)
     launches = g.launch_count() - l0
     if world > 1:

@@ -538,11 +538,19 @@ extern "C" sw_status sw_residual_norm(sw_grid *g, double *rel_out, sw_stream_t s
     sw_status st;
     if ((st = finish(g, nb, 2, 0, &g->cg->rr, cs)) != SW_OK) return st;
     if ((st = finish(g, nb, 2, 1, &g->cg->bb, cs)) != SW_OK) return st;
-    CgScalars h;
+    // one synchronisation for the scalars and the status flag
+    if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars) + sizeof(int)));
+    CgScalars &h = *g->hcg;
+    int *hf = reinterpret_cast<int *>(g->hcg + 1);
     CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
+    CK(cudaMemcpyAsync(hf, g->flag, sizeof(int), cudaMemcpyDeviceToHost, cs));
     CK(cudaStreamSynchronize(cs));
     *rel_out = h.bb > 0 ? sqrt(h.rr) / sqrt(h.bb) : sqrt(h.rr);
-    return sw_check_status(g, s);
+    if (*hf) {
+        CK(cudaMemset(g->flag, 0, sizeof(int)));
+        return fail(SW_ESINGULAR, "singular coupled system or non-positive ILU pivot");
+    }
+    return SW_OK;
 }
 
 extern "C" sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s) {
@@ -917,7 +925,7 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
                 : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
         g->launches++;
     };
-    if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars)));   // pinned: the readback is a graph node
+    if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars) + sizeof(int)));   // pinned: the readback is a graph node
     CgScalars &h = *g->hcg;
     // b.b, z0 = P^-1 r0, r.z, p = z
     k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->B, g->B, g->partial);
