@@ -236,6 +236,62 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv_dot_r(Rows R, double beta,
     if (threadIdx.x == 0) partial[blockIdx.x] = sm;
 }
 
+// The PCG direction update fused into the next SpMV: p_new = z + beta p_old at
+// the node and its stencil neighbours (each value exactly as k_pupdate_r computes it), q = A p_new,
+// p_new stored (a second buffer: other threads still read p_old), partial[blk] = sum p_new.q.
+template <int DIM, bool FACES>
+__global__ void __launch_bounds__(RED_THREADS) k_pspmv_dot_r(Rows R, double beta_a, const double *beta_dev,
+                                                             const double *__restrict__ F0,
+                                                             const double *__restrict__ F1,
+                                                             const double *__restrict__ F2,
+                                                             const double *__restrict__ z,
+                                                             const double *__restrict__ pold,
+                                                             double *__restrict__ pnew, double *__restrict__ q,
+                                                             DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    const double be = *beta_dev;
+    auto P = [&](int64_t j) { return fma(be, pold[j], z[j]); };
+    DD acc = {0.0, 0.0};
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t b = row_base(R, row);
+        for (int h = 0; h < 2; ++h) {
+            const int64_t x = xb + h * RSEG;
+            if (x < R.n0) {
+                const int64_t i = b + x;
+                double c0 = 1.0, c1 = 1.0, c2 = 1.0, c3 = 1.0, c4 = 1.0, c5 = 1.0;
+                if (FACES) {
+                    c0 = F0[i]; c1 = F0[i + 1];
+                    if (DIM > 1) { c2 = F1[i]; c3 = F1[i + R.P0]; }
+                    if (DIM > 2) { c4 = F2[i]; c5 = F2[i + R.P01]; }
+                }
+                double ap = c0 + c1;
+                if (DIM > 1) ap = ap + (c2 + c3);
+                if (DIM > 2) ap = ap + (c4 + c5);
+                ap = ap + beta_a;
+                const double pi = P(i);
+                double v = ap * pi;
+                v = fma(-c0, P(i - 1), v);
+                v = fma(-c1, P(i + 1), v);
+                if (DIM > 1) {
+                    v = fma(-c2, P(i - R.P0), v);
+                    v = fma(-c3, P(i + R.P0), v);
+                }
+                if (DIM > 2) {
+                    v = fma(-c4, P(i - R.P01), v);
+                    v = fma(-c5, P(i + R.P01), v);
+                }
+                pnew[i] = pi;
+                q[i] = v;
+                dd_add_prod(acc, pi, v);
+            }
+        }
+    }
+    DD sm = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm;
+}
+
 // partial[blk] = sum a.b
 __global__ void __launch_bounds__(RED_THREADS) k_dot_r(Rows R, const double *__restrict__ a,
                                                        const double *__restrict__ b, DD *partial) {

@@ -56,6 +56,7 @@ struct sw_grid {
     double *F[3] = {nullptr, nullptr, nullptr};
     double *invD = nullptr, *R = nullptr, *Z = nullptr, *Pv = nullptr, *Q = nullptr, *Y = nullptr;
     double *W1 = nullptr, *W2 = nullptr;   // m-step preconditioner work (allocated when pc_steps > 1)
+    double *Pv2 = nullptr;                 // second PCG direction buffer (fused direction update + SpMV)
     int pc_steps = 1;                      // sw_set_precond_steps
     double pc_theta = 1.0;
     // geometric multigrid (sw_mg_setup): coarse levels 1.., and per level the V-cycle's right-hand
@@ -132,7 +133,7 @@ static void free_all(sw_grid *g) {
     g->mg.clear();
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
                        &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2,
-                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2};
+                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->hcg) cudaFreeHost(g->hcg);
@@ -915,14 +916,27 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     const Rows RW = make_rows(G);
     const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
     const bool fc = !G.poisson;
-    auto spmv = [&]() {
+    if ((st = alloc_arr(g, &g->Pv2)) != SW_OK) return st;
+    double *pcur = g->Pv, *pprev = g->Pv2;     // current direction, and the buffer of the other one
+    // q = A p (first iteration) or, fused, p' = z + beta p, q = A p'
+    auto spmv = [&](bool fused) {
         const double *F0 = g->F[0], *F1 = g->F[1], *F2 = g->F[2];
-        if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
-                            : k_spmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
-        else if (g->dim == 2) fc ? k_spmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
-                                 : k_spmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
-        else fc ? k_spmv_dot_r<3, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial)
-                : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, g->Pv, g->Q, g->partial);
+        if (!fused) {
+            if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial)
+                                : k_spmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial);
+            else if (g->dim == 2) fc ? k_spmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial)
+                                     : k_spmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial);
+            else fc ? k_spmv_dot_r<3, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial)
+                    : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial);
+        } else {
+            const double *bd = &g->cg->beta;
+            if (g->dim == 1) fc ? k_pspmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                                : k_pspmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            else if (g->dim == 2) fc ? k_pspmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                                     : k_pspmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            else fc ? k_pspmv_dot_r<3, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                    : k_pspmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+        }
         g->launches++;
     };
     if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars) + sizeof(int)));   // pinned: the readback is a graph node
@@ -935,7 +949,7 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->R, z, g->partial);
     g->launches++;
     if ((st = finish(g, nr, 1, 0, &g->cg->rz, cs)) != SW_OK) return st;
-    k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 1, z, g->Pv);
+    k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 1, z, pcur);
     g->launches++;
     CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
     CK(cudaStreamSynchronize(cs));
@@ -943,20 +957,21 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     *iters_out = 0;
     *relres_out = 1.0;
     if (bnorm == 0.0) { *relres_out = 0.0; return SW_OK; }
-    // q = A p, alpha, x += alpha p, r -= alpha q (r.r), and the readback of the scalars
-    auto head = [&]() -> sw_status {
-        spmv();
+    // q = A p (fused: after p = z + beta p), alpha, x += alpha p, r -= alpha q (r.r), and the
+    // readback of the scalars
+    auto head = [&](bool fused) -> sw_status {
+        spmv(fused);
         sw_status t = finish(g, nr, 1, 0, &g->cg->pq, ws);
         if (t != SW_OK) return t;
         k_cg_alpha<<<1, 1, 0, ws>>>(g->cg);
         g->launches++;
-        k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, g->Pv, g->Q, g->partial);
+        k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, pcur, g->Q, g->partial);
         g->launches++;
         if ((t = finish(g, nr, 1, 0, &g->cg->rr, ws)) != SW_OK) return t;
         CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, ws));
         return SW_OK;
     };
-    // z = P^-1 r, r.z, beta, p = z + beta p
+    // z = P^-1 r, r.z, beta (the direction update p = z + beta p is fused into the next SpMV)
     auto tail = [&]() -> sw_status {
         sw_status t = apply_pc();
         if (t != SW_OK) return t;
@@ -965,61 +980,65 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         if ((t = finish(g, nr, 1, 0, &g->cg->rz_new, ws)) != SW_OK) return t;
         k_cg_beta<<<1, 1, 0, ws>>>(g->cg);
         g->launches++;
-        k_pupdate_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->beta, 0, z, g->Pv);
-        g->launches++;
         CK(cudaGetLastError());
         return SW_OK;
     };
-    // Iterations 2.. replay one CUDA graph of tail + head (tens of launches, hundreds with the
-    // multigrid preconditioner): one launch and one synchronisation per iteration.
+    auto swap_p = [&]() { std::swap(pcur, pprev); };   // pprev = the old direction, pcur = where the new one goes
+    // Iterations 2.. replay a CUDA graph of tail + fused head (tens of launches, hundreds with the
+    // multigrid preconditioner): one launch and one synchronisation per iteration.  The direction
+    // buffers alternate, so there is one graph per parity.
     static const bool no_graph = getenv("SW_NO_GRAPH") != nullptr;
-    cudaGraphExec_t exec = nullptr;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
     int64_t graph_launches = 0;
     bool graph_ok = !no_graph;
     auto cleanup = [&]() {
-        if (exec) cudaGraphExecDestroy(exec);
-        exec = nullptr;
+        for (auto &e : exec)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
     };
     for (int it = 1; it <= maxit; ++it) {
+        const int par = it & 1;
         if (it == 1) {
             ws = cs;
-            if ((st = head()) != SW_OK) return st;
-        } else if (graph_ok && !exec) {
-            // capture on a private stream (the caller's may be the legacy default stream)
-            if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
-            CK(cudaStreamSynchronize(cs));
-            const int64_t l0 = g->launches;
-            cudaGraph_t graph = nullptr;
-            ws = g->cap_stream;
-            bool ok = cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-            sw_status t1 = ok ? tail() : SW_OK;
-            sw_status t2 = (ok && t1 == SW_OK) ? head() : SW_OK;
-            const cudaError_t ce = ok ? cudaStreamEndCapture(ws, &graph) : cudaErrorUnknown;
-            ws = cs;
-            graph_launches = g->launches - l0;
-            g->launches = l0;
-            if (ok && t1 == SW_OK && t2 == SW_OK && ce == cudaSuccess && graph &&
-                cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
-                cudaGraphDestroy(graph);
-            } else {                                   // no graph: run the iteration as plain launches
-                if (graph) cudaGraphDestroy(graph);
-                cudaGetLastError();
-                graph_ok = false;
-                exec = nullptr;
-                if ((st = tail()) != SW_OK) return st;
-                if ((st = head()) != SW_OK) return st;
-            }
-            if (exec) {
-                if (cudaGraphLaunch(exec, cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "cudaGraphLaunch"); }
-                g->launches += graph_launches;
-            }
-        } else if (exec) {
-            if (cudaGraphLaunch(exec, cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "cudaGraphLaunch"); }
-            g->launches += graph_launches;
+            if ((st = head(false)) != SW_OK) return st;
         } else {
-            ws = cs;
-            if ((st = tail()) != SW_OK) return st;
-            if ((st = head()) != SW_OK) return st;
+            swap_p();
+            if (graph_ok && !exec[par]) {
+                // capture on a private stream (the caller's may be the legacy default stream)
+                if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+                CK(cudaStreamSynchronize(cs));
+                const int64_t l0 = g->launches;
+                cudaGraph_t graph = nullptr;
+                ws = g->cap_stream;
+                bool ok = cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                sw_status t1 = ok ? tail() : SW_OK;
+                sw_status t2 = (ok && t1 == SW_OK) ? head(true) : SW_OK;
+                const cudaError_t ce = ok ? cudaStreamEndCapture(ws, &graph) : cudaErrorUnknown;
+                ws = cs;
+                graph_launches = g->launches - l0;
+                g->launches = l0;
+                if (ok && t1 == SW_OK && t2 == SW_OK && ce == cudaSuccess && graph &&
+                    cudaGraphInstantiate(&exec[par], graph, 0) == cudaSuccess) {
+                    cudaGraphDestroy(graph);
+                } else {                               // no graphs: plain launches from here on
+                    if (graph) cudaGraphDestroy(graph);
+                    cudaGetLastError();
+                    graph_ok = false;
+                    cleanup();
+                    if ((st = tail()) != SW_OK) return st;
+                    if ((st = head(true)) != SW_OK) return st;
+                }
+            }
+            if (graph_ok && exec[par]) {
+                if (cudaGraphLaunch(exec[par], cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "cudaGraphLaunch"); }
+                g->launches += graph_launches;
+            } else if (!graph_ok) {
+                ws = cs;
+                if ((st = tail()) != SW_OK) return st;
+                if ((st = head(true)) != SW_OK) return st;
+            }
         }
         if (cudaStreamSynchronize(cs) != cudaSuccess) { cleanup(); return fail(SW_ECUDA, "PCG iteration failed"); }
         *iters_out = it;
