@@ -9,6 +9,7 @@
 #include <deque>
 #include <string>
 #include <vector>
+#include <cmath>
 
 #include "../../include/sweep.h"
 #include "blas.cuh"
@@ -59,6 +60,7 @@ struct sw_grid {
     double *Pv2 = nullptr;                 // second PCG direction buffer (fused direction update + SpMV)
     int pc_steps = 1;                      // sw_set_precond_steps
     double pc_theta = 1.0;
+    double zscale = 1.0;                   // power-of-two scale folded into the solves' coef (multigrid)
     // geometric multigrid (sw_mg_setup): coarse levels 1.., and per level the V-cycle's right-hand
     // side / correction (MGR, MGX, coarse levels) and two temporaries (MT1, MT2)
     std::vector<sw_grid *> mg;
@@ -584,7 +586,9 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     if (!r || !z || z == g->Y || r == z) return fail(SW_EINVAL, "bad r/z pointers");
     if (stage < 0 || stage >= tri_nstages(g, pairing)) return fail(SW_EINVAL, "bad stage");
     const int base = base_bits(g->dim, g->factor_phase), rev = base ^ ((1 << g->dim) - 1);
-    const double coef = ilu ? 1.0 : 2.0 - omega;
+    // (zscale: a power of two folded into the backward solves, so their result is exactly zscale
+    // times the unscaled one: every step of the recurrences is linear in r0 = coef y)
+    const double coef = (ilu ? 1.0 : 2.0 - omega) * g->zscale;
     const double *invd = ilu ? g->invD : nullptr;
     if (g->dim == 2 && g->fast2d && g->maps.ok) {
         // 64 x 64 engine (sweep2v MODE_TRI, tri2t)
@@ -707,7 +711,8 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
     for (int j = 1; j < g->pc_steps; ++j) {
         if ((st = spmv_launch(g, RW, nr, z, g->W1, s, 0)) != SW_OK) return st;   // W1 = A z
-        k_sub_r<<<nr, RED_THREADS, 0, s>>>(RW, r, g->pc_theta, g->W1, g->W2);     // W2 = r - theta A z
+        // W2 = r - theta A z (with zscale = theta folded in, z is already theta times the iterate)
+        k_sub_r<<<nr, RED_THREADS, 0, s>>>(RW, r, g->zscale != 1.0 ? 1.0 : g->pc_theta, g->W1, g->W2);
         g->launches++;
         if ((st = tri_apply1(g, ilu, omega, g->W2, g->W1, pairing, s)) != SW_OK) return st;   // W1 = P^-1 W2
         k_addto_r<<<nr, RED_THREADS, 0, s>>>(RW, z, g->W1);                       // z += W1
@@ -783,10 +788,14 @@ static sw_status mg_smooth(sw_grid *l, const double *r, double *x, int m, double
     l->pc_steps = m;
     l->pc_theta = theta;
     l->factor_phase = 0;
+    int e2;
+    const bool pow2 = std::frexp(theta, &e2) == 0.5;   // theta = 2^k: scale folded into the solves, exact
+    if (pow2) l->zscale = theta;
     sw_status st = tri_apply(l, false, 1.0, r, x, SW_PAIR_SYMMETRIC, s);
+    l->zscale = 1.0;
     l->pc_steps = keep_m;
     l->pc_theta = keep_t;
-    if (st != SW_OK || theta == 1.0) return st;
+    if (st != SW_OK || pow2) return st;
     const Rows RW = make_rows(l->G);
     const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
     k_scale_r<<<nr, RED_THREADS, 0, s>>>(RW, theta, x);
