@@ -292,6 +292,27 @@ __global__ void __launch_bounds__(RED_THREADS) k_pspmv_dot_r(Rows R, double beta
     if (threadIdx.x == 0) partial[blockIdx.x] = sm;
 }
 
+// out = r - A x (interior nodes): the residual of a multigrid level in one pass (the same values as
+// k_spmv_dot_r followed by k_sub_r with theta = 1)
+template <int DIM, bool FACES>
+__global__ void __launch_bounds__(RED_THREADS) k_resid_r(Rows R, double beta, const double *__restrict__ F0,
+                                                         const double *__restrict__ F1, const double *__restrict__ F2,
+                                                         const double *__restrict__ x, const double *__restrict__ r,
+                                                         double *__restrict__ out) {
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t b = row_base(R, row);
+        for (int h = 0; h < 2; ++h) {
+            const int64_t xx = xb + h * RSEG;
+            if (xx < R.n0) {
+                const int64_t i = b + xx;
+                out[i] = __dsub_rn(r[i], apply_A_fast<DIM, FACES>(F0, F1, F2, x, i, R.P0, R.P01, beta));
+            }
+        }
+    }
+}
+
 // partial[blk] = sum a.b
 __global__ void __launch_bounds__(RED_THREADS) k_dot_r(Rows R, const double *__restrict__ a,
                                                        const double *__restrict__ b, DD *partial) {

@@ -5,6 +5,7 @@
 // (the lower index of the first remaining axis first, pairwise), mirrored by the oracle-side test.
 #pragma once
 #include "common.cuh"
+#include "blas.cuh"
 
 namespace sw {
 
@@ -54,6 +55,25 @@ __global__ void k_restrict(Geo Gf, Geo Gc, const double *__restrict__ rf, double
         double v = rf[i] + rf[i + 1];
         if (DIM > 1) v = v + (rf[i + S1] + rf[i + S1 + 1]);
         if (DIM > 2) v = v + ((rf[i + S2] + rf[i + S2 + 1]) + (rf[i + S2 + S1] + rf[i + S2 + S1 + 1]));
+        rc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] = v;
+    }
+}
+
+// r_c[I] = sum over the 2^d fine nodes of I of (r - A x), in k_restrict's order: the residual of
+// the pre-smoothed iterate restricted in one pass (each fine residual as k_resid_r computes it)
+template <int DIM, bool FACES>
+__global__ void k_resid_restrict(Geo Gf, Geo Gc, double beta, const double *__restrict__ F0,
+                                 const double *__restrict__ F1, const double *__restrict__ F2,
+                                 const double *__restrict__ x, const double *__restrict__ r, double *__restrict__ rc) {
+    const int64_t total = Gc.n[0] * Gc.n[1] * Gc.n[2];
+    const int64_t S1 = Gf.P0, S2 = Gf.P01;
+    auto res = [&](int64_t i) { return __dsub_rn(r[i], apply_A_fast<DIM, FACES>(F0, F1, F2, x, i, S1, S2, beta)); };
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t I[3] = {e % Gc.n[0], (e / Gc.n[0]) % Gc.n[1], e / (Gc.n[0] * Gc.n[1])};
+        const int64_t i = gidx(Gf, 2 * I[0] + Gf.off[0], 2 * I[1] + Gf.off[1], 2 * I[2] + Gf.off[2]);
+        double v = res(i) + res(i + 1);
+        if (DIM > 1) v = v + (res(i + S1) + res(i + S1 + 1));
+        if (DIM > 2) v = v + ((res(i + S2) + res(i + S2 + 1)) + (res(i + S2 + S1) + res(i + S2 + S1 + 1)));
         rc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] = v;
     }
 }

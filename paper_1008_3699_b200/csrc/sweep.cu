@@ -807,9 +807,33 @@ static sw_status mg_smooth(sw_grid *l, const double *r, double *x, int m, double
 static sw_status mg_residual(sw_grid *l, const double *r, const double *x, double *out, cudaStream_t s) {
     const Rows RW = make_rows(l->G);
     const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
-    sw_status st = spmv_launch(l, RW, nr, x, l->MT1, s, 0);   // MT1 = A x
-    if (st != SW_OK) return st;
-    k_sub_r<<<nr, RED_THREADS, 0, s>>>(RW, r, 1.0, l->MT1, out);
+    const double *F0 = l->F[0], *F1 = l->F[1], *F2 = l->F[2];
+    const bool fc = !l->G.poisson;
+    const double bt = l->G.beta;
+    if (l->dim == 1) fc ? k_resid_r<1, true><<<nr, RED_THREADS, 0, s>>>(RW, bt, F0, F1, F2, x, r, out)
+                        : k_resid_r<1, false><<<nr, RED_THREADS, 0, s>>>(RW, bt, F0, F1, F2, x, r, out);
+    else if (l->dim == 2) fc ? k_resid_r<2, true><<<nr, RED_THREADS, 0, s>>>(RW, bt, F0, F1, F2, x, r, out)
+                             : k_resid_r<2, false><<<nr, RED_THREADS, 0, s>>>(RW, bt, F0, F1, F2, x, r, out);
+    else fc ? k_resid_r<3, true><<<nr, RED_THREADS, 0, s>>>(RW, bt, F0, F1, F2, x, r, out)
+            : k_resid_r<3, false><<<nr, RED_THREADS, 0, s>>>(RW, bt, F0, F1, F2, x, r, out);
+    l->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+// r_c = R (r - A x), one pass
+static sw_status mg_resid_restrict(sw_grid *l, sw_grid *c, const double *r, const double *x, cudaStream_t s) {
+    const int64_t nct = c->G.n[0] * c->G.n[1] * c->G.n[2];
+    const int nb = (int)std::min<int64_t>((nct + 255) / 256, 8192);
+    const double *F0 = l->F[0], *F1 = l->F[1], *F2 = l->F[2];
+    const bool fc = !l->G.poisson;
+    const double bt = l->G.beta;
+    if (l->dim == 1) fc ? k_resid_restrict<1, true><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR)
+                        : k_resid_restrict<1, false><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR);
+    else if (l->dim == 2) fc ? k_resid_restrict<2, true><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR)
+                             : k_resid_restrict<2, false><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR);
+    else fc ? k_resid_restrict<3, true><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR)
+            : k_resid_restrict<3, false><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR);
     l->launches++;
     CK(cudaGetLastError());
     return SW_OK;
@@ -822,15 +846,8 @@ static sw_status mg_vcycle(sw_grid *g, int lev, const double *r, double *x, cuda
     sw_status st;
     if (lev == nlev - 1) return mg_smooth(l, r, x, g->mg_nu_coarse, g->mg_theta, s);
     if ((st = mg_smooth(l, r, x, g->mg_nu, g->mg_theta, s)) != SW_OK) return st;          // pre-smoothing
-    if ((st = mg_residual(l, r, x, l->MT2, s)) != SW_OK) return st;                      // MT2 = r - A x
     sw_grid *c = g->mg[lev];
-    const int64_t nct = c->G.n[0] * c->G.n[1] * c->G.n[2];
-    const int nbc = (int)std::min<int64_t>((nct + 255) / 256, 8192);
-    if (g->dim == 1) k_restrict<1><<<nbc, 256, 0, s>>>(l->G, c->G, l->MT2, c->MGR);
-    else if (g->dim == 2) k_restrict<2><<<nbc, 256, 0, s>>>(l->G, c->G, l->MT2, c->MGR);
-    else k_restrict<3><<<nbc, 256, 0, s>>>(l->G, c->G, l->MT2, c->MGR);
-    l->launches++;
-    CK(cudaGetLastError());
+    if ((st = mg_resid_restrict(l, c, r, x, s)) != SW_OK) return st;                    // r_c = R (r - A x)
     if ((st = mg_vcycle(g, lev + 1, c->MGR, c->MGX, s)) != SW_OK) return st;             // coarse correction
     const int64_t nft = l->G.n[0] * l->G.n[1] * l->G.n[2];
     const int nbf = (int)std::min<int64_t>((nft + 255) / 256, 8192);
