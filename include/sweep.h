@@ -153,7 +153,7 @@ sw_status sw_set_precond_steps(sw_grid *g, int m, double theta);
 /* Geometric multigrid preconditioner (the decomposed sweep as the smoother
  * inside multigrid).  Builds `levels` - 1 coarse grids by halving the
  * node count per axis (every level must have even counts): piecewise-constant aggregation of
- * 2^d fine nodes, restriction R = P^T and the Galerkin operator R A P, which is again a
+ * the fine nodes of a coarse node, restriction R = P^T and the Galerkin operator R A P, which is again a
  * face-coefficient operator (coarse face = sum of the 2^(d-1) fine faces it covers, beta_c =
  * 2^d beta; DESIGN R-19).  Coarse boxes: the fine box shape, shrunk to divide the level.
  * The symmetric V-cycle (sw_mg_apply, and SW_PC_MG in sw_pcg_solve): nu Richardson steps of length
@@ -162,8 +162,11 @@ sw_status sw_set_precond_steps(sw_grid *g, int m, double theta);
  * over-correction of piecewise-constant interpolation; any value > 0 keeps the V-cycle symmetric
  * positive definite); on the coarsest level nu_coarse steps.  Single rank.  SW_EINVAL for levels
  * outside [2, 16], nu outside [1, 64], nu_coarse outside [1, 1024], theta outside (0, 1],
- * coarse_scale outside (0, 4] or an odd count on a level to be coarsened. */
-sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale);
+ * coarse_scale outside (0, 4] or an odd count on a level to be coarsened.  `axes` (bit a = axis a)
+ * selects the coarsened axes of every level, 0 = all: for anisotropic problems (config 5's
+ * 1 : 0.1 : 0.01) semi-coarsening of the strongly coupled axes only; a coarse node then aggregates
+ * 2^k fine nodes, k the number of coarsened axes, and beta_c = 2^k beta. */
+sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale, int axes);
 
 /* z = B r, one V-cycle from zero (padded device arrays as for sw_ilu_apply; borrowed). */
 sw_status sw_mg_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_stream_t s);

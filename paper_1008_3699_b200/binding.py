@@ -58,7 +58,7 @@ def load():
     L.sw_ssor_apply.argtypes = [P_, D, P_, P_, I, P_]
     L.sw_pcg_solve.argtypes = [P_, I, D, I, D, I, ctypes.POINTER(I), ctypes.POINTER(D), P_]
     L.sw_set_precond_steps.argtypes = [P_, I, D]
-    L.sw_mg_setup.argtypes = [P_, I, I, D, I, D]
+    L.sw_mg_setup.argtypes = [P_, I, I, D, I, D, I]
     L.sw_mg_apply.argtypes = [P_, P_, P_, P_]
     L.sw_precond_stages.argtypes = [P_, I]
     L.sw_precond_stages.restype = I
@@ -247,10 +247,12 @@ class Grid:
         _check(load().sw_set_precond_steps(self.h, int(m), float(theta)), "sw_set_precond_steps")
         return self
 
-    def mg_setup(self, levels: int, nu: int = 1, theta: float = 0.5, nu_coarse: int = 8, coarse_scale: float = 1.0):
-        """Geometric multigrid preconditioner with the decomposed sweep as smoother (sw_mg_setup)."""
-        _check(load().sw_mg_setup(self.h, int(levels), int(nu), float(theta), int(nu_coarse), float(coarse_scale)),
-               "sw_mg_setup")
+    def mg_setup(self, levels: int, nu: int = 1, theta: float = 0.5, nu_coarse: int = 8, coarse_scale: float = 1.0,
+                 axes: int = 0):
+        """Geometric multigrid preconditioner with the decomposed sweep as smoother (sw_mg_setup);
+        axes = bit mask of the coarsened axes (0 = all)."""
+        _check(load().sw_mg_setup(self.h, int(levels), int(nu), float(theta), int(nu_coarse), float(coarse_scale),
+                                  int(axes)), "sw_mg_setup")
         return self
 
     def mg_apply(self, r_ptr: int, z_ptr: int, stream=None):

@@ -1,91 +1,112 @@
 // mg.cuh -- grid transfer kernels of the geometric multigrid preconditioner:
-// piecewise-constant aggregation of 2^d fine nodes into one coarse node, R = P^T, and the Galerkin
-// coarse operator R A P, which is again a face-coefficient operator: each coarse face is the sum
-// of the 2^(d-1) fine faces it covers, beta_c = 2^d beta (DESIGN R-19).  All sums in a fixed order
-// (the lower index of the first remaining axis first, pairwise), mirrored by the oracle-side test.
+// piecewise-constant aggregation of the 2^k fine nodes that share a coarse node (k = number of
+// coarsened axes; all axes, or the strongly coupled ones only for anisotropic problems), R = P^T,
+// and the Galerkin coarse operator R A P, which is again a face-coefficient operator: each coarse
+// face is the sum of the fine faces it covers, beta_c = 2^k beta (DESIGN R-19).  Every sum is
+// pairwise along the coarsened axes in ascending order (pairs along the first, then pairs of
+// pairs along the next), mirrored by the oracle-side composition in tests/test_gpu_mg.py.
 #pragma once
 #include "common.cuh"
 #include "blas.cuh"
 
 namespace sw {
 
-// coarse face along axis a at coarse node I (I_a in [0, nc_a], the other axes in [0, nc_b))
-template <int DIM>
-__global__ void k_coarsen_faces(Geo Gf, Geo Gc, int a, const double *__restrict__ Ff, double *__restrict__ Fc) {
+// the coarsened axes of one level (bit a of `mask`), their fine strides and the node ratio per axis
+struct Coarsen {
+    int mask;
+    int k;             // number of coarsened axes
+    int ax[3];         // the coarsened axes, ascending
+};
+
+__host__ __device__ inline Coarsen make_coarsen(int mask, int dim) {
+    Coarsen c{};
+    c.mask = mask;
+    for (int a = 0; a < dim; ++a)
+        if ((mask >> a) & 1) c.ax[c.k++] = a;
+    return c;
+}
+
+// pairwise sum of v(offset) over the 2^k offsets spanned by strides s[0..k-1] (s[0] fastest)
+template <typename V>
+__device__ __forceinline__ double agg_sum(int k, const int64_t s[3], V v) {
+    if (k == 0) return v(0);
+    if (k == 1) return v(0) + v(s[0]);
+    const double lo = (v(0) + v(s[0])) + (v(s[1]) + v(s[1] + s[0]));
+    if (k == 2) return lo;
+    return lo + ((v(s[2]) + v(s[2] + s[0])) + (v(s[2] + s[1]) + v(s[2] + s[1] + s[0])));
+}
+
+__device__ __forceinline__ int64_t axis_stride(const Geo &G, int a) { return a == 0 ? 1 : (a == 1 ? G.P0 : G.P01); }
+
+// coarse face along axis a at coarse node I (I_a in [0, nc_a], the other axes in [0, nc_b)): the
+// sum of the fine faces at fine position r_a I_a along a over the coarsened axes other than a
+__global__ void k_coarsen_faces(Geo Gf, Geo Gc, Coarsen C, int a, const double *__restrict__ Ff,
+                                double *__restrict__ Fc) {
     int64_t m[3] = {1, 1, 1};
-    for (int b = 0; b < DIM; ++b) m[b] = Gc.n[b] + (b == a ? 1 : 0);
+    for (int b = 0; b < Gc.dim; ++b) m[b] = Gc.n[b] + (b == a ? 1 : 0);
     const int64_t total = m[0] * m[1] * m[2];
+    int k = 0;
+    int64_t s[3] = {0, 0, 0};
+    for (int t = 0; t < C.k; ++t)
+        if (C.ax[t] != a) s[k++] = axis_stride(Gf, C.ax[t]);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t I[3] = {e % m[0], (e / m[0]) % m[1], e / (m[0] * m[1])};
-        int64_t f[3] = {2 * I[0], 2 * I[1], 2 * I[2]};
-        double v;
-        auto F = [&](int64_t f0, int64_t f1, int64_t f2) {
-            return Ff ? Ff[gidx(Gf, f0 + Gf.off[0], f1 + Gf.off[1], f2 + Gf.off[2])] : 1.0;
-        };
-        if (DIM == 1) {
-            v = F(f[0], 0, 0);
-        } else if (DIM == 2) {
-            const int b = a == 0 ? 1 : 0;                 // the other axis
-            int64_t g1[3] = {f[0], f[1], 0};
-            g1[b] += 1;
-            v = F(f[0], f[1], 0) + F(g1[0], g1[1], 0);
-        } else {
-            const int b = a == 0 ? 1 : 0, c = a == 2 ? 1 : 2;   // the other two axes, ascending
-            int64_t q[4][3];
-            for (int t = 0; t < 4; ++t) {
-                q[t][0] = f[0]; q[t][1] = f[1]; q[t][2] = f[2];
-                q[t][b] += t & 1;
-                q[t][c] += t >> 1;
-            }
-            v = (F(q[0][0], q[0][1], q[0][2]) + F(q[1][0], q[1][1], q[1][2])) +
-                (F(q[2][0], q[2][1], q[2][2]) + F(q[3][0], q[3][1], q[3][2]));
-        }
+        int64_t f[3];
+        for (int b = 0; b < 3; ++b) f[b] = ((C.mask >> b) & 1) ? 2 * I[b] : I[b];
+        const int64_t i0 = gidx(Gf, f[0] + Gf.off[0], f[1] + Gf.off[1], f[2] + Gf.off[2]);
+        const double v = agg_sum(k, s, [&](int64_t d) { return Ff ? Ff[i0 + d] : 1.0; });
         Fc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] = v;
     }
 }
 
-// r_c[I] = sum of r over the 2^d fine nodes of I: pairs along x, then pairs of pairs along y, z
-template <int DIM>
-__global__ void k_restrict(Geo Gf, Geo Gc, const double *__restrict__ rf, double *__restrict__ rc) {
+// first fine node of coarse node I
+__device__ __forceinline__ int64_t fine_first(const Geo &Gf, const Coarsen &C, const int64_t I[3]) {
+    int64_t f[3];
+    for (int b = 0; b < 3; ++b) f[b] = ((C.mask >> b) & 1) ? 2 * I[b] : I[b];
+    return gidx(Gf, f[0] + Gf.off[0], f[1] + Gf.off[1], f[2] + Gf.off[2]);
+}
+
+// r_c[I] = sum of r over the fine nodes of I
+__global__ void k_restrict(Geo Gf, Geo Gc, Coarsen C, const double *__restrict__ rf, double *__restrict__ rc) {
     const int64_t total = Gc.n[0] * Gc.n[1] * Gc.n[2];
-    const int64_t S1 = Gf.P0, S2 = Gf.P01;
+    int64_t s[3] = {0, 0, 0};
+    for (int t = 0; t < C.k; ++t) s[t] = axis_stride(Gf, C.ax[t]);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t I[3] = {e % Gc.n[0], (e / Gc.n[0]) % Gc.n[1], e / (Gc.n[0] * Gc.n[1])};
-        const int64_t i = gidx(Gf, 2 * I[0] + Gf.off[0], 2 * I[1] + Gf.off[1], 2 * I[2] + Gf.off[2]);
-        double v = rf[i] + rf[i + 1];
-        if (DIM > 1) v = v + (rf[i + S1] + rf[i + S1 + 1]);
-        if (DIM > 2) v = v + ((rf[i + S2] + rf[i + S2 + 1]) + (rf[i + S2 + S1] + rf[i + S2 + S1 + 1]));
-        rc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] = v;
+        const int64_t i = fine_first(Gf, C, I);
+        rc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] =
+            agg_sum(C.k, s, [&](int64_t d) { return rf[i + d]; });
     }
 }
 
-// r_c[I] = sum over the 2^d fine nodes of I of (r - A x), in k_restrict's order: the residual of
-// the pre-smoothed iterate restricted in one pass (each fine residual as k_resid_r computes it)
+// r_c[I] = sum over the fine nodes of I of (r - A x), in k_restrict's order: the residual of the
+// pre-smoothed iterate restricted in one pass (each fine residual as k_resid_r computes it)
 template <int DIM, bool FACES>
-__global__ void k_resid_restrict(Geo Gf, Geo Gc, double beta, const double *__restrict__ F0,
+__global__ void k_resid_restrict(Geo Gf, Geo Gc, Coarsen C, double beta, const double *__restrict__ F0,
                                  const double *__restrict__ F1, const double *__restrict__ F2,
                                  const double *__restrict__ x, const double *__restrict__ r, double *__restrict__ rc) {
     const int64_t total = Gc.n[0] * Gc.n[1] * Gc.n[2];
-    const int64_t S1 = Gf.P0, S2 = Gf.P01;
-    auto res = [&](int64_t i) { return __dsub_rn(r[i], apply_A_fast<DIM, FACES>(F0, F1, F2, x, i, S1, S2, beta)); };
+    int64_t s[3] = {0, 0, 0};
+    for (int t = 0; t < C.k; ++t) s[t] = axis_stride(Gf, C.ax[t]);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t I[3] = {e % Gc.n[0], (e / Gc.n[0]) % Gc.n[1], e / (Gc.n[0] * Gc.n[1])};
-        const int64_t i = gidx(Gf, 2 * I[0] + Gf.off[0], 2 * I[1] + Gf.off[1], 2 * I[2] + Gf.off[2]);
-        double v = res(i) + res(i + 1);
-        if (DIM > 1) v = v + (res(i + S1) + res(i + S1 + 1));
-        if (DIM > 2) v = v + ((res(i + S2) + res(i + S2 + 1)) + (res(i + S2 + S1) + res(i + S2 + S1 + 1)));
-        rc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] = v;
+        const int64_t i = fine_first(Gf, C, I);
+        rc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])] = agg_sum(C.k, s, [&](int64_t d) {
+            return __dsub_rn(r[i + d], apply_A_fast<DIM, FACES>(F0, F1, F2, x, i + d, Gf.P0, Gf.P01, beta));
+        });
     }
 }
 
-// x[i] += s x_c[i / 2]  (product and sum rounded separately; s = 1 adds x_c)
-template <int DIM>
-__global__ void k_prolong_add(Geo Gf, Geo Gc, double sc, const double *__restrict__ xc, double *__restrict__ xf) {
+// x[i] += s x_c[parent(i)]  (product and sum rounded separately; s = 1 adds x_c)
+__global__ void k_prolong_add(Geo Gf, Geo Gc, Coarsen C, double sc, const double *__restrict__ xc,
+                              double *__restrict__ xf) {
     const int64_t total = Gf.n[0] * Gf.n[1] * Gf.n[2];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i[3] = {e % Gf.n[0], (e / Gf.n[0]) % Gf.n[1], e / (Gf.n[0] * Gf.n[1])};
+        int64_t I[3];
+        for (int b = 0; b < 3; ++b) I[b] = ((C.mask >> b) & 1) ? i[b] / 2 : i[b];
         const int64_t fi = gidx(Gf, i[0] + Gf.off[0], i[1] + Gf.off[1], i[2] + Gf.off[2]);
-        xf[fi] = __dadd_rn(xf[fi], __dmul_rn(sc, xc[gidx(Gc, i[0] / 2 + Gc.off[0], i[1] / 2 + Gc.off[1], i[2] / 2 + Gc.off[2])]));
+        xf[fi] = __dadd_rn(xf[fi], __dmul_rn(sc, xc[gidx(Gc, I[0] + Gc.off[0], I[1] + Gc.off[1], I[2] + Gc.off[2])]));
     }
 }
 

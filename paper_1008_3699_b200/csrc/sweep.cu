@@ -66,6 +66,7 @@ struct sw_grid {
     std::vector<sw_grid *> mg;
     int mg_nu = 1, mg_nu_coarse = 8;
     double mg_theta = 0.5, mg_scale = 1.0;
+    int mg_axes = 0;                       // coarsened axes (bit a), every level
     double *MGR = nullptr, *MGX = nullptr, *MT1 = nullptr, *MT2 = nullptr;
     CgScalars *hcg = nullptr;              // pinned host copy of the PCG scalars
     cudaStream_t cap_stream = nullptr;     // private stream for CUDA-graph capture
@@ -723,13 +724,17 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
 }
 
 // ---------------------------------------------------------------- geometric multigrid (N1)
-extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale) {
+extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale,
+                                 int axes) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (g->nranks > 1) return fail(SW_EINVAL, "multigrid is single-rank in this build");
     if (levels < 2 || levels > 16 || nu < 1 || nu > 64 || nu_coarse < 1 || nu_coarse > 1024 ||
         !(theta > 0.0 && theta <= 1.0) || !(coarse_scale > 0.0 && coarse_scale <= 4.0))
         return fail(SW_EINVAL, "bad multigrid parameters");
+    if (axes == 0) axes = (1 << g->dim) - 1;
+    if (axes < 0 || axes >= (1 << g->dim)) return fail(SW_EINVAL, "bad multigrid axes mask");
     g->mg_scale = coarse_scale;
+    g->mg_axes = axes;
     for (sw_grid *c : g->mg) sw_destroy(c);
     g->mg.clear();
     g->mg_nu = nu;
@@ -743,13 +748,14 @@ extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, i
         int64_t nc[3] = {1, 1, 1};
         int tc[3] = {1, 1, 1};
         for (int a = 0; a < g->dim; ++a) {
-            if (fine->ng[a] % 2) return fail(SW_EINVAL, "every level must have an even node count per axis");
-            nc[a] = fine->ng[a] / 2;
+            const bool co = (axes >> a) & 1;
+            if (co && fine->ng[a] % 2) return fail(SW_EINVAL, "every level must have an even node count per axis");
+            nc[a] = co ? fine->ng[a] / 2 : fine->ng[a];
             tc[a] = fine->tile[a] <= nc[a] ? fine->tile[a] : (int)nc[a];
             while (nc[a] % tc[a]) --tc[a];
         }
         sw_grid *c = nullptr;
-        double bc = fine->beta * (double)(1 << g->dim);
+        double bc = fine->beta * (double)(1 << __builtin_popcount(axes));
         if ((st = sw_create_grid(g->dim, nc, SW_COEF_FACES, bc, g->dev, &c)) != SW_OK) return st;
         g->mg.push_back(c);
         c->fast2d = g->fast2d;
@@ -759,9 +765,7 @@ extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, i
             const double *ff = (fine == g) ? (src_faces ? src_faces[a] : nullptr) : fine->F[a];
             const int64_t tot = (nc[0] + (a == 0)) * (nc[1] + (a == 1)) * (nc[2] + (a == 2));
             const int nb = (int)std::min<int64_t>((tot + 255) / 256, 4096);
-            if (g->dim == 1) k_coarsen_faces<1><<<nb, 256>>>(fine->G, c->G, a, ff, c->F[a]);
-            else if (g->dim == 2) k_coarsen_faces<2><<<nb, 256>>>(fine->G, c->G, a, ff, c->F[a]);
-            else k_coarsen_faces<3><<<nb, 256>>>(fine->G, c->G, a, ff, c->F[a]);
+            k_coarsen_faces<<<nb, 256>>>(fine->G, c->G, make_coarsen(axes, g->dim), a, ff, c->F[a]);
             CK(cudaGetLastError());
         }
         CK(cudaDeviceSynchronize());
@@ -822,18 +826,19 @@ static sw_status mg_residual(sw_grid *l, const double *r, const double *x, doubl
 }
 
 // r_c = R (r - A x), one pass
-static sw_status mg_resid_restrict(sw_grid *l, sw_grid *c, const double *r, const double *x, cudaStream_t s) {
+static sw_status mg_resid_restrict(sw_grid *l, sw_grid *c, int axes, const double *r, const double *x, cudaStream_t s) {
     const int64_t nct = c->G.n[0] * c->G.n[1] * c->G.n[2];
     const int nb = (int)std::min<int64_t>((nct + 255) / 256, 8192);
     const double *F0 = l->F[0], *F1 = l->F[1], *F2 = l->F[2];
     const bool fc = !l->G.poisson;
     const double bt = l->G.beta;
-    if (l->dim == 1) fc ? k_resid_restrict<1, true><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR)
-                        : k_resid_restrict<1, false><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR);
-    else if (l->dim == 2) fc ? k_resid_restrict<2, true><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR)
-                             : k_resid_restrict<2, false><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR);
-    else fc ? k_resid_restrict<3, true><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR)
-            : k_resid_restrict<3, false><<<nb, 256, 0, s>>>(l->G, c->G, bt, F0, F1, F2, x, r, c->MGR);
+    const Coarsen C = make_coarsen(axes, l->dim);
+    if (l->dim == 1) fc ? k_resid_restrict<1, true><<<nb, 256, 0, s>>>(l->G, c->G, C, bt, F0, F1, F2, x, r, c->MGR)
+                        : k_resid_restrict<1, false><<<nb, 256, 0, s>>>(l->G, c->G, C, bt, F0, F1, F2, x, r, c->MGR);
+    else if (l->dim == 2) fc ? k_resid_restrict<2, true><<<nb, 256, 0, s>>>(l->G, c->G, C, bt, F0, F1, F2, x, r, c->MGR)
+                             : k_resid_restrict<2, false><<<nb, 256, 0, s>>>(l->G, c->G, C, bt, F0, F1, F2, x, r, c->MGR);
+    else fc ? k_resid_restrict<3, true><<<nb, 256, 0, s>>>(l->G, c->G, C, bt, F0, F1, F2, x, r, c->MGR)
+            : k_resid_restrict<3, false><<<nb, 256, 0, s>>>(l->G, c->G, C, bt, F0, F1, F2, x, r, c->MGR);
     l->launches++;
     CK(cudaGetLastError());
     return SW_OK;
@@ -847,13 +852,11 @@ static sw_status mg_vcycle(sw_grid *g, int lev, const double *r, double *x, cuda
     if (lev == nlev - 1) return mg_smooth(l, r, x, g->mg_nu_coarse, g->mg_theta, s);
     if ((st = mg_smooth(l, r, x, g->mg_nu, g->mg_theta, s)) != SW_OK) return st;          // pre-smoothing
     sw_grid *c = g->mg[lev];
-    if ((st = mg_resid_restrict(l, c, r, x, s)) != SW_OK) return st;                    // r_c = R (r - A x)
+    if ((st = mg_resid_restrict(l, c, g->mg_axes, r, x, s)) != SW_OK) return st;       // r_c = R (r - A x)
     if ((st = mg_vcycle(g, lev + 1, c->MGR, c->MGX, s)) != SW_OK) return st;             // coarse correction
     const int64_t nft = l->G.n[0] * l->G.n[1] * l->G.n[2];
     const int nbf = (int)std::min<int64_t>((nft + 255) / 256, 8192);
-    if (g->dim == 1) k_prolong_add<1><<<nbf, 256, 0, s>>>(l->G, c->G, g->mg_scale, c->MGX, x);
-    else if (g->dim == 2) k_prolong_add<2><<<nbf, 256, 0, s>>>(l->G, c->G, g->mg_scale, c->MGX, x);
-    else k_prolong_add<3><<<nbf, 256, 0, s>>>(l->G, c->G, g->mg_scale, c->MGX, x);
+    k_prolong_add<<<nbf, 256, 0, s>>>(l->G, c->G, make_coarsen(g->mg_axes, g->dim), g->mg_scale, c->MGX, x);
     l->launches++;
     CK(cudaGetLastError());
     if ((st = mg_residual(l, r, x, l->MT2, s)) != SW_OK) return st;                      // MT2 = r - A x

@@ -13,42 +13,39 @@ from tests.gpu_helpers import make_grid, rand_faces, rel_maxdiff
 pytestmark = pytest.mark.gpu
 
 
-# ---- the oracle-side V-cycle (numpy + oracle calls; sums in the order DESIGN R-19 fixes)
-def coarsen_faces(faces, n):
+# ---- the oracle-side V-cycle (numpy + oracle calls; sums in the order DESIGN R-19 fixes: pairwise
+# along the coarsened axes, ascending)
+def _pairs(v, ax):
+    return np.take(v, np.arange(0, v.shape[ax], 2), axis=ax) + np.take(v, np.arange(1, v.shape[ax], 2), axis=ax)
+
+
+def coarsen_faces(faces, n, mask):
     dim = len(n)
     out = []
     for a in range(dim):
         f = np.ones(O.face_shape(n, a)) if faces is None else np.asarray(faces[a])
         ax = dim - 1 - a                                   # numpy axis of grid axis a
-        g = np.take(f, np.arange(0, f.shape[ax], 2), axis=ax)          # the faces at even positions along a
-        others = [b for b in range(dim) if b != a]         # ascending grid axes
-        if dim == 1:
-            out.append(g)
-            continue
-        b = others[0]
-        nb = dim - 1 - b
-        h = np.take(g, np.arange(0, g.shape[nb], 2), axis=nb) + np.take(g, np.arange(1, g.shape[nb], 2), axis=nb)
-        if dim == 3:
-            c = others[1]
-            nc = dim - 1 - c
-            h = np.take(h, np.arange(0, h.shape[nc], 2), axis=nc) + np.take(h, np.arange(1, h.shape[nc], 2), axis=nc)
-        out.append(h)
+        g = np.take(f, np.arange(0, f.shape[ax], 2), axis=ax) if (mask >> a) & 1 else f
+        for b in range(dim):                               # the other coarsened axes, ascending
+            if b != a and (mask >> b) & 1:
+                g = _pairs(g, dim - 1 - b)
+        out.append(g)
     return tuple(out)
 
 
-def restrict(r):
+def restrict(r, mask):
     dim = r.ndim
-    v = r[..., 0::2] + r[..., 1::2]
-    if dim > 1:
-        v = v[..., 0::2, :] + v[..., 1::2, :]
-    if dim > 2:
-        v = v[0::2] + v[1::2]
-    return v
+    for a in range(dim):
+        if (mask >> a) & 1:
+            r = _pairs(r, dim - 1 - a)
+    return r
 
 
-def prolong(xc):
-    for ax in range(xc.ndim):
-        xc = np.repeat(xc, 2, axis=ax)
+def prolong(xc, mask):
+    dim = xc.ndim
+    for a in range(dim):
+        if (mask >> a) & 1:
+            xc = np.repeat(xc, 2, axis=dim - 1 - a)
     return xc
 
 
@@ -59,13 +56,14 @@ def coarse_tile(t, nc):
     return t
 
 
-def build_levels(n, tile, faces, beta, levels):
+def build_levels(n, tile, faces, beta, levels, mask):
     lv = [(tuple(n), tuple(tile), faces, beta)]
+    k = bin(mask).count("1")
     for _ in range(levels - 1):
         n0, t0, f0, b0 = lv[-1]
-        nc = tuple(v // 2 for v in n0)
+        nc = tuple(v // 2 if (mask >> a) & 1 else v for a, v in enumerate(n0))
         tc = tuple(coarse_tile(t, v) for t, v in zip(t0, nc))
-        lv.append((nc, tc, coarsen_faces(f0, n0), b0 * 2 ** len(n)))
+        lv.append((nc, tc, coarsen_faces(f0, n0, mask), b0 * 2 ** k))
     return [O.tiled(nn, tt, faces=ff, beta=bb) for nn, tt, ff, bb in lv]
 
 
@@ -76,32 +74,35 @@ def smooth(pb, r, m, theta):
     return theta * z
 
 
-def vcycle(pbs, lev, r, nu, theta, nu_c, sc=1.0):
+def vcycle(pbs, lev, r, nu, theta, nu_c, sc=1.0, mask=7):
     pb = pbs[lev]
     if lev == len(pbs) - 1:
         return smooth(pb, r, nu_c, theta)
     x = smooth(pb, r, nu, theta)
-    xc = vcycle(pbs, lev + 1, restrict(r - O.apply_A(pb, x)), nu, theta, nu_c, sc)
-    x = x + sc * prolong(xc)
+    xc = vcycle(pbs, lev + 1, restrict(r - O.apply_A(pb, x), mask), nu, theta, nu_c, sc, mask)
+    x = x + sc * prolong(xc, mask)
     return x + smooth(pb, r - O.apply_A(pb, x), nu, theta)
 
 
-CASES = [((256, 256), (64, 64), False, 0.0, 3), ((128, 128), (64, 64), True, 0.0, 4),
-         ((64, 32, 32), (32, 8, 4), True, 0.0, 3), ((32, 32, 32), (16, 8, 4), False, 0.1, 3)]
+CASES = [((256, 256), (64, 64), False, 0.0, 3, 0), ((128, 128), (64, 64), True, 0.0, 4, 0),
+         ((64, 32, 32), (32, 8, 4), True, 0.0, 3, 0), ((32, 32, 32), (16, 8, 4), False, 0.1, 3, 0),
+         ((64, 32, 16), (32, 8, 4), True, 0.0, 3, 3), ((128, 64), (64, 64), True, 0.05, 3, 1),
+         ((32, 32, 16), (16, 8, 4), True, 0.0, 3, 5)]
 
 
-@pytest.mark.parametrize("n,tile,var,beta,levels", CASES)
+@pytest.mark.parametrize("n,tile,var,beta,levels,axes", CASES)
 @pytest.mark.parametrize("nu,theta,sc", [(1, 0.5, 1.0), (2, 0.6, 1.7)])
-def test_vcycle_matches_oracle(n, tile, var, beta, levels, nu, theta, sc):
+def test_vcycle_matches_oracle(n, tile, var, beta, levels, axes, nu, theta, sc):
     faces = rand_faces(n, 17) if var else None
-    pbs = build_levels(n, tile, faces, beta, levels)
+    mask = axes or (1 << len(n)) - 1
+    pbs = build_levels(n, tile, faces, beta, levels, mask)
     r = gen.uniform_field(8, gen.STREAM_TEST, pbs[0].shape)
-    g = make_grid(B, n, tile, faces, beta).mg_setup(levels, nu, theta, 6, sc)
+    g = make_grid(B, n, tile, faces, beta).mg_setup(levels, nu, theta, 6, sc, axes)
     g.set_vector(B.R, r)
     g.mg_apply(g.ptr(B.R), g.ptr(B.Z))
     torch.cuda.synchronize()
     g.check()
-    want = vcycle(pbs, 0, r, nu, theta, 6, sc)
+    want = vcycle(pbs, 0, r, nu, theta, 6, sc, mask)
     assert rel_maxdiff(g.get_vector(B.Z), want) <= 1e-12
 
 
