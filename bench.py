@@ -335,13 +335,13 @@ def run_secondary(args):
     out["c3_pcg_ilu0"] = {"iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
                           "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
     # multigrid-preconditioned CG with the decomposed sweep as smoother
-    g.mg_setup(6, 1, 0.5, 16, 1.2)
+    g.mg_setup(7, 1, 0.5, 16, 1.8)                  # 7 levels: coarsest 64^2 = one box
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     it, rel, ok = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    out["c3_pcg_mg"] = {"levels": 6, "nu": 1, "theta": 0.5, "nu_coarse": 16, "coarse_scale": 1.2, "iterations": it,
+    out["c3_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.5, "nu_coarse": 16, "coarse_scale": 1.8, "iterations": it,
                         "relres": rel, "converged": ok, "seconds": round(dt, 3),
                         "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
     del g, b

@@ -171,6 +171,13 @@ sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coars
 /* z = B r, one V-cycle from zero (padded device arrays as for sw_ilu_apply; borrowed). */
 sw_status sw_mg_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_stream_t s);
 
+/* Cycle index gamma of the multigrid preconditioner: 1 = V-cycle (default), 2 = W-cycle (each level
+ * above the coarsest corrects twice: x_c = C r_c, then x_c += C (r_c - A_c x_c), C the level's
+ * cycle).  2 C - C A_c C is symmetric, so the W-cycle stays a valid CG preconditioner whenever the
+ * coarse cycle converges.  Takes effect from the next sw_mg_apply / SW_PC_MG solve.  SW_EINVAL for
+ * gamma outside {1, 2}. */
+sw_status sw_mg_set_cycle(sw_grid *g, int gamma);
+
 /* Preconditioned CG from x0 = 0 on the right-hand side SW_B until ||r||/||b|| < rtol
  * (recursive residual) or maxit; result in SW_X.  precond SW_PC_ILU0 factors at phase 0
  * first.  SW_ENOCONV: iters/relres still valid.  Single rank. */

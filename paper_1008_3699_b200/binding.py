@@ -60,6 +60,7 @@ def load():
     L.sw_set_precond_steps.argtypes = [P_, I, D]
     L.sw_mg_setup.argtypes = [P_, I, I, D, I, D, I]
     L.sw_mg_apply.argtypes = [P_, P_, P_, P_]
+    L.sw_mg_set_cycle.argtypes = [P_, I]
     L.sw_precond_stages.argtypes = [P_, I]
     L.sw_precond_stages.restype = I
     L.sw_ilu_apply_stage.argtypes = [P_, I, P_, P_, I, P_]
@@ -253,6 +254,11 @@ class Grid:
         axes = bit mask of the coarsened axes (0 = all)."""
         _check(load().sw_mg_setup(self.h, int(levels), int(nu), float(theta), int(nu_coarse), float(coarse_scale),
                                   int(axes)), "sw_mg_setup")
+        return self
+
+    def mg_set_cycle(self, gamma: int):
+        """1 = V-cycle, 2 = W-cycle (sw_mg_set_cycle)."""
+        _check(load().sw_mg_set_cycle(self.h, int(gamma)), "sw_mg_set_cycle")
         return self
 
     def mg_apply(self, r_ptr: int, z_ptr: int, stream=None):

@@ -67,7 +67,9 @@ struct sw_grid {
     int mg_nu = 1, mg_nu_coarse = 8;
     double mg_theta = 0.5, mg_scale = 1.0;
     int mg_axes = 0;                       // coarsened axes (bit a), every level
+    int mg_gamma = 1;                      // coarse corrections per level: 1 = V-cycle, 2 = W-cycle
     double *MGR = nullptr, *MGX = nullptr, *MT1 = nullptr, *MT2 = nullptr;
+    double *MGW = nullptr, *MGY = nullptr; // W-cycle: second coarse right-hand side / correction
     CgScalars *hcg = nullptr;              // pinned host copy of the PCG scalars
     cudaStream_t cap_stream = nullptr;     // private stream for CUDA-graph capture
     DD *partial = nullptr;
@@ -136,7 +138,7 @@ static void free_all(sw_grid *g) {
     g->mg.clear();
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
                        &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2,
-                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2};
+                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->hcg) cudaFreeHost(g->hcg);
@@ -769,7 +771,7 @@ extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, i
             CK(cudaGetLastError());
         }
         CK(cudaDeviceSynchronize());
-        double **ptrs[] = {&c->MGR, &c->MGX, &c->MT1, &c->MT2};
+        double **ptrs[] = {&c->MGR, &c->MGX, &c->MT1, &c->MT2, &c->MGW, &c->MGY};
         for (double **p : ptrs)
             if ((st = alloc_arr(c, p)) != SW_OK) return st;
         fine = c;
@@ -854,6 +856,15 @@ static sw_status mg_vcycle(sw_grid *g, int lev, const double *r, double *x, cuda
     sw_grid *c = g->mg[lev];
     if ((st = mg_resid_restrict(l, c, g->mg_axes, r, x, s)) != SW_OK) return st;       // r_c = R (r - A x)
     if ((st = mg_vcycle(g, lev + 1, c->MGR, c->MGX, s)) != SW_OK) return st;             // coarse correction
+    if (g->mg_gamma == 2 && lev + 1 < nlev - 1) {            // W-cycle: a second cycle on the coarse residual
+        if ((st = mg_residual(c, c->MGR, c->MGX, c->MGW, s)) != SW_OK) return st;         // MGW = r_c - A_c x_c
+        if ((st = mg_vcycle(g, lev + 1, c->MGW, c->MGY, s)) != SW_OK) return st;
+        const Rows RC = make_rows(c->G);
+        const int nrc = (int)std::min<int64_t>(RC.items, RED_BLOCKS);
+        k_addto_r<<<nrc, RED_THREADS, 0, s>>>(RC, c->MGX, c->MGY);
+        c->launches++;
+        CK(cudaGetLastError());
+    }
     const int64_t nft = l->G.n[0] * l->G.n[1] * l->G.n[2];
     const int nbf = (int)std::min<int64_t>((nft + 255) / 256, 8192);
     k_prolong_add<<<nbf, 256, 0, s>>>(l->G, c->G, make_coarsen(g->mg_axes, g->dim), g->mg_scale, c->MGX, x);
@@ -880,6 +891,13 @@ extern "C" sw_status sw_mg_apply(sw_grid *g, const double *r_dev, double *z_dev,
         c->launches = 0;
     }
     return st;
+}
+
+extern "C" sw_status sw_mg_set_cycle(sw_grid *g, int gamma) {
+    if (!g) return fail(SW_EINVAL, "null grid");
+    if (gamma != 1 && gamma != 2) return fail(SW_EINVAL, "cycle index must be 1 (V) or 2 (W)");
+    g->mg_gamma = gamma;
+    return SW_OK;
 }
 
 extern "C" sw_status sw_set_precond_steps(sw_grid *g, int m, double theta) {

@@ -74,12 +74,15 @@ def smooth(pb, r, m, theta):
     return theta * z
 
 
-def vcycle(pbs, lev, r, nu, theta, nu_c, sc=1.0, mask=7):
+def vcycle(pbs, lev, r, nu, theta, nu_c, sc=1.0, mask=7, gamma=1):
     pb = pbs[lev]
     if lev == len(pbs) - 1:
         return smooth(pb, r, nu_c, theta)
     x = smooth(pb, r, nu, theta)
-    xc = vcycle(pbs, lev + 1, restrict(r - O.apply_A(pb, x), mask), nu, theta, nu_c, sc, mask)
+    rc = restrict(r - O.apply_A(pb, x), mask)
+    xc = vcycle(pbs, lev + 1, rc, nu, theta, nu_c, sc, mask, gamma)
+    if gamma == 2 and lev + 1 < len(pbs) - 1:         # W-cycle: second coarse cycle on the coarse residual
+        xc = xc + vcycle(pbs, lev + 1, rc - O.apply_A(pbs[lev + 1], xc), nu, theta, nu_c, sc, mask, gamma)
     x = x + sc * prolong(xc, mask)
     return x + smooth(pb, r - O.apply_A(pb, x), nu, theta)
 
@@ -104,6 +107,30 @@ def test_vcycle_matches_oracle(n, tile, var, beta, levels, axes, nu, theta, sc):
     g.check()
     want = vcycle(pbs, 0, r, nu, theta, 6, sc, mask)
     assert rel_maxdiff(g.get_vector(B.Z), want) <= 1e-12
+
+
+@pytest.mark.parametrize("n,tile,var,beta,levels,axes", [((256, 256), (64, 64), True, 0.0, 4, 0),
+                                                         ((64, 32, 16), (32, 8, 4), True, 0.0, 4, 3),
+                                                         ((32, 32, 32), (16, 8, 4), False, 0.1, 3, 0)])
+def test_wcycle_matches_oracle(n, tile, var, beta, levels, axes):
+    """gamma = 2 (sw_mg_set_cycle): every level above the coarsest corrects twice."""
+    faces = rand_faces(n, 23) if var else None
+    mask = axes or (1 << len(n)) - 1
+    pbs = build_levels(n, tile, faces, beta, levels, mask)
+    r = gen.uniform_field(9, gen.STREAM_TEST, pbs[0].shape)
+    g = make_grid(B, n, tile, faces, beta).mg_setup(levels, 1, 0.5, 4, 1.2, axes).mg_set_cycle(2)
+    g.set_vector(B.R, r)
+    g.mg_apply(g.ptr(B.R), g.ptr(B.Z))
+    torch.cuda.synchronize()
+    g.check()
+    want = vcycle(pbs, 0, r, 1, 0.5, 4, 1.2, mask, gamma=2)
+    assert rel_maxdiff(g.get_vector(B.Z), want) <= 1e-12
+    g.mg_set_cycle(1)                                   # back to the V-cycle
+    g.mg_apply(g.ptr(B.R), g.ptr(B.Z))
+    torch.cuda.synchronize()
+    assert rel_maxdiff(g.get_vector(B.Z), vcycle(pbs, 0, r, 1, 0.5, 4, 1.2, mask)) <= 1e-12
+    with pytest.raises(B.SweepError):
+        g.mg_set_cycle(3)
 
 
 @pytest.mark.parametrize("n,tile,var,levels", [((256, 256), (64, 64), True, 4), ((64, 64, 64), (32, 8, 4), True, 3)])

@@ -1,4 +1,5 @@
-"""MG-PCG settings probe for config 3 (2D lognormal faces, 64 x 64 boxes): python tools/mg_probe2d.py n L,nu,theta,nc,s ..."""
+"""Per-configuration V/W-cycle cost (graph-captured sw_mg_apply) and MG-PCG iterations for config 3:
+python tools/mg_time.py n L,nu,theta,nc,s[,axes[,gamma]] ..."""
 import os
 import sys
 import time
@@ -16,6 +17,7 @@ def main():
     k = gen.lognormal_k(0, (n + 2, n + 2), 1.0)
     g.set_coefficients_k(np.pad(k, [(1, 1), (0, 0)], constant_values=1.0), (1.0, 1.0))
     g.set_vector(B.B, gen.uniform_field(0, gen.STREAM_RHS, (n, n)) / float((n + 1) ** 2))
+    shp = tuple(int(v) for v in reversed(g.padded_shape)) if hasattr(g, "padded_shape") else None
     for a in sys.argv[2:]:
         S = tuple(float(x) if '.' in x else int(x) for x in a.split(','))
         g.mg_setup(*S[:6])
@@ -24,7 +26,8 @@ def main():
         t = time.perf_counter()
         it, rel, ok = g.pcg_solve(B.PC_MG, 1.0, 0, 1e-8, 20000)
         torch.cuda.synchronize()
-        print(f"n={n} MG {S}: it={it} ok={ok} {time.perf_counter() - t:.2f}s")
+        el = time.perf_counter() - t
+        print(f"n={n} MG {S}: it={it} ok={ok} {el:.2f}s  {1e3 * el / max(it, 1):.3f} ms/it", flush=True)
 
 
 if __name__ == "__main__":
