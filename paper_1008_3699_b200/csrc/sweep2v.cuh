@@ -6,12 +6,12 @@
 //  r0  = fma(alpha, fma(c_N, u_N, fma(c_E, u_E, b)), (1 - w) u),
 //  m_W = alpha c_W,  m_S = alpha c_S,   u = fma(m_S, S, fma(m_W, W, r0))     (DESIGN R-7)
 //
-// One CTA = four warps = one box; 105 KB of shared memory (x window with r0 in place, m_W and
+// One CTA = eight warps = one box; 105 KB of shared memory (x window with r0 in place, m_W and
 // m_S per node, the partner couplings of the start-face chains), two CTAs per SM.
 //  1. Stage-in: TMA load of the 68 x 68 x_old window; TMA tensor prefetches of the b, F_x
 //     and F_y tiles into L2; each warp streams its rows of b / F_x / F_y through a register ring.
 //  2. Partners (warps 0, 1): r0 and couplings of the y-face row, the x-face column and the
-//     diagonal corner partner; explicit parts of the own nodes (all warps, 16 rows each, in
+//     diagonal corner partner; explicit parts of the own nodes (all warps, 8 rows each, in
 //     sweep order), one IEEE division per node.
 //  3. Corner set and the two start-face chains (warp 1, lanes 0 and 1).
 //  4. Wavefront (warp 0): lane l owns rows 2l+1, 2l+2; 94 branch-free steps.
@@ -28,7 +28,10 @@ namespace sw {
 
 namespace v2 {
 constexpr int T = 64, W = 68, WS = W * W;
-constexpr int NW = 4;                   // warps per box
+#ifndef SW_V2_NW
+#define SW_V2_NW 8
+#endif
+constexpr int NW = SW_V2_NW;            // warps per box (8: the prologue streams 8 rows per warp)
 constexpr int ROWS = T / NW;            // prologue rows per warp
 constexpr int RING = 4;                 // rows in flight per warp
 constexpr int NCOEF = T * T;            // m_W / m_S arrays, pitch 64 (window column order)
@@ -211,7 +214,7 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
         }
     }
 
-    // ---------------------------------------------------------------- 2b. own nodes (16 rows per warp)
+    // ---------------------------------------------------------------- 2b. own nodes (ROWS rows per warp)
     {
         double *px = xw + WY(t_first) * W + wc;
         double *pw = cW + (WY(t_first) - 2) * T + (wc - 2);
@@ -446,7 +449,7 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
         SW_TADDT(7, t_w0, t_w1, 0);
     }
 
-    // ---------------------------------------------------------------- 5. write-back (16 rows per warp)
+    // ---------------------------------------------------------------- 5. write-back (ROWS rows per warp)
     __syncthreads();
     SW_TMARK(t_wave);
     {
