@@ -247,6 +247,190 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
     const int n0 = cpl[0] ? T2 : 0, n1 = cpl[1] ? T2 : 0, n2 = cpl[2] ? T1 : 0;
     const int nlines = NA == 1 ? n0 + n1 + n2 : 3;
     const int dmax = NA == 2 ? tmax - 1 : T0 - 1 + (T1 > T2 ? T1 : T2) - 1;
+    // geometry of line `ln` at step d: active?, rank-0 corner gl of the set, set axes, and the
+    // line's walk / fixed axes
+    auto geom = [&](int d, int ln, bool &ok, int64_t (&gl)[3], int &mask, int &walk, int &fixax) {
+        int fa = -1, fixv = 0;
+        walk = 0;
+        fixax = 0;
+        if (NA == 1) {
+            if (ln < n0) { fa = 0; fixax = 2; fixv = ln; walk = 1; }
+            else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
+            else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
+        } else {
+            if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; fixax = -1; }
+        }
+        ok = fa >= 0;
+        int l[3] = {0, 0, 0};
+        if (ok && NA == 1) {
+            l[fixax] = fixv;
+            l[walk] = d - fixv;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (a != fa && (l[a] < (cpl[a] ? 1 : 0) || l[a] >= G.T[a])) ok = false;
+        } else if (ok) {
+            l[walk] = d;
+            if (d < (cpl[walk] ? 1 : 0) || d >= G.T[walk]) ok = false;
+        }
+        mask = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            gl[a] = 0;
+            if (ok) {
+                const int64_t g = s[a] ? (lo_g[a] + G.T[a] - 1 - l[a]) : (lo_g[a] + l[a]);
+                gl[a] = g;
+                if (cpl[a] && l[a] == 0) {
+                    mask |= 1 << a;
+                    const int64_t other = s[a] ? (lo_g[a] + G.T[a]) : (lo_g[a] - 1);
+                    if (other < gl[a]) gl[a] = other;
+                }
+            }
+        }
+    };
+    if (nlines <= 32 / K) {
+        // Fast path (every line in one pass; 32 x 8 x 4 boxes).  Along a line every member row has
+        // the same shape: the partner across each set axis (the matrix entry), the node beyond it
+        // (a value of phase 1 or of the previous launch), the next node along the line (this lane's
+        // result of the previous step) and, for sheets, the same node of the next line (the result
+        // of lane + K in the previous step).  So the row is built from per-line constants and
+        // values already in registers, with exactly the operations and order of tri3t_row (axes
+        // ascending, one term per axis), and the loads of step d - 1 are issued during step d.
+        const int ln = grp;
+        bool act;
+        int64_t gl0[3];
+        int mask, walk, fixax;
+        // geometry at the line's first active step (any active d gives the same mask and the
+        // same coordinates off the walk axis)
+        int fixv = 0, lo_w = 0;
+        {
+            int l_ln = ln, fa = -1;
+            if (NA == 1) {
+                if (l_ln < n0) { fa = 0; fixv = l_ln; }
+                else if ((l_ln -= n0) < n1) { fa = 1; fixv = l_ln; }
+                else if ((l_ln -= n1) < n2) { fa = 2; fixv = l_ln; }
+            } else if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) {
+                fa = ln;
+            }
+            act = fa >= 0;
+            int w_ = 0, f_ = 0;
+            if (act) {
+                if (NA == 1) { w_ = fa == 0 ? 1 : 0; f_ = fa == 2 ? 1 : 2; }
+                else w_ = fa;
+            }
+            lo_w = cpl[w_] ? 1 : 0;
+            if (NA == 1 && act && (fixv < (cpl[f_] ? 1 : 0) || fixv >= G.T[f_])) act = false;
+            bool okg = false;
+            int wk, fx;
+            geom(NA == 1 ? lo_w + fixv : lo_w, ln, okg, gl0, mask, wk, fx);
+            act = act && okg;
+            walk = w_;
+            fixax = f_;
+        }
+        const int Tw = G.T[walk];
+        // member coordinates at l[walk] = lo_w, and the per-axis roles
+        int bitof[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) bitof[a] = __popc(mask & ((1 << a) - 1));
+        int64_t g[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g[a] = gl0[a] + (((mask >> a) & 1) ? ((p >> bitof[a]) & 1) : 0);
+        const int64_t S[3] = {1, G.P0, G.P01};
+        const int lw = s[walk] ? -1 : 1;                       // global step of local +1 along the walk
+        const int lf = NA == 1 ? (s[fixax] ? -1 : 1) : 0;
+        const int64_t istep = lw * S[walk];
+        const int64_t i_lo = act ? gidx(G, g[0], g[1], g[2]) : 0;   // member index at l[walk] = lo_w
+        const bool fix_term = NA == 1 && act && fixv + 1 < G.T[fixax];
+        // set axes: direction of the partner / of the node beyond; the node beyond exists unless
+        // the box is one node thick there
+        int sdp[3], sdb[3];
+        bool bey[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int b = ((mask >> a) & 1) ? ((p >> bitof[a]) & 1) : 0;
+            sdp[a] = b ? -1 : 1;
+            sdb[a] = -sdp[a];
+            bey[a] = G.T[a] >= 2;
+        }
+        const double *const F[3] = {A.f0, A.f1, A.f2};
+        struct Pre { double src, invd, fm[3], fp[3], zb[3]; };
+        auto pref = [&](int64_t i, Pre &P) {
+            P.src = A.src[i];
+            P.invd = A.invd ? A.invd[i] : 0.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                P.fm[a] = G.poisson ? 1.0 : F[a][i];
+                P.fp[a] = G.poisson ? 1.0 : F[a][i + S[a]];
+                P.zb[a] = ((mask >> a) & 1) ? A.z[i + sdb[a] * S[a]] : 0.0;
+            }
+        };
+        auto lw_at = [&](int d) { return NA == 1 ? d - fixv : d; };   // l[walk] at step d
+        Pre cur, nxt;
+        {
+            const int l = lw_at(dmax);
+            if (act && l >= lo_w && l < Tw) pref(i_lo + (l - lo_w) * istep, cur);
+        }
+        double prev = 0.0;
+        for (int d = dmax; d >= 0; --d) {
+            const int l = lw_at(d);
+            const bool okc = act && l >= lo_w && l < Tw;
+            const int ln1 = l - 1;
+            if (d > 0 && act && ln1 >= lo_w && ln1 < Tw) pref(i_lo + (ln1 - lo_w) * istep, nxt);
+            const double adj = __shfl_sync(0xffffffffu, prev, (threadIdx.x + K) & 31);   // next line, same member
+            double rhs = 0.0, off[NA];
+#pragma unroll
+            for (int t = 0; t < NA; ++t) off[t] = 0.0;
+            if (okc) {
+                double al;
+                if (A.invd) {
+                    al = cur.invd;
+                } else {
+                    const double ap = (((cur.fm[0] + cur.fp[0]) + (cur.fm[1] + cur.fp[1])) + (cur.fm[2] + cur.fp[2])) + G.beta;
+                    al = A.omega / ap;
+                }
+                double acc = A.coef * cur.src;
+                int t = 0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    if ((mask >> a) & 1) {                       // set axis: partner entry, node beyond
+                        const double mp = al * (sdp[a] < 0 ? cur.fm[a] : cur.fp[a]);
+                        const double mb = al * (sdb[a] < 0 ? cur.fm[a] : cur.fp[a]);
+                        // the original loop visits sd = -1 first: the partner entry does not touch acc
+                        if (bey[a]) acc = fma(mb, cur.zb[a], acc);
+#pragma unroll
+                        for (int u = 0; u < NA; ++u)
+                            if (u == t) off[u] = -mp;
+                        ++t;
+                    } else if (a == walk) {
+                        if (l + 1 < Tw) acc = fma(al * (lw < 0 ? cur.fm[a] : cur.fp[a]), prev, acc);
+                    } else if (fix_term) {                       // NA = 1: the fixed axis
+                        acc = fma(al * (lf < 0 ? cur.fm[a] : cur.fp[a]), adj, acc);
+                    }
+                }
+                rhs = acc;
+            }
+            double Mall[K][K], rall[K], u[K];
+            const int src0 = threadIdx.x & ~(K - 1);
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                rall[q] = __shfl_sync(0xffffffffu, rhs, src0 + q);
+#pragma unroll
+                for (int c = 0; c < K; ++c) Mall[q][c] = (c == q) ? 1.0 : 0.0;
+#pragma unroll
+                for (int tt = 0; tt < NA; ++tt) Mall[q][q ^ (1 << tt)] = __shfl_sync(0xffffffffu, off[tt], src0 + q);
+            }
+            if (okc) {
+                tri3t_ge<K>(Mall, rall, u, A.flag, p == 0);
+                double mine = u[0];
+#pragma unroll
+                for (int c = 1; c < K; ++c)
+                    if (c == p) mine = u[c];
+                A.z[i_lo + (l - lo_w) * istep] = mine;
+                prev = mine;
+            }
+            cur = nxt;
+        }
+        return;
+    }
     for (int d = dmax; d >= 0; --d) {
         for (int base_ln = 0; base_ln < nlines; base_ln += 32 / K) {
             int ln = base_ln + grp;
