@@ -436,6 +436,8 @@ def run_secondary(args):
     for name, pc in (("ilu0", binding.PC_ILU0), ("ssor", binding.PC_SSOR), ("none", binding.PC_NONE)):
         it, rel, ok = g.pcg_solve(pc, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
         res[f"pcg_{name}"] = it
+    # the PAPER pairing (nonsymmetric) with the flexible (Polak-Ribiere) beta it needs
+    res["pcg_ilu0_paper_pairing_flexible"], _, _ = g.pcg_solve(binding.PC_ILU0, 1.0, binding.PAIR_PAPER, 1e-8, 20000)
     w = 2.0 / (1.0 + np.sin(np.pi / (n2 + 1)))
     g.set_vector(binding.X, np.zeros((n2, n2)))
     ph, sweeps = 0, 0

@@ -180,9 +180,16 @@ sw_status sw_mg_set_cycle(sw_grid *g, int gamma);
 
 /* Preconditioned CG from x0 = 0 on the right-hand side SW_B until ||r||/||b|| < rtol
  * (recursive residual) or maxit; result in SW_X.  precond SW_PC_ILU0 factors at phase 0
- * first.  SW_ENOCONV: iters/relres still valid.  Single rank. */
+ * first.  SW_ENOCONV: iters/relres still valid.  Single rank.  beta = (r+.z+)/(r.z), or the
+ * flexible (Polak-Ribiere) beta = z+.(r+ - r)/(r.z) that the nonsymmetric PAPER pairing needs
+ * (SURVEY §8(c) C-PCG; sw_set_pcg_flexible). */
 sw_status sw_pcg_solve(sw_grid *g, sw_precond precond, double omega, sw_pairing pairing, double rtol, int maxit,
                        int *iters_out, double *relres_out, sw_stream_t s);
+
+/* Which beta sw_pcg_solve uses: -1 (default) the flexible one exactly when the preconditioner is
+ * ILU(0) or SSOR with SW_PAIR_PAPER, 0 always the standard one, 1 always the flexible one (one
+ * extra copy of r and one extra dot product per iteration).  SW_EINVAL for other modes. */
+sw_status sw_set_pcg_flexible(sw_grid *g, int mode);
 
 /* Staged preconditioner application, for drivers that run one PCG over several ranks (the
  * sw_*_apply calls above are the single-rank composition of all stages).  Stage 0 solves the

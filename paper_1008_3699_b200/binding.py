@@ -61,6 +61,7 @@ def load():
     L.sw_mg_setup.argtypes = [P_, I, I, D, I, D, I]
     L.sw_mg_apply.argtypes = [P_, P_, P_, P_]
     L.sw_mg_set_cycle.argtypes = [P_, I]
+    L.sw_set_pcg_flexible.argtypes = [P_, I]
     L.sw_precond_stages.argtypes = [P_, I]
     L.sw_precond_stages.restype = I
     L.sw_ilu_apply_stage.argtypes = [P_, I, P_, P_, I, P_]
@@ -254,6 +255,11 @@ class Grid:
         axes = bit mask of the coarsened axes (0 = all)."""
         _check(load().sw_mg_setup(self.h, int(levels), int(nu), float(theta), int(nu_coarse), float(coarse_scale),
                                   int(axes)), "sw_mg_setup")
+        return self
+
+    def set_pcg_flexible(self, mode: int):
+        """-1 auto (flexible beta with the PAPER pairing), 0 standard, 1 flexible (sw_set_pcg_flexible)."""
+        _check(load().sw_set_pcg_flexible(self.h, int(mode)), "sw_set_pcg_flexible")
         return self
 
     def mg_set_cycle(self, gamma: int):

@@ -329,6 +329,25 @@ __global__ void __launch_bounds__(RED_THREADS) k_dot_r(Rows R, const double *__r
     if (threadIdx.x == 0) partial[blockIdx.x] = sm;
 }
 
+// partial = sum z.(r - rold), the difference rounded first (the oracle's rold = r - rold, then z.rold)
+__global__ void __launch_bounds__(RED_THREADS) k_dot_diff_r(Rows R, const double *__restrict__ z,
+                                                            const double *__restrict__ r,
+                                                            const double *__restrict__ rold, DD *partial) {
+    __shared__ DD sh[RED_THREADS / 32];
+    DD acc = {0.0, 0.0};
+    for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
+        const int64_t row = it / R.segs, seg = it % R.segs;
+        const int64_t xb = seg * 2 * RSEG + threadIdx.x;
+        const int64_t base = row_base(R, row);
+        for (int h = 0; h < 2; ++h) {
+            const int64_t i = base + xb + h * RSEG;
+            if (xb + h * RSEG < R.n0) dd_add_prod(acc, z[i], __dsub_rn(r[i], rold[i]));
+        }
+    }
+    DD sm = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm;
+}
+
 // x = fma(alpha, p, x) ; r = fma(-alpha, q, r) ; partial = sum r.r
 __global__ void __launch_bounds__(RED_THREADS) k_axpy2_dot_r(Rows R, const double *alpha_dev, double *__restrict__ x,
                                                              double *__restrict__ r, const double *__restrict__ p,
@@ -432,7 +451,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_axpby_r(Rows R, double a, const
 
 // PCG scalars kept on the device
 struct CgScalars {
-    double rz, pq, alpha, beta, rr, bb, rz_new;
+    double rz, pq, alpha, beta, rr, bb, rz_new, zd;   // zd = z.(r_new - r_old) (flexible CG)
 };
 
 // sum `nparts` partials (stride `stride`, offset `off`) in fixed order into *dst = hi + lo
@@ -463,6 +482,12 @@ __global__ void k_cg_alpha(CgScalars *c) { c->alpha = c->rz / c->pq; }
 // beta = rz_new / rz ; rz = rz_new
 __global__ void k_cg_beta(CgScalars *c) {
     c->beta = c->rz_new / c->rz;
+    c->rz = c->rz_new;
+}
+
+// flexible (Polak-Ribiere) beta = z+.(r+ - r) / (r.z)
+__global__ void k_cg_beta_flex(CgScalars *c) {
+    c->beta = c->zd / c->rz;
     c->rz = c->rz_new;
 }
 

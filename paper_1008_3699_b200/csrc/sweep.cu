@@ -58,6 +58,8 @@ struct sw_grid {
     double *invD = nullptr, *R = nullptr, *Z = nullptr, *Pv = nullptr, *Q = nullptr, *Y = nullptr;
     double *W1 = nullptr, *W2 = nullptr;   // m-step preconditioner work (allocated when pc_steps > 1)
     double *Pv2 = nullptr;                 // second PCG direction buffer (fused direction update + SpMV)
+    double *Rold = nullptr;                // flexible PCG: r before the update
+    int pcg_flexible = -1;                 // sw_set_pcg_flexible: -1 auto (PAPER pairing), 0, 1
     int pc_steps = 1;                      // sw_set_precond_steps
     double pc_theta = 1.0;
     double zscale = 1.0;                   // power-of-two scale folded into the solves' coef (multigrid)
@@ -138,7 +140,7 @@ static void free_all(sw_grid *g) {
     g->mg.clear();
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
                        &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2,
-                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY};
+                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY, &g->Rold};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->hcg) cudaFreeHost(g->hcg);
@@ -893,6 +895,13 @@ extern "C" sw_status sw_mg_apply(sw_grid *g, const double *r_dev, double *z_dev,
     return st;
 }
 
+extern "C" sw_status sw_set_pcg_flexible(sw_grid *g, int mode) {
+    if (!g) return fail(SW_EINVAL, "null grid");
+    if (mode < -1 || mode > 1) return fail(SW_EINVAL, "flexible mode must be -1, 0 or 1");
+    g->pcg_flexible = mode;
+    return SW_OK;
+}
+
 extern "C" sw_status sw_mg_set_cycle(sw_grid *g, int gamma) {
     if (!g) return fail(SW_EINVAL, "null grid");
     if (gamma != 1 && gamma != 2) return fail(SW_EINVAL, "cycle index must be 1 (V) or 2 (W)");
@@ -964,6 +973,10 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
     const bool fc = !G.poisson;
     if ((st = alloc_arr(g, &g->Pv2)) != SW_OK) return st;
+    // Polak-Ribiere beta (the oracle's flexible CG): needed for the nonsymmetric PAPER pairing
+    const bool flex = g->pcg_flexible == 1 ||
+                      (g->pcg_flexible < 0 && pairing == SW_PAIR_PAPER && (pc == SW_PC_ILU0 || pc == SW_PC_SSOR));
+    if (flex && (st = alloc_arr(g, &g->Rold)) != SW_OK) return st;
     double *pcur = g->Pv, *pprev = g->Pv2;     // current direction, and the buffer of the other one
     // q = A p (first iteration) or, fused, p' = z + beta p, q = A p'
     auto spmv = [&](bool fused) {
@@ -1012,6 +1025,7 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         if (t != SW_OK) return t;
         k_cg_alpha<<<1, 1, 0, ws>>>(g->cg);
         g->launches++;
+        if (flex) CK(cudaMemcpyAsync(g->Rold, g->R, sizeof(double) * (size_t)g->nelem, cudaMemcpyDeviceToDevice, ws));
         k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, pcur, g->Q, g->partial);
         g->launches++;
         if ((t = finish(g, nr, 1, 0, &g->cg->rr, ws)) != SW_OK) return t;
@@ -1025,7 +1039,14 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         k_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, g->R, z, g->partial);
         g->launches++;
         if ((t = finish(g, nr, 1, 0, &g->cg->rz_new, ws)) != SW_OK) return t;
-        k_cg_beta<<<1, 1, 0, ws>>>(g->cg);
+        if (flex) {
+            k_dot_diff_r<<<nr, RED_THREADS, 0, ws>>>(RW, z, g->R, g->Rold, g->partial);
+            g->launches++;
+            if ((t = finish(g, nr, 1, 0, &g->cg->zd, ws)) != SW_OK) return t;
+            k_cg_beta_flex<<<1, 1, 0, ws>>>(g->cg);
+        } else {
+            k_cg_beta<<<1, 1, 0, ws>>>(g->cg);
+        }
         g->launches++;
         CK(cudaGetLastError());
         return SW_OK;

@@ -150,3 +150,34 @@ def test_pcg_iterations_match_oracle(gpu_lib, n, tile, var, pc):
     assert abs(it - ito) <= 1, (it, ito)
     x = g.get_vector(gpu_lib.X)
     assert O.relres(pb, x, b) < 2e-8
+
+
+@pytest.mark.parametrize("n,tile,var,pc,pairing,mode", [
+    ((64, 64), (16, 16), False, 2, 1, -1),          # PAPER pairing: flexible beta chosen automatically
+    ((64, 64), (16, 16), True, 1, 1, -1),
+    ((16, 16, 16), (8, 8, 8), True, 2, 1, -1),
+    ((32, 16, 8), (16, 8, 4), True, 2, 1, -1),
+    ((64, 64), (16, 16), True, 2, 0, 1),            # flexible beta forced with the SYMMETRIC pairing
+])
+def test_flexible_pcg_matches_oracle(gpu_lib, n, tile, var, pc, pairing, mode):
+    """Flexible (Polak-Ribiere) PCG, which the nonsymmetric PAPER pairing needs (SURVEY §8(c)
+    C-PCG): iteration count within 1 of the oracle's or_pcg(flexible=1), solution to 2e-8."""
+    faces = None
+    if var:
+        ring = tuple(v + 2 for v in reversed(n))
+        faces = O.faces_from_k(n, gen.lognormal_k(0, ring, 1.0))
+    pb = O.tiled(n, tile, faces=faces)
+    g = make_grid(gpu_lib, n, tile, faces).set_pcg_flexible(mode)
+    b = gen.uniform_field(0, gen.STREAM_RHS, pb.shape) / float((n[0] + 1) ** 2)
+    g.set_vector(gpu_lib.B, b)
+    it, rel, ok = g.pcg_solve(pc, 1.0, pairing, 1e-8, 5000)
+    xo, ito, relo, oko = O.pcg(pb, b, precond=pc, omega=1.0, pairing=pairing, flexible=True, rtol=1e-8, maxit=5000)
+    assert ok and oko
+    assert abs(it - ito) <= 1, (it, ito)
+    assert O.relres(pb, g.get_vector(gpu_lib.X), b) < 2e-8
+
+
+def test_pcg_flexible_mode_validation(gpu_lib):
+    g = make_grid(gpu_lib, (64, 64), (16, 16))
+    with pytest.raises(gpu_lib.SweepError):
+        g.set_pcg_flexible(2)
