@@ -138,11 +138,13 @@ class DistComm:
 
 
 def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol: float = 1e-8,
-              maxit: int = 10000, msteps: int = 1, theta: float = 0.5):
+              maxit: int = 10000, msteps: int = 1, theta: float = 0.5, flexible=None):
     """Preconditioned CG from x0 = 0 on the right-hand side SW_B of every slab grid of `comm`
     (same algorithm and stop test as sw_pcg_solve).  msteps > 1 applies the m-step form of the
     preconditioner (sw_set_precond_steps: z_{j+1} = z_j + P^-1 (r - theta A z_j)) through the
-    staged solves, sw_apply_A and sw_axpby.  Returns (iterations, relres, converged)."""
+    staged solves, sw_apply_A and sw_axpby.  flexible: the Polak-Ribiere beta z+.(r+ - r)/(r.z)
+    (None: exactly when the preconditioner is ILU(0) or SSOR with the PAPER pairing, as
+    sw_pcg_solve).  Returns (iterations, relres, converged)."""
     import torch
 
     from . import binding as B
@@ -152,6 +154,11 @@ def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol
     V = {w: [g.view(w) for g in grids] for w in vecs}
     ptr = {w: [t.data_ptr() for t in V[w]] for w in V}
     dd = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in grids]
+    if flexible is None:
+        flexible = pairing == B.PAIR_PAPER and precond in (B.PC_ILU0, B.PC_SSOR)
+    if flexible:                             # r before its update, and r+ - r
+        rold = [torch.empty_like(t) for t in V[B.R]]
+        rdif = [torch.empty_like(t) for t in V[B.R]]
 
     def reduce(fn):
         for i, g in enumerate(grids):
@@ -206,6 +213,9 @@ def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol
         comm.exchange(V[B.P], 1)
         pq = reduce(lambda i, g: g.apply_A(ptr[B.P][i], ptr[B.Q][i], dd[i].data_ptr()))
         alpha = rz / pq
+        if flexible:
+            for i in range(len(grids)):
+                rold[i].copy_(V[B.R][i])
         rr = reduce(lambda i, g: g.axpy2(alpha, ptr[B.X][i], ptr[B.R][i], ptr[B.P][i], ptr[B.Q][i],
                                          dd[i].data_ptr()))
         relres = rr ** 0.5 / bnorm
@@ -217,7 +227,12 @@ def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol
             raise FloatingPointError("PCG produced NaN")
         apply_pc()
         rzn = reduce(lambda i, g: g.dot(ptr[B.R][i], ptr[z][i], dd[i].data_ptr()))
-        beta = rzn / rz
+        if flexible:                         # (r+ - r) rounded first, then z.(r+ - r), as the oracle
+            for i, g in enumerate(grids):
+                g.axpby(1.0, ptr[B.R][i], -1.0, rold[i].data_ptr(), rdif[i].data_ptr())
+            beta = reduce(lambda i, g: g.dot(ptr[z][i], rdif[i].data_ptr(), dd[i].data_ptr())) / rz
+        else:
+            beta = rzn / rz
         rz = rzn
         for i, g in enumerate(grids):
             g.xpby(ptr[z][i], beta, ptr[B.P][i])

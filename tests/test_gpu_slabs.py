@@ -167,3 +167,27 @@ def test_msteps_pcg_over_slabs_matches_single_grid(n, tile, nranks, var, pc):
     assert ok and ok1
     assert abs(it - it1) <= 1, (it, it1)
     assert O.relres(pb, gather(sl, B.X), b) < 2e-8
+
+
+@pytest.mark.parametrize("n,tile,nranks,var,pc", [((128, 128), (32, 32), 2, True, B.PC_ILU0),
+                                                  ((32, 16, 16), (16, 8, 4), 2, True, B.PC_ILU0),
+                                                  ((128, 128), (32, 32), 4, False, B.PC_SSOR)])
+def test_flexible_pcg_over_slabs_matches_oracle(n, tile, nranks, var, pc):
+    """The PAPER pairing over slabs: flexible (Polak-Ribiere) CG chosen automatically, iteration
+    count within 1 of the single-grid sw_pcg_solve and of the oracle's flexible or_pcg."""
+    faces = None
+    if var:
+        ring = tuple(v + 2 for v in reversed(n))
+        faces = O.faces_from_k(n, gen.lognormal_k(0, ring, 1.0))
+    pb = O.tiled(n, tile, faces=faces)
+    b = gen.uniform_field(0, gen.STREAM_RHS, pb.shape) / float((n[0] + 1) ** 2)
+    one = make_grid(B, n, tile, faces)
+    one.set_vector(B.B, b)
+    it1, rel1, ok1 = one.pcg_solve(pc, 1.0, B.PAIR_PAPER, 1e-8, 5000)
+    _, ito, _, oko = O.pcg(pb, b, precond=pc, omega=1.0, pairing=1, flexible=True, rtol=1e-8, maxit=5000)
+    sl = make_slabs(n, tile, nranks, faces)
+    scatter(sl, B.B, b)
+    it, rel, ok = parallel.pcg_slabs(parallel.LocalComm(sl), pc, 1.0, B.PAIR_PAPER, 1e-8, 5000)
+    assert ok and ok1 and oko
+    assert abs(it - it1) <= 1 and abs(it - ito) <= 1, (it, it1, ito)
+    assert O.relres(pb, gather(sl, B.X), b) < 2e-8
