@@ -225,8 +225,17 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
     }
     const int T0 = G.T[0], T1 = G.T[1], T2 = G.T[2];
     const int tmax = T0 > T1 ? (T0 > T2 ? T0 : T2) : (T1 > T2 ? T1 : T2);
+    // Every set is shared by the 2 / 4 / 8 boxes whose start corners meet at it, and each of them
+    // would compute it (bitwise the same values: the rows use global indices only).  On one rank
+    // only the box with the lowest index along every set axis does (it starts at the high end of
+    // each: s = 1); over slabs every box still computes its sets, because a set across the slab
+    // boundary must be written on both ranks.
+    const bool single = G.nt[2] == G.ntg[2];
+    int own[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) own[a] = cpl[a] && (!single || s[a] == 1);
     if (NA == 3) {                                   // the corner set: one lane
-        if (threadIdx.x == 0 && cpl[0] && cpl[1] && cpl[2]) {
+        if (threadIdx.x == 0 && own[0] && own[1] && own[2]) {
             int64_t gl[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
     constexpr int K = 1 << NA;
     const int p = threadIdx.x & (K - 1);
     const int grp = threadIdx.x / K;                    // 16 sheet lines / 8 edge groups per pass
-    const int n0 = cpl[0] ? T2 : 0, n1 = cpl[1] ? T2 : 0, n2 = cpl[2] ? T1 : 0;
+    const int n0 = own[0] ? T2 : 0, n1 = own[1] ? T2 : 0, n2 = own[2] ? T1 : 0;
     const int nlines = NA == 1 ? n0 + n1 + n2 : 3;
     const int dmax = NA == 2 ? tmax - 1 : T0 - 1 + (T1 > T2 ? T1 : T2) - 1;
     // geometry of line `ln` at step d: active?, rank-0 corner gl of the set, set axes, and the
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
             else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
             else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
         } else {
-            if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; fixax = -1; }
+            if (ln < 3 && own[(ln + 1) % 3] && own[(ln + 2) % 3]) { fa = ln; walk = ln; fixax = -1; }
         }
         ok = fa >= 0;
         int l[3] = {0, 0, 0};
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
                 if (l_ln < n0) { fa = 0; fixv = l_ln; }
                 else if ((l_ln -= n0) < n1) { fa = 1; fixv = l_ln; }
                 else if ((l_ln -= n1) < n2) { fa = 2; fixv = l_ln; }
-            } else if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) {
+            } else if (ln < 3 && own[(ln + 1) % 3] && own[(ln + 2) % 3]) {
                 fa = ln;
             }
             act = fa >= 0;
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
                 else if ((ln -= n0) < n1) { fa = 1; fixax = 2; fixv = ln; walk = 0; }
                 else if ((ln -= n1) < n2) { fa = 2; fixax = 1; fixv = ln; walk = 0; }
             } else {
-                if (ln < 3 && cpl[(ln + 1) % 3] && cpl[(ln + 2) % 3]) { fa = ln; walk = ln; }
+                if (ln < 3 && own[(ln + 1) % 3] && own[(ln + 2) % 3]) { fa = ln; walk = ln; }
             }
             bool ok = fa >= 0;
             int l[3] = {0, 0, 0};
