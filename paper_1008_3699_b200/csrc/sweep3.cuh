@@ -380,6 +380,12 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
                 const int o = o_[kb];
+                if (!on[kb]) {                        // layer across an uncoupled face: never read
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) f[kb][a][0] = f[kb][a][1] = xn[kb][a] = 0.0;
+                    xo[kb] = av[kb] = 0.0;
+                    continue;
+                }
                 if (FACES) {
                     f[kb][0][0] = __ldg(f0b + o); f[kb][0][1] = __ldg(f0b + o + 1);
                     f[kb][1][0] = __ldg(f1b + o); f[kb][1][1] = __ldg(f1b + o + P0i);
