@@ -284,6 +284,9 @@ __device__ __forceinline__ void edge_chain(double *X, int WS, int lane, int T, i
 }
 
 
+#ifndef SW_KB
+#define SW_KB 2
+#endif
 template <bool FACES, int SHAPE>
 __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     extern __shared__ __align__(128) double sm[];
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         const int NE = E0 * E1 * E2;
         int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
         const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
-        constexpr int KB = 3;      // nodes per batch: all their loads are issued before any use
+        constexpr int KB = SW_KB;      // nodes per batch: all their loads are issued before any use
         for (int e0 = tid; e0 < NE; e0 += KB * k3::NT) {
             int cw_[KB], Lm[KB], o_[KB], mz[KB];
             bool on[KB];
