@@ -374,13 +374,13 @@ def run_secondary(args):
     out["c3_pcg_ilu0"] = {"iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
                           "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
     # multigrid-preconditioned CG with the decomposed sweep as smoother
-    g.mg_setup(7, 1, 0.5, 16, 1.8)                  # 7 levels: coarsest 64^2 = one box
+    g.mg_setup(7, 1, 0.45, 32, 1.8)                 # 7 levels: coarsest 64^2 = one box
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     it, rel, ok = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 20000)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    out["c3_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.5, "nu_coarse": 16, "coarse_scale": 1.8, "iterations": it,
+    out["c3_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.45, "nu_coarse": 32, "coarse_scale": 1.8, "iterations": it,
                         "relres": rel, "converged": ok, "seconds": round(dt, 3),
                         "ms_per_iteration": round(dt / max(it, 1) * 1e3, 4)}
     del g, b
@@ -405,13 +405,13 @@ def run_secondary(args):
         dt = time.perf_counter() - t0
         out["c5_pcg_ilu0"] = {"n": [n3] * 3, "tile": [32, 8, 4], "iterations": it, "relres": rel, "converged": ok,
                               "seconds": round(dt, 3), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
-        g.mg_setup(7, 1, 0.5, 16, 1.2, 3)           # semi-coarsening in x and y (alpha_z = 0.01)
+        g.mg_setup(7, 1, 0.35, 16, 1.0, 3)          # semi-coarsening in x and y (alpha_z = 0.01)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         it, rel, ok = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 5000)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        out["c5_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.5, "nu_coarse": 16, "coarse_scale": 1.2,
+        out["c5_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.35, "nu_coarse": 16, "coarse_scale": 1.0,
                             "coarsened_axes": "x, y",
                             "iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
                             "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
