@@ -405,14 +405,15 @@ def run_secondary(args):
         dt = time.perf_counter() - t0
         out["c5_pcg_ilu0"] = {"n": [n3] * 3, "tile": [32, 8, 4], "iterations": it, "relres": rel, "converged": ok,
                               "seconds": round(dt, 3), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
-        g.mg_setup(7, 1, 0.35, 16, 1.0, 3)          # semi-coarsening in x and y (alpha_z = 0.01)
+        g.mg_setup(7, 1, 0.35, 4, 1.0, 3)           # semi-coarsening in x and y (alpha_z = 0.01)
+        g.mg_set_cycle(2)                           # W-cycle
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         it, rel, ok = g.pcg_solve(binding.PC_MG, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 5000)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        out["c5_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.35, "nu_coarse": 16, "coarse_scale": 1.0,
-                            "coarsened_axes": "x, y",
+        out["c5_pcg_mg"] = {"levels": 7, "nu": 1, "theta": 0.35, "nu_coarse": 4, "coarse_scale": 1.0,
+                            "coarsened_axes": "x, y", "cycle": "W",
                             "iterations": it, "relres": rel, "converged": ok, "seconds": round(dt, 3),
                             "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
     del g
