@@ -292,6 +292,81 @@ __global__ void __launch_bounds__(RED_THREADS) k_pspmv_dot_r(Rows R, double beta
     if (threadIdx.x == 0) partial[blockIdx.x] = sm;
 }
 
+// 3D form of k_pspmv_dot_r that marches z: a block owns 32 x 8 columns, keeps p_new of the planes
+// z-1, z, z+1 in registers and the x / y neighbours of plane z in shared memory, so every value of
+// p_old, z and the faces is read from DRAM once and p_new = z + beta p_old is formed once per node
+// (the row kernel re-reads the planes z +- 1, 1.5x the algorithmic bytes).  q and p_new are the
+// same operations in the same order as k_pspmv_dot_r (bitwise equal); the per-block partial sums
+// follow the block's own (fixed) order.
+#ifndef SW_ZC
+#define SW_ZC 8
+#endif
+template <bool FACES>
+__global__ void __launch_bounds__(256) k_pspmv3_zm(Rows R, double beta_a, const double *beta_dev,
+                                                   const double *__restrict__ F0, const double *__restrict__ F1,
+                                                   const double *__restrict__ F2, const double *__restrict__ z,
+                                                   const double *__restrict__ pold, double *__restrict__ pnew,
+                                                   double *__restrict__ q, DD *partial) {
+    constexpr int TX = 32, TY = 8;
+    __shared__ double tile[2][TY + 2][TX + 2];
+    __shared__ DD sh[256 / 32];
+    const double be = *beta_dev;
+    auto P = [&](int64_t j) { return fma(be, pold[j], z[j]); };
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    constexpr int ZC = SW_ZC;                 // planes per work item (more items in flight)
+    const int64_t ntx = (R.n0 + TX - 1) / TX, nty = (R.n1 + TY - 1) / TY, n2 = R.rows / R.n1;
+    const int64_t nzc = (n2 + ZC - 1) / ZC;
+    DD acc = {0.0, 0.0};
+    for (int64_t t = blockIdx.x; t < ntx * nty * nzc; t += gridDim.x) {
+        const int64_t tc = t % (ntx * nty), z0 = (t / (ntx * nty)) * ZC;
+        const int64_t z1 = z0 + ZC < n2 ? z0 + ZC : n2;
+        const int64_t x = (tc % ntx) * TX + tx, y = (tc / ntx) * TY + ty;
+        const bool in = x < R.n0 && y < R.n1;
+        const bool hx = in && (tx == TX - 1 || x == R.n0 - 1), hy = in && (ty == TY - 1 || y == R.n1 - 1);
+        int64_t i = R.origin + (in ? y : 0) * R.P0 + (in ? x : 0) + z0 * R.P01;
+        double Pm = P(i - R.P01), Pc = P(i);
+        double f4 = FACES ? F2[i] : 1.0;
+        for (int64_t k = z0; k < z1; ++k) {
+            const int b = (int)(k & 1);
+            const double Pp = P(i + R.P01);
+            double c0 = 1.0, c1 = 1.0, c2 = 1.0, c3 = 1.0, c5 = 1.0;
+            if (FACES) { c0 = F0[i]; c1 = F0[i + 1]; c2 = F1[i]; c3 = F1[i + R.P0]; c5 = F2[i + R.P01]; }
+            if (in) {
+                tile[b][ty + 1][tx + 1] = Pc;
+                if (tx == 0) tile[b][ty + 1][0] = P(i - 1);
+                if (hx) tile[b][ty + 1][tx + 2] = P(i + 1);
+                if (ty == 0) tile[b][0][tx + 1] = P(i - R.P0);
+                if (hy) tile[b][ty + 2][tx + 1] = P(i + R.P0);
+            }
+            __syncthreads();
+            if (in) {
+                const double c4 = f4;
+                double ap = c0 + c1;
+                ap = ap + (c2 + c3);
+                ap = ap + (c4 + c5);
+                ap = ap + beta_a;
+                double v = ap * Pc;
+                v = fma(-c0, tile[b][ty + 1][tx], v);
+                v = fma(-c1, tile[b][ty + 1][tx + 2], v);
+                v = fma(-c2, tile[b][ty][tx + 1], v);
+                v = fma(-c3, tile[b][ty + 2][tx + 1], v);
+                v = fma(-c4, Pm, v);
+                v = fma(-c5, Pp, v);
+                pnew[i] = Pc;
+                q[i] = v;
+                dd_add_prod(acc, Pc, v);
+            }
+            Pm = Pc;
+            Pc = Pp;
+            f4 = c5;
+            i += R.P01;
+        }
+        __syncthreads();                      // the next tile reuses the buffers
+    }
+    DD sm = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm;
+}
+
 // out = r - A x (interior nodes): the residual of a multigrid level in one pass (the same values as
 // k_spmv_dot_r followed by k_sub_r with theta = 1)
 template <int DIM, bool FACES>

@@ -994,8 +994,8 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
                                 : k_pspmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
             else if (g->dim == 2) fc ? k_pspmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
                                      : k_pspmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
-            else fc ? k_pspmv_dot_r<3, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
-                    : k_pspmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            else fc ? k_pspmv3_zm<true><<<nr, 256, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                    : k_pspmv3_zm<false><<<nr, 256, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
         }
         g->launches++;
     };
