@@ -153,7 +153,11 @@ class Grid:
 
     # -------------------------------------------------------------- vectors
     def set_vector(self, which: int, src, stream=None):
-        """src: local-slab interior values (numpy array, or torch tensor on host/device)."""
+        """src: local-slab interior values (numpy array, or torch tensor on host/device).
+
+        numpy arrays are copied synchronously.  torch tensors are copied stream-ordered on
+        `stream` and the call returns at once (so uploads can overlap other work): a host
+        tensor must stay unchanged until that stream has passed the copy."""
         try:
             import torch
             if isinstance(src, torch.Tensor):
@@ -170,6 +174,10 @@ class Grid:
         self.sync(stream)
 
     def get_vector(self, which: int, out=None, stream=None):
+        """Local-slab interior values into `out` (a new numpy array if None).
+
+        numpy: synchronous.  torch tensor: stream-ordered on `stream`, returns at once; for a
+        host (e.g. pinned) tensor synchronise that stream before reading it."""
         if out is None:
             out = np.empty(self.local_shape)
         try:

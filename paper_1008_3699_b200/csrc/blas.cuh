@@ -11,7 +11,18 @@
 namespace sw {
 
 constexpr int RED_THREADS = 256;
-constexpr int RED_BLOCKS = 1184;   // 8 x 148 SMs
+// Grid size of the row-segment / reduction kernels: 8 CTAs per SM of the current device (1184 on
+// a 148-SM B200), queried once per process, so every reduction of a run has one fixed order.
+inline int red_blocks() {
+    static const int v = [] {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+            sms = 148;
+        return 8 * sms;
+    }();
+    return v;
+}
 
 // Accurate reductions: every dot product is accumulated in double-double (TwoProd by fma,
 // TwoSum), per thread, then per CTA in fixed warp-shuffle order, then across CTAs in CTA

@@ -12,8 +12,9 @@
 // count.  All values live in global memory; a box also writes the partner values it
 // computes (identical bits to what the owner writes).
 //
-// This is the general path (1D, 3D, ILU/SSOR).  The 2D SOR sweep has a specialised
-// register-wavefront kernel in sweep2d.cuh.
+// This is the general path (1D, box shapes outside the specialised engines, the ILU(0)
+// factor).  2D 64 x 64 boxes run on sweep2p.cuh / sweep2v.cuh / tri2t.cuh, 3D on
+// sweep3.cuh / tri3t.cuh.
 #pragma once
 #include "common.cuh"
 

@@ -1,7 +1,7 @@
 // sweep.cu -- host runtime of the C ABI (include/sweep.h): grid/slab geometry, device
 // memory, kernel dispatch for the decomposed SOR sweep, D-ILU(0)/SSOR application and
-// the PCG driver.  Kernels: generic.cuh (all dims/modes), sweep2d.cuh (fast 2D SOR),
-// blas.cuh (PCG vector work).
+// the PCG driver.  Kernels: generic.cuh (all dims/modes), sweep2p.cuh / sweep2v.cuh / tri2t.cuh
+// (2D 64 x 64 engine), sweep3.cuh / tri3t.cuh (3D engine), blas.cuh (PCG vector work), mg.cuh.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -14,14 +14,13 @@
 #include "../../include/sweep.h"
 #include "blas.cuh"
 #include "generic.cuh"
-#include "sweep2d.cuh"
+#include "maps2d.cuh"
 #include "sweep2p.cuh"
 #include "sweep2v.cuh"
 #include "tri2t.cuh"
 #include "sweep3.cuh"
 #include "tri3t.cuh"
 #include "mg.cuh"
-#include <vector>
 
 using namespace sw;
 
@@ -90,18 +89,23 @@ struct sw_grid {
     std::deque<MapEntry> mapcache;    // TMA descriptors of arrays used as solve inputs (stable references)
 };
 
-// TMA descriptor (box x box window at the padded origin) of a padded array, cached by pointer
-static const CUtensorMap *get_map(sw_grid *g, const double *ptr, int box) {
+// TMA descriptor (box x box window at the padded origin) of a padded array, cached by pointer.
+// Copied out by value: a later lookup may evict the cache entry.
+static bool get_map(sw_grid *g, const double *ptr, int box, CUtensorMap *out) {
     for (auto &e : g->mapcache)
-        if (e.ptr == ptr && e.box == box) return &e.map;
+        if (e.ptr == ptr && e.box == box) {
+            *out = e.map;
+            return true;
+        }
     sw_grid::MapEntry e;
     e.ptr = ptr;
     e.box = box;
     const bool ok = g->dim == 2 && encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box);
-    if (!ok) return nullptr;
-    if (g->mapcache.size() > 32) g->mapcache.pop_front();   // never one of the (<= 3) maps of the current call
+    if (!ok) return false;
+    if (g->mapcache.size() >= 32) g->mapcache.pop_front();
     g->mapcache.push_back(e);
-    return &g->mapcache.back().map;
+    *out = e.map;
+    return true;
 }
 
 extern "C" const char *sw_last_error(void) { return g_err.c_str(); }
@@ -126,9 +130,8 @@ extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, d
     g->kind = kind;
     g->beta = beta;
     g->dev = cuda_device;
-    const char *env = getenv("SW_DISABLE_FAST2D");   // 1: generic kernel only; 2: v1 2D kernel for faces
+    const char *env = getenv("SW_DISABLE_FAST2D");   // 1: the level-synchronous generic kernel only
     if (env && env[0] == '1') g->fast2d = 0;
-    if (env && env[0] == '2') g->fast2d = 2;
     *out = g;
     return SW_OK;
 }
@@ -223,7 +226,7 @@ extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int n
     if (!G.poisson)
         for (int a = 0; a < d; ++a)
             if ((st = alloc_arr(g, &g->F[a])) != SW_OK) { free_all(g); return st; }
-    if (cudaMalloc(&g->partial, sizeof(DD) * 2 * RED_BLOCKS) != cudaSuccess ||
+    if (cudaMalloc(&g->partial, sizeof(DD) * 2 * red_blocks()) != cudaSuccess ||
         cudaMalloc(&g->cg, sizeof(CgScalars)) != cudaSuccess || cudaMalloc(&g->flag, sizeof(int)) != cudaSuccess) {
         free_all(g);
         return fail(SW_ENOMEM, "cudaMalloc of scratch failed");
@@ -371,7 +374,7 @@ extern "C" sw_status sw_set_faces(sw_grid *g, const double *const face_host[3], 
 
 static int grid_blocks(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;
-    if (b > RED_BLOCKS) b = RED_BLOCKS;
+    if (b > red_blocks()) b = red_blocks();
     if (b < 1) b = 1;
     return (int)b;
 }
@@ -463,7 +466,7 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             cudaError_t e = launch_sweep2p(g->maps.x[g->cur], g->maps.b, g->G, base, w8, g->B, xn, g->flag, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2p launch: ") + cudaGetErrorString(e));
-        } else if (g->dim == 2 && g->fast2d && g->maps.ok && g->maps.fok && g->fast2d != 2) {
+        } else if (g->dim == 2 && g->fast2d && g->maps.ok && g->maps.fok) {
             cudaError_t e = launch_sweep2v(g->maps.x[g->cur], g->maps.b, g->maps.f[0], g->maps.f[1], g->G, base, w8,
                                            g->B, g->F[0], g->F[1], xn, g->flag, cs);
             g->launches++;
@@ -484,10 +487,6 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
             cudaError_t e = launch_sweep3(A3, cs);
             g->launches++;
             if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
-        } else if (g->dim == 2 && g->fast2d && g->maps.ok) {
-            cudaError_t e = launch_sweep2d(g->maps, g->cur, g->G, base, w8, g->B, g->F, xn, g->flag, !g->G.poisson, cs);
-            g->launches++;
-            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2d launch: ") + cudaGetErrorString(e));
         } else {
             KParams P = base_params(g);
             P.mode = M_FWD;
@@ -600,14 +599,14 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
         const double *fx = g->G.poisson ? nullptr : g->F[0], *fy = g->G.poisson ? nullptr : g->F[1];
         const CUtensorMap &mfx = g->G.poisson ? g->maps.b : g->maps.f[0];
         const CUtensorMap &mfy = g->G.poisson ? g->maps.b : g->maps.f[1];
-        const CUtensorMap *maux = get_map(g, g->invD, T2);
-        const CUtensorMap *msrc = get_map(g, stage == 0 ? r : g->Y, WW);
-        if (!msrc || !maux) return fail(SW_ECUDA, "cuTensorMapEncodeTiled failed");
+        CUtensorMap maux, msrc;
+        if (!get_map(g, g->invD, T2, &maux) || !get_map(g, stage == 0 ? r : g->Y, WW, &msrc))
+            return fail(SW_ECUDA, "cuTensorMapEncodeTiled failed");
         cudaError_t e;
         if (stage == 0)
-            e = launch_tri2v(*msrc, *maux, mfx, mfy, g->G, base, omega, invd, fx, fy, true, 1.0, true, g->Y, g->flag, s);
+            e = launch_tri2v(msrc, maux, mfx, mfy, g->G, base, omega, invd, fx, fy, true, 1.0, true, g->Y, g->flag, s);
         else if (stage == 1)
-            e = launch_tri2v(*msrc, *maux, mfx, mfy, g->G, rev, omega, invd, fx, fy, false, coef,
+            e = launch_tri2v(msrc, maux, mfx, mfy, g->G, rev, omega, invd, fx, fy, false, coef,
                              pairing == SW_PAIR_PAPER, z, g->flag, s);
         else
             e = launch_tri2t_stage(g->G, base, omega, invd, fx, fy, g->Y, z, coef, g->flag, stage - 2, s);
@@ -713,7 +712,7 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     if ((st = alloc_arr(g, &g->W1)) != SW_OK) return st;
     if ((st = alloc_arr(g, &g->W2)) != SW_OK) return st;
     const Rows RW = make_rows(g->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     for (int j = 1; j < g->pc_steps; ++j) {
         if ((st = spmv_launch(g, RW, nr, z, g->W1, s, 0)) != SW_OK) return st;   // W1 = A z
         // W2 = r - theta A z (with zscale = theta folded in, z is already theta times the iterate)
@@ -728,6 +727,8 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
 }
 
 // ---------------------------------------------------------------- geometric multigrid (N1)
+static sw_status mg_build(sw_grid *g, int levels, int axes);
+
 extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale,
                                  int axes) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
@@ -737,6 +738,15 @@ extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, i
         return fail(SW_EINVAL, "bad multigrid parameters");
     if (axes == 0) axes = (1 << g->dim) - 1;
     if (axes < 0 || axes >= (1 << g->dim)) return fail(SW_EINVAL, "bad multigrid axes mask");
+    {   // every level to be coarsened must have an even count: check before building anything
+        int64_t m[3] = {g->ng[0], g->ng[1], g->ng[2]};
+        for (int l = 1; l < levels; ++l)
+            for (int a = 0; a < g->dim; ++a)
+                if ((axes >> a) & 1) {
+                    if (m[a] % 2) return fail(SW_EINVAL, "every level must have an even node count per axis");
+                    m[a] /= 2;
+                }
+    }
     g->mg_scale = coarse_scale;
     g->mg_axes = axes;
     for (sw_grid *c : g->mg) sw_destroy(c);
@@ -744,6 +754,15 @@ extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, i
     g->mg_nu = nu;
     g->mg_theta = theta;
     g->mg_nu_coarse = nu_coarse;
+    sw_status st = mg_build(g, levels, axes);
+    if (st != SW_OK) {                          // no half-built hierarchy survives a failure
+        for (sw_grid *c : g->mg) sw_destroy(c);
+        g->mg.clear();
+    }
+    return st;
+}
+
+static sw_status mg_build(sw_grid *g, int levels, int axes) {
     sw_status st;
     if ((st = ensure_work(g)) != SW_OK) return st;
     const double *const *src_faces = g->G.poisson ? nullptr : g->F;
@@ -753,7 +772,6 @@ extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, i
         int tc[3] = {1, 1, 1};
         for (int a = 0; a < g->dim; ++a) {
             const bool co = (axes >> a) & 1;
-            if (co && fine->ng[a] % 2) return fail(SW_EINVAL, "every level must have an even node count per axis");
             nc[a] = co ? fine->ng[a] / 2 : fine->ng[a];
             tc[a] = fine->tile[a] <= nc[a] ? fine->tile[a] : (int)nc[a];
             while (nc[a] % tc[a]) --tc[a];
@@ -805,7 +823,7 @@ static sw_status mg_smooth(sw_grid *l, const double *r, double *x, int m, double
     l->pc_theta = keep_t;
     if (st != SW_OK || pow2) return st;
     const Rows RW = make_rows(l->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     k_scale_r<<<nr, RED_THREADS, 0, s>>>(RW, theta, x);
     l->launches++;
     CK(cudaGetLastError());
@@ -814,7 +832,7 @@ static sw_status mg_smooth(sw_grid *l, const double *r, double *x, int m, double
 
 static sw_status mg_residual(sw_grid *l, const double *r, const double *x, double *out, cudaStream_t s) {
     const Rows RW = make_rows(l->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     const double *F0 = l->F[0], *F1 = l->F[1], *F2 = l->F[2];
     const bool fc = !l->G.poisson;
     const double bt = l->G.beta;
@@ -862,7 +880,7 @@ static sw_status mg_vcycle(sw_grid *g, int lev, const double *r, double *x, cuda
         if ((st = mg_residual(c, c->MGR, c->MGX, c->MGW, s)) != SW_OK) return st;         // MGW = r_c - A_c x_c
         if ((st = mg_vcycle(g, lev + 1, c->MGW, c->MGY, s)) != SW_OK) return st;
         const Rows RC = make_rows(c->G);
-        const int nrc = (int)std::min<int64_t>(RC.items, RED_BLOCKS);
+        const int nrc = (int)std::min<int64_t>(RC.items, red_blocks());
         k_addto_r<<<nrc, RED_THREADS, 0, s>>>(RC, c->MGX, c->MGY);
         c->launches++;
         CK(cudaGetLastError());
@@ -875,7 +893,7 @@ static sw_status mg_vcycle(sw_grid *g, int lev, const double *r, double *x, cuda
     if ((st = mg_residual(l, r, x, l->MT2, s)) != SW_OK) return st;                      // MT2 = r - A x
     if ((st = mg_smooth(l, l->MT2, l->MT1, g->mg_nu, g->mg_theta, s)) != SW_OK) return st;   // post-smoothing
     const Rows RW = make_rows(l->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     k_addto_r<<<nr, RED_THREADS, 0, s>>>(RW, x, l->MT1);
     l->launches++;
     CK(cudaGetLastError());
@@ -970,7 +988,7 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     };
     // row-segment kernels, launch shape fixed per grid (deterministic reductions)
     const Rows RW = make_rows(G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     const bool fc = !G.poisson;
     if ((st = alloc_arr(g, &g->Pv2)) != SW_OK) return st;
     // Polak-Ribiere beta (the oracle's flexible CG): needed for the nonsymmetric PAPER pairing
@@ -1056,16 +1074,21 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     // multigrid preconditioner): one launch and one synchronisation per iteration.  The direction
     // buffers alternate, so there is one graph per parity.
     static const bool no_graph = getenv("SW_NO_GRAPH") != nullptr;
-    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    struct GraphPair {                          // destroyed on every exit path
+        cudaGraphExec_t e[2] = {nullptr, nullptr};
+        void reset() {
+            for (auto &x : e)
+                if (x) {
+                    cudaGraphExecDestroy(x);
+                    x = nullptr;
+                }
+        }
+        ~GraphPair() { reset(); }
+    } graphs;
+    cudaGraphExec_t *exec = graphs.e;
     int64_t graph_launches = 0;
     bool graph_ok = !no_graph;
-    auto cleanup = [&]() {
-        for (auto &e : exec)
-            if (e) {
-                cudaGraphExecDestroy(e);
-                e = nullptr;
-            }
-    };
+    auto cleanup = [&]() { graphs.reset(); };
     for (int it = 1; it <= maxit; ++it) {
         const int par = it & 1;
         if (it == 1) {
@@ -1150,7 +1173,7 @@ extern "C" sw_status sw_apply_A(sw_grid *g, const double *x, double *y, double *
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (!x || !y || !dot_dd || x == y) return fail(SW_EINVAL, "bad pointers");
     const Rows RW = make_rows(g->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     sw_status st = spmv_launch(g, RW, nr, x, y, (cudaStream_t)s, 0);
     return st != SW_OK ? st : finish_dd(g, nr, dot_dd, (cudaStream_t)s);
 }
@@ -1159,7 +1182,7 @@ extern "C" sw_status sw_dot(sw_grid *g, const double *a, const double *b, double
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (!a || !b || !dot_dd) return fail(SW_EINVAL, "bad pointers");
     const Rows RW = make_rows(g->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     k_dot_r<<<nr, RED_THREADS, 0, (cudaStream_t)s>>>(RW, a, b, g->partial);
     g->launches++;
     CK(cudaGetLastError());
@@ -1172,7 +1195,7 @@ extern "C" sw_status sw_axpy2(sw_grid *g, double alpha, double *x, double *r, co
     if (!x || !r || !p || !q || !rr_dd) return fail(SW_EINVAL, "bad pointers");
     cudaStream_t cs = (cudaStream_t)s;
     const Rows RW = make_rows(g->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     k_set_scalar<<<1, 1, 0, cs>>>(&g->cg->alpha, alpha);
     k_axpy2_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->alpha, x, r, p, q, g->partial);
     g->launches += 2;
@@ -1185,7 +1208,7 @@ extern "C" sw_status sw_xpby(sw_grid *g, const double *z, double beta, double *p
     if (!z || !p || z == p) return fail(SW_EINVAL, "bad pointers");
     cudaStream_t cs = (cudaStream_t)s;
     const Rows RW = make_rows(g->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     k_set_scalar<<<1, 1, 0, cs>>>(&g->cg->beta, beta);
     k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 0, z, p);
     g->launches += 2;
@@ -1198,7 +1221,7 @@ extern "C" sw_status sw_axpby(sw_grid *g, double a, const double *x, double b, c
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (!x || !y || !out) return fail(SW_EINVAL, "bad pointers");
     const Rows RW = make_rows(g->G);
-    const int nr = (int)std::min<int64_t>(RW.items, RED_BLOCKS);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     k_axpby_r<<<nr, RED_THREADS, 0, (cudaStream_t)s>>>(RW, a, x, b, y, out);
     g->launches++;
     CK(cudaGetLastError());

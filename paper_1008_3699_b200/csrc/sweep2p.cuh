@@ -1,6 +1,5 @@
 // sweep2p.cuh -- 2D decomposed SOR sweep, constant coefficients (Poisson), 64 x 64 boxes,
-// sm_100a.  Version 2 of the 2D kernel (the v1 kernel in sweep2d.cuh still serves the
-// variable-coefficient case).
+// sm_100a (sweep2v.cuh is the variable-coefficient counterpart).
 //
 // One CTA = two warps = one box.  Six CTAs fit on an SM (36 KB of shared
 // memory each), so 12 warps share the latency of the staged loads.  Per box:

@@ -30,7 +30,7 @@ CASES = [
     ((130, 66), (26, 22), False, 0.0, [1.5]),                       # ragged tiles, 5x3 boxes
     ((64, 64), (64, 64), True, 0.0, [1.2]),                         # one box
     ((1024,), (256,), False, 0.0, [2 / (1 + np.sin(np.pi / 1025))]),  # config 1
-    ((100,), (7,) if False else (10,), True, 0.05, [0.9, 1.4]),
+    ((100,), (10,), True, 0.05, [0.9, 1.4]),                         # 1D faces, per-direction omega
     ((32, 32, 32), (16, 8, 8), True, 0.0, [1.0]),                   # 3D, boxes long in x
     ((24, 16, 16), (8, 8, 8), False, 0.0, [1.3]),
     ((12, 12, 12), (4, 6, 3), True, 0.2, list(0.6 + 0.15 * np.arange(8))),
@@ -134,7 +134,11 @@ def test_ilu_and_ssor_apply_match_oracle(gpu_lib, n, tile, var, beta):
 @pytest.mark.parametrize("n,tile,var,pc", [((64, 64), (16, 16), False, 2), ((256, 256), (64, 64), False, 2),
                                            ((256, 256), (64, 64), True, 2), ((128, 128), (32, 32), True, 1),
                                            ((16, 16, 16), (8, 8, 8), True, 2), ((128, 64), (32, 32), False, 0),
-                                           ((192, 256), (64, 64), True, 1), ((256, 128), (64, 64), False, 1)])
+                                           ((192, 256), (64, 64), True, 1), ((256, 128), (64, 64), False, 1),
+                                           # 3D ragged for the z-marching fused update + SpMV (k_pspmv3_zm): n1 not
+                                           # a multiple of its 8-row tile, n2 not a multiple of its 8-plane chunk
+                                           ((24, 12, 10), (8, 6, 5), False, 2), ((24, 12, 10), (8, 6, 5), True, 2),
+                                           ((40, 20, 18), (8, 4, 6), True, 1), ((24, 13, 11), (24, 13, 11), True, 0)])
 def test_pcg_iterations_match_oracle(gpu_lib, n, tile, var, pc):
     faces = None
     if var:
