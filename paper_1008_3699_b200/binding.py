@@ -14,7 +14,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsweep.so")
+# SW_LIBRARY selects another build of the same library in this directory (the race-exposure build
+# libsweep_jitter.so of tests/test_gpu_jitter.py); it is never a CPU path.
+LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("SW_LIBRARY", "libsweep.so")))
 
 SW_OK, SW_EINVAL, SW_ESINGULAR, SW_ENOCONV, SW_ECUDA, SW_ENOMEM, SW_ESTATE = 0, 1, 2, 3, 4, 6, 7
 COEF_POISSON, COEF_FACES = 0, 1
@@ -76,6 +78,11 @@ def load():
     L.sw_launch_count.restype = I64
     L.sw_destroy.argtypes = [P_]
     L.sw_last_error.restype = ctypes.c_char_p
+    L.sw_debug_set_jitter.argtypes = [ctypes.c_uint]
+    L.sw_debug_set_jitter.restype = I
+    seed = os.environ.get("SW_JITTER_SEED")
+    if seed is not None and L.sw_debug_set_jitter(int(seed)) != 1:
+        raise RuntimeError(f"SW_JITTER_SEED set but {LIB_PATH} is not the jitter build")
     _lib = L
     return L
 

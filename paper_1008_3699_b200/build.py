@@ -7,6 +7,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsweep.so")
+# race-exposure variant (-DSW_JITTER, csrc/common.cuh): randomised sleeps after every barrier;
+# loaded only by tests/test_gpu_jitter.py through SW_LIBRARY
+LIB_JITTER = os.path.join(HERE, "libsweep_jitter.so")
 SRC = os.path.join(HERE, "csrc", "sweep.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -19,20 +22,26 @@ def sources():
     return [os.path.join(d, f) for f in os.listdir(d)] + [os.path.join(ROOT, "include", "sweep.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    newest = max(os.path.getmtime(p) for p in sources())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    extra = ["-DSW_TRACE"] if os.environ.get("SW_TRACE") == "1" else []
-    extra += [f"-D{d}" for d in os.environ.get("SW_DEFINES", "").split()]
-    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB, SRC, "-lcuda"]
+def _compile(out: str, defines, verbose: bool, log: str):
+    cmd = [NVCC, *FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-o", out, SRC, "-lcuda", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stderr)
-    with open(os.path.join(HERE, "ptxas.log"), "w") as f:
+    with open(os.path.join(HERE, log), "w") as f:
         f.write(res.stderr)
+
+
+def build(force: bool = False, verbose: bool = False, jitter: bool = True) -> str:
+    """Build libsweep.so (and the race-exposure variant libsweep_jitter.so) if a source is newer."""
+    newest = max(os.path.getmtime(p) for p in sources())
+    extra = ["-DSW_TRACE"] if os.environ.get("SW_TRACE") == "1" else []
+    extra += [f"-D{d}" for d in os.environ.get("SW_DEFINES", "").split()]
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+        _compile(LIB, extra, verbose, "ptxas.log")
+    if jitter and (force or not os.path.exists(LIB_JITTER) or os.path.getmtime(LIB_JITTER) < newest):
+        _compile(LIB_JITTER, ["-DSW_JITTER"], False, "ptxas_jitter.log")
     return LIB
 
 

@@ -155,6 +155,7 @@ __device__ void factor_node(const KParams &P, const int64_t g[3]) {
 
 template <int DIM>
 __global__ void __launch_bounds__(128) k_generic(KParams P) {
+    SW_JITTER_POINT();
     const Geo &G = P.G;
     // tile of this CTA (local tile index, x fastest)
     int64_t t = blockIdx.x;

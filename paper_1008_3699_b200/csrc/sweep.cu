@@ -1238,6 +1238,17 @@ extern "C" sw_status sw_destroy(sw_grid *g) {
     return SW_OK;
 }
 
+// Test aid (not part of sweep.h): seed of the race-exposure build (-DSW_JITTER, common.cuh);
+// 1 = set, 0 = this library was built without jitter, -1 = CUDA error.
+extern "C" int sw_debug_set_jitter(unsigned seed) {
+#ifdef SW_JITTER
+    return cudaMemcpyToSymbol(sw_jitter_seed, &seed, sizeof(seed)) == cudaSuccess ? 1 : -1;
+#else
+    (void)seed;
+    return 0;
+#endif
+}
+
 // Tuning aid (not part of sweep.h): per-phase clock sums of the traced kernels, then reset.
 extern "C" int sw_debug_phase_times(unsigned long long out[16]) {
 #ifdef SW_TRACE

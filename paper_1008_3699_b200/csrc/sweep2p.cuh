@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(64, 6)
     k_sweep2p(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb, Sweep2pArgs A) {
     extern __shared__ __align__(128) double xw[];
     __shared__ uint64_t bar;
+    SW_JITTER_POINT();
     const Geo &G = A.G;
     const int tid = threadIdx.x;
     const int tx = blockIdx.x % G.nt[0];

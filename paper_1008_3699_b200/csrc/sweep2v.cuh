@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(v2::NW * 32, 2)
     k_sweep2v(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
               const __grid_constant__ CUtensorMap tmfx, const __grid_constant__ CUtensorMap tmfy, Sweep2vArgs A) {
     extern __shared__ __align__(128) double sm[];
+    SW_JITTER_POINT();
     __shared__ uint64_t bar;
     const Geo &G = A.G;
     const int tx = blockIdx.x % G.nt[0];

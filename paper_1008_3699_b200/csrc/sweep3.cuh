@@ -290,6 +290,7 @@ __device__ __forceinline__ void edge_chain(double *X, int WS, int lane, int T, i
 template <bool FACES, int SHAPE>
 __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     extern __shared__ __align__(128) double sm[];
+    SW_JITTER_POINT();
     const Geo &G = A.G;
     using SH = Shape3<SHAPE>;
     const int T0 = SH::t0(A), T1 = SH::t1(A), T2 = SH::t2(A);
@@ -531,7 +532,10 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         else if (warp == 3) edge_chain<3>(X, WS, lane, T2, wof(0, 0, 1), st[2], st, sb, A.flag, (cb & 3) == 3);
         else __syncthreads();
         if (!conc_x) __syncthreads();
-        else if (warp != 1) asm volatile("bar.sync 1, %0;" ::"r"(k3::NT - 32) : "memory");
+        else if (warp != 1) {
+            asm volatile("bar.sync 1, %0;" ::"r"(k3::NT - 32) : "memory");
+            SW_JITTER_POINT();
+        }
     }
 
     SW_TMARK(t_sets);
@@ -626,6 +630,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                     do {
                         asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(got) : "r"(smem_u32(&s_edge_done)) : "memory");
                     } while (got < need);
+                    SW_JITTER_POINT();
                 }
             };
             Ld va, vb;

@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace sw {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -33,6 +35,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+    SW_JITTER_POINT();
 }
 
 // 2D tiled TMA load global -> shared, completion on mbarrier

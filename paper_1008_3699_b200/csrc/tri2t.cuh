@@ -34,6 +34,7 @@ struct Tri2tArgs {
 
 template <bool FACES>
 __global__ void __launch_bounds__(32) k_tri2t(Tri2tArgs A) {
+    SW_JITTER_POINT();
     constexpr int T = 64;
     __shared__ double ch[2][11][T];          // per chain, per quantity, per position k
     const Geo &G = A.G;

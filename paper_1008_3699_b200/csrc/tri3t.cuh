@@ -211,6 +211,7 @@ __device__ __forceinline__ void tri3t_ge(double (&M)[K][K], double (&rhs)[K], do
 
 template <int NA>
 __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
+    SW_JITTER_POINT();
     const Geo &G = A.G;
     const int64_t t = blockIdx.x;
     int64_t R[3] = {t % G.nt[0], (t / G.nt[0]) % G.nt[1], t / ((int64_t)G.nt[0] * G.nt[1])};
