@@ -18,11 +18,15 @@
  * of a box = sum_a s_a << a; omega arrays are indexed by it (1D: 0 = LR, 1 = RL;
  * 2D: 0 = SW, 1 = SE, 2 = NW, 3 = NE).
  *
- * Multi-GPU: the slowest used axis (y in 2D, z in 3D) is split into contiguous slabs of
- * whole tile rows, one per rank.  Every per-node array on the device carries 2 ghost
- * layers on each side of every axis; the ghost layers of the slab axis hold the
- * neighbouring ranks' values and are refreshed by the caller through sw_ghost_view()
- * (the Python binding does this with torch.distributed / NCCL).
+ * Multi-GPU: the slowest used axis (y in 2D, z in 3D) is split into
+ * contiguous slabs of whole tile rows, one per rank (one process per GPU).  Every per-node
+ * array on the device carries 2 ghost layers on each side of every axis; the ghost layers of
+ * the slab axis hold the neighbouring ranks' values.  With a communicator (sw_comm, passed to
+ * sw_decompose) the library refreshes them itself -- "halo points ... renewed (via
+ * communication) prior to a new iteration" -- by NCCL point-to-point over
+ * NVLink, overlapped with the sweep of the interior tile rows, and
+ * sums the PCG reductions over ranks on the device.  Without one, the caller refreshes them
+ * through sw_ghost_view() and drives the staged calls.
  *
  * Conventions.  Every call returns sw_status; nothing aborts the process; on error
  * sw_last_error() returns a thread-local message.  The library owns all device memory
@@ -34,6 +38,7 @@
 #ifndef SWEEP_H
 #define SWEEP_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -41,6 +46,7 @@ extern "C" {
 #endif
 
 typedef struct sw_grid sw_grid; /* opaque */
+typedef struct sw_comm sw_comm; /* opaque: the ranks of one slab decomposition */
 typedef struct CUstream_st *sw_stream_t; /* == cudaStream_t */
 
 typedef enum {
@@ -49,6 +55,7 @@ typedef enum {
     SW_ESINGULAR = 2,  /* a coupled system had |pivot| < 1e-14 or an ILU pivot D~ <= 0 */
     SW_ENOCONV = 3,    /* PCG hit maxit (outputs still valid) */
     SW_ECUDA = 4,      /* CUDA runtime error */
+    SW_ENCCL = 5,      /* communicator error (NCCL, or a host transport callback returned non-zero) */
     SW_ENOMEM = 6,     /* device allocation failed */
     SW_ESTATE = 7      /* call out of order (e.g. ilu_apply before ilu0_factor) */
 } sw_status;
@@ -68,12 +75,37 @@ typedef enum {
  * until sw_decompose.  *out is NULL on error. */
 sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, double beta, int cuda_device, sw_grid **out);
 
+/* ---- communicators ----------------------------------------
+ * NCCL: rank 0 calls sw_comm_unique_id and the caller broadcasts the 128 bytes (e.g. with
+ * torch.distributed); every rank then calls sw_comm_init_nccl (collective, blocking).  NCCL is
+ * loaded at run time (the libnccl.so.2 already in the process, e.g. torch's, else the system
+ * one); SW_ENCCL if none can be loaded.  One rank per GPU.
+ * HOST: a transport of the caller's (tests: several processes or threads sharing one GPU, over
+ * gloo or shared memory).  The library stages the layers through pinned host memory, after a
+ * stream synchronisation, and calls
+ *   exchange(ctx, send_lo, recv_lo, bytes_lo, send_hi, recv_hi, bytes_hi): send send_lo to rank-1
+ *       and receive its layers into recv_lo, likewise with rank+1 (bytes 0: no such neighbour);
+ *   allgather(ctx, send, recv, bytes): recv = the nranks send buffers in rank order;
+ * each returns 0 on success (else SW_ENCCL).  Host pointers, valid only during the call.
+ * A communicator may serve several grids of the same ranks (one call at a time). */
+typedef int (*sw_exchange_fn)(void *ctx, const void *send_lo, void *recv_lo, size_t bytes_lo, const void *send_hi,
+                              void *recv_hi, size_t bytes_hi);
+typedef int (*sw_allgather_fn)(void *ctx, const void *send, void *recv, size_t bytes);
+sw_status sw_comm_unique_id(unsigned char id[128]);
+sw_status sw_comm_init_nccl(const unsigned char id[128], int rank, int nranks, int cuda_device, sw_comm **out);
+sw_status sw_comm_init_host(int rank, int nranks, sw_exchange_fn exchange, sw_allgather_fn allgather, void *ctx,
+                            sw_comm **out);
+sw_status sw_comm_destroy(sw_comm *c);
+
 /* Fix the box shape (tile[a] must divide n[a]) and this rank's slab: rank r of nranks
  * owns tile rows [r*R/nranks, (r+1)*R/nranks) of the slowest axis (R = n_slow/tile_slow,
  * nranks must divide R).  Allocates the device arrays (2 iterate buffers, b, faces, ILU
  * and PCG work vectors) for the local slab plus 2 ghost layers per side of every axis,
- * all zero. */
-sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int nranks);
+ * all zero.  comm: NULL for one rank, or for several ranks whose ghost layers the caller
+ * refreshes (the staged calls); else a communicator of the same rank / nranks (borrowed; it
+ * must outlive the grid), which makes sw_sor_sweep, sw_residual_norm, sw_ilu0_factor,
+ * sw_ilu_apply, sw_ssor_apply and sw_pcg_solve multi-rank operations. */
+sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int nranks, sw_comm *comm);
 
 /* Local slab geometry: n_local[3] (x,y,z), slab offset (global index of the first local
  * node along the slab axis), padded dims pad[3] of every device array and the element
@@ -115,23 +147,31 @@ sw_status sw_set_coefficients_k(sw_grid *g, const double *k_host, const double s
  * directions) or 2^dim values indexed by direction bits, each in (0, 2).  Each sweep
  * solves (D/Omega + A_I(k)) u+ = b + (D/Omega - D) u - A_E(k) u exactly, i.e. every box
  * is relaxed from its start corner with the coupled 2x2 / 4x4 / 8x8 systems at faces
- * where two boxes start.  Single rank only for nsweeps > 1; with
- * nranks > 1 call with nsweeps = 1 and refresh the SW_X ghost layers before each call. */
+ * where two boxes start.  Multi-rank with a communicator: before its first
+ * sweep the call refreshes the 2 ghost layers of the iterate if sw_set_vector(SW_X) made them
+ * stale; each sweep then runs the slab's boundary tile rows first, hands the 2 new boundary
+ * layers to the neighbours on a high-priority stream (NCCL send/recv) while the interior tile
+ * rows run, and waits for them before the next sweep.  The result is
+ * bitwise independent of nranks.  Without a communicator and nranks > 1: nsweeps = 1 per
+ * call, the caller refreshes the SW_X ghost layers before each call. */
 sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, int nsweeps, int64_t *phase_inout,
                        sw_stream_t s);
 
-/* ||b - A x||_2 / ||b||_2 of the current iterate (single rank; synchronises). */
+/* ||b - A x||_2 / ||b||_2 of the current iterate (synchronises; over all ranks with a
+ * communicator, single rank otherwise). */
 sw_status sw_residual_norm(sw_grid *g, double *rel_out, sw_stream_t s);
 
 /* D-ILU(0) factor at phase k0 (R-C): D~_p = a_P,p - sum_{q implicit for p, same box}
- * c_pq^2 / D~_q, stored as 1/D~ in SW_INVD.  Tile-local.  SW_ESINGULAR (reported at the
- * next synchronising call or sw_check_status) if some D~ <= 0. */
+ * c_pq^2 / D~_q, stored as 1/D~ in SW_INVD.  Tile-local (with a communicator the 1-layer
+ * ghost of 1/D~ is exchanged after it).  SW_ESINGULAR (reported at the next synchronising call
+ * or sw_check_status) if some D~ <= 0. */
 sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s);
 
 /* z = P^-1 r for the D-ILU(0) of sw_ilu0_factor.  r_dev / z_dev are device pointers to
  * PADDED arrays of the layout reported by sw_local_shape (e.g. from sw_ghost_view);
- * r's ghost layers must be current.  Borrowed.  Single rank (several ranks: the staged form
- * below). */
+ * Borrowed.  With a communicator the library refreshes the ghost layers of r and of the
+ * intermediate arrays between the stages itself; without one and nranks > 1 use the staged
+ * form below (the caller refreshes them). */
 sw_status sw_ilu_apply(sw_grid *g, const double *r_dev, double *z_dev, sw_pairing pairing, sw_stream_t s);
 
 /* Same for the SSOR / SGS preconditioner z = w(2-w)(D + w L^T)^-1 D (D + w L)^-1 r at the
@@ -146,7 +186,8 @@ sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev, double *z
  * any theta).  With the SYMMETRIC pairing the operator is symmetric, and positive definite iff
  * theta * lambda_max(P^-1 A) < 2.  The decomposed SGS / D-ILU(0) preconditioners have
  * lambda_max(P^-1 A) = 2 (the start-face pairs; DESIGN R-C), so use theta < 1 (0.5 recommended)
- * for even m.  Single rank (the staged form below applies one step).  SW_EINVAL unless
+ * for even m.  Single rank, or multi-rank with a communicator (the staged form below applies
+ * one step).  SW_EINVAL unless
  * 1 <= m <= 64 and 0 < theta <= 1. */
 sw_status sw_set_precond_steps(sw_grid *g, int m, double theta);
 
@@ -180,9 +221,14 @@ sw_status sw_mg_set_cycle(sw_grid *g, int gamma);
 
 /* Preconditioned CG from x0 = 0 on the right-hand side SW_B until ||r||/||b|| < rtol
  * (recursive residual) or maxit; result in SW_X.  precond SW_PC_ILU0 factors at phase 0
- * first.  SW_ENOCONV: iters/relres still valid.  Single rank.  beta = (r+.z+)/(r.z), or the
- * flexible (Polak-Ribiere) beta = z+.(r+ - r)/(r.z) that the nonsymmetric PAPER pairing needs
- * (SURVEY §8(c) C-PCG; sw_set_pcg_flexible). */
+ * first.  SW_ENOCONV: iters/relres still valid.  beta = (r+.z+)/(r.z), or the flexible
+ * (Polak-Ribiere) beta = z+.(r+ - r)/(r.z) that the nonsymmetric PAPER pairing needs
+ * (SURVEY §8(c) C-PCG; sw_set_pcg_flexible).  alpha, beta and the stop test stay on the
+ * device.  With a communicator (SW_PC_NONE / SSOR / ILU0): every reduction is each rank's
+ * double-double partial, all-gathered on the device and summed in rank order, so all ranks take
+ * identical steps; ghost layers are exchanged inside the iteration (r and the preconditioner's
+ * intermediate layers, then z, from which each rank forms the neighbours' direction values
+ * itself).  Iteration counts agree with the single-rank solve to +-1. */
 sw_status sw_pcg_solve(sw_grid *g, sw_precond precond, double omega, sw_pairing pairing, double rtol, int maxit,
                        int *iters_out, double *relres_out, sw_stream_t s);
 

@@ -18,13 +18,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # libsweep_jitter.so of tests/test_gpu_jitter.py); it is never a CPU path.
 LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("SW_LIBRARY", "libsweep.so")))
 
-SW_OK, SW_EINVAL, SW_ESINGULAR, SW_ENOCONV, SW_ECUDA, SW_ENOMEM, SW_ESTATE = 0, 1, 2, 3, 4, 6, 7
+SW_OK, SW_EINVAL, SW_ESINGULAR, SW_ENOCONV, SW_ECUDA, SW_ENCCL, SW_ENOMEM, SW_ESTATE = 0, 1, 2, 3, 4, 5, 6, 7
 COEF_POISSON, COEF_FACES = 0, 1
 PC_NONE, PC_SSOR, PC_ILU0, PC_MG = 0, 1, 2, 3
 PAIR_SYMMETRIC, PAIR_PAPER = 0, 1
 X, B, R, Z, P, Q, INVD, Y, W1, W2 = range(10)
 
 _lib = None
+
+# host-transport callbacks of sw_comm_init_host (include/sweep.h)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
 
 
 class SweepError(RuntimeError):
@@ -46,7 +51,11 @@ def load():
     I = ctypes.c_int
     D = ctypes.c_double
     L.sw_create_grid.argtypes = [I, P_, I, D, I, ctypes.POINTER(P_)]
-    L.sw_decompose.argtypes = [P_, P_, I, I]
+    L.sw_decompose.argtypes = [P_, P_, I, I, P_]
+    L.sw_comm_unique_id.argtypes = [P_]
+    L.sw_comm_init_nccl.argtypes = [P_, I, I, I, ctypes.POINTER(P_)]
+    L.sw_comm_init_host.argtypes = [I, I, EXCHANGE_FN, ALLGATHER_FN, P_, ctypes.POINTER(P_)]
+    L.sw_comm_destroy.argtypes = [P_]
     L.sw_local_shape.argtypes = [P_, P_, P_, P_, P_]
     L.sw_set_vector.argtypes = [P_, I, P_, I, P_]
     L.sw_get_vector.argtypes = [P_, I, P_, I, P_]
@@ -110,6 +119,69 @@ def _host_ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
+def _bytes_at(ptr, nbytes):
+    """numpy uint8 view of host memory the library hands to a callback (valid during the call)."""
+    if not ptr or not nbytes:
+        return None
+    return np.ctypeslib.as_array((ctypes.c_uint8 * int(nbytes)).from_address(int(ptr)))
+
+
+def unique_id() -> bytes:
+    """NCCL unique id for sw_comm_init_nccl (rank 0 creates it, the caller broadcasts it)."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(load().sw_comm_unique_id(buf), "sw_comm_unique_id")
+    return bytes(buf)
+
+
+class Comm:
+    """A communicator of the ranks of one slab decomposition (sw_comm)."""
+
+    def __init__(self, handle, keep=()):
+        self.h = handle
+        self._keep = keep
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, nranks: int, device: int) -> "Comm":
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        _check(load().sw_comm_init_nccl(buf, int(rank), int(nranks), int(device), ctypes.byref(h)), "sw_comm_init_nccl")
+        return cls(h)
+
+    @classmethod
+    def host(cls, rank: int, nranks: int, transport) -> "Comm":
+        """transport.exchange(send_lo, recv_lo, send_hi, recv_hi) and transport.allgather(send, recv)
+        on numpy uint8 views (None where there is no neighbour); exceptions become SW_ENCCL."""
+        def xfn(_ctx, slo, rlo, blo, shi, rhi, bhi):
+            try:
+                transport.exchange(_bytes_at(slo, blo), _bytes_at(rlo, blo), _bytes_at(shi, bhi), _bytes_at(rhi, bhi))
+                return 0
+            except Exception:                          # reported as SW_ENCCL by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def gfn(_ctx, send, recv, nbytes):
+            try:
+                transport.allgather(_bytes_at(send, nbytes), _bytes_at(recv, nbytes * nranks))
+                return 0
+            except Exception:
+                import traceback
+                traceback.print_exc()
+                return 1
+        cx, cg = EXCHANGE_FN(xfn), ALLGATHER_FN(gfn)
+        h = ctypes.c_void_p()
+        _check(load().sw_comm_init_host(int(rank), int(nranks), cx, cg, None, ctypes.byref(h)), "sw_comm_init_host")
+        return cls(h, keep=(cx, cg, transport))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                load().sw_comm_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Grid:
     """A structured grid with its decomposition, owned device arrays and operations."""
 
@@ -127,15 +199,19 @@ class Grid:
     def __del__(self):
         try:
             if getattr(self, "h", None):
-                load().sw_destroy(self.h)
+                load().sw_destroy(self.h)      # before its communicator (self.comm) goes
                 self.h = None
         except Exception:
             pass
 
     # -------------------------------------------------------------- geometry
-    def decompose(self, tile: Sequence[int], rank: int = 0, nranks: int = 1):
+    def decompose(self, tile: Sequence[int], rank: int = 0, nranks: int = 1, comm: Optional[Comm] = None):
+        """comm: a Comm of the same ranks (the library then exchanges ghost layers and sums
+        reductions itself); kept alive by the grid."""
         t = (ctypes.c_int * 3)(*(list(tile) + [1] * (3 - self.dim)))
-        _check(load().sw_decompose(self.h, t, int(rank), int(nranks)), "sw_decompose")
+        _check(load().sw_decompose(self.h, t, int(rank), int(nranks), comm.h if comm is not None else None),
+               "sw_decompose")
+        self.comm = comm
         nl = (ctypes.c_int64 * 3)()
         pad = (ctypes.c_int64 * 3)()
         off = ctypes.c_int64()

@@ -561,6 +561,18 @@ __global__ void k_finish_dd(const DD *partial, int nparts, double *dst) {
     }
 }
 
+// same with a stride / offset over the partials (k_residual's interleaved r.r and b.b)
+__global__ void k_finish_dd_strided(const DD *partial, int nparts, int stride, int off, double *dst) {
+    __shared__ DD sh[RED_THREADS / 32];
+    DD acc = {0.0, 0.0};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc = dd_merge(acc, partial[(int64_t)i * stride + off]);
+    DD s = block_sum_dd(acc, sh);
+    if (threadIdx.x == 0) {
+        dst[0] = s.hi;
+        dst[1] = s.lo;
+    }
+}
+
 __global__ void k_set_scalar(double *dst, double v) { *dst = v; }
 
 // alpha = rz / pq

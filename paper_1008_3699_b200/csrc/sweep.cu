@@ -21,6 +21,7 @@
 #include "sweep3.cuh"
 #include "tri3t.cuh"
 #include "mg.cuh"
+#include "comm.cuh"
 
 using namespace sw;
 
@@ -84,31 +85,104 @@ struct sw_grid {
     struct MapEntry {
         const void *ptr;
         int box;
+        int64_t rows;
         CUtensorMap map;
     };
     std::deque<MapEntry> mapcache;    // TMA descriptors of arrays used as solve inputs (stable references)
+    // multi-rank with a communicator
+    sw_comm *comm = nullptr;
+    bool xghost_ok = false;                // ghost layers of the current iterate hold the neighbours' values
+    bool bghost_ok = false;                // same for b (the partner nodes' right-hand sides)
+    cudaStream_t xs = nullptr;             // high-priority stream of the halo exchange
+    cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
+    double *dds = nullptr, *ddg = nullptr; // this rank's double-double partial pairs / all ranks' pairs
 };
 
-// TMA descriptor (box x box window at the padded origin) of a padded array, cached by pointer.
-// Copied out by value: a later lookup may evict the cache entry.
-static bool get_map(sw_grid *g, const double *ptr, int box, CUtensorMap *out) {
+// TMA descriptor (box x box window) of a padded array with `rows` rows (0 = the slab's pad[1]),
+// cached by pointer.  Copied out by value: a later lookup may evict the cache entry.
+static bool get_map(sw_grid *g, const double *ptr, int box, CUtensorMap *out, int64_t rows = 0) {
+    if (rows == 0) rows = g->pad[1];
     for (auto &e : g->mapcache)
-        if (e.ptr == ptr && e.box == box) {
+        if (e.ptr == ptr && e.box == box && e.rows == rows) {
             *out = e.map;
             return true;
         }
     sw_grid::MapEntry e;
     e.ptr = ptr;
     e.box = box;
-    const bool ok = g->dim == 2 && encode_2d(&e.map, ptr, g->pad[0], g->pad[1], box, box);
+    e.rows = rows;
+    const bool ok = g->dim == 2 && encode_2d(&e.map, ptr, g->pad[0], rows, box, box);
     if (!ok) return false;
-    if (g->mapcache.size() >= 32) g->mapcache.pop_front();
+    if (g->mapcache.size() >= 48) g->mapcache.pop_front();
     g->mapcache.push_back(e);
     *out = e.map;
     return true;
 }
 
 extern "C" const char *sw_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------------ communicators
+extern "C" sw_status sw_comm_unique_id(unsigned char id[128]) {
+    if (!id) return fail(SW_EINVAL, "id is NULL");
+    NcclApi &N = nccl();
+    if (!N.ok) return fail(SW_ENCCL, N.why);
+    ncclUniqueId u;
+    ncclResult_t r = N.GetUniqueId(&u);
+    if (r != ncclSuccess) return fail(SW_ENCCL, std::string("ncclGetUniqueId: ") + N.GetErrorString(r));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(id, &u, 128);
+    return SW_OK;
+}
+
+extern "C" sw_status sw_comm_init_nccl(const unsigned char id[128], int rank, int nranks, int cuda_device,
+                                       sw_comm **out) {
+    if (!out || !id) return fail(SW_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SW_EINVAL, "bad rank / nranks");
+    NcclApi &N = nccl();
+    if (!N.ok) return fail(SW_ENCCL, N.why);
+    CK(cudaSetDevice(cuda_device));
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    sw_comm *c = new sw_comm();
+    c->kind = sw_comm::NCCL;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->dev = cuda_device;
+    ncclResult_t r = N.CommInitRank(&c->nc, nranks, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(SW_ENCCL, std::string("ncclCommInitRank: ") + N.GetErrorString(r));
+    }
+    *out = c;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_comm_init_host(int rank, int nranks, sw_exchange_fn exchange, sw_allgather_fn allgather,
+                                       void *ctx, sw_comm **out) {
+    if (!out) return fail(SW_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SW_EINVAL, "bad rank / nranks");
+    if (!exchange || !allgather) return fail(SW_EINVAL, "host transport needs both callbacks");
+    sw_comm *c = new sw_comm();
+    c->kind = sw_comm::HOST;
+    c->rank = rank;
+    c->nranks = nranks;
+    cudaGetDevice(&c->dev);
+    c->xfn = exchange;
+    c->gfn = allgather;
+    c->ctx = ctx;
+    *out = c;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_comm_destroy(sw_comm *c) {
+    if (!c) return SW_OK;
+    if (c->kind == sw_comm::NCCL && c->nc) nccl().CommDestroy(c->nc);
+    if (c->stage) cudaFreeHost(c->stage);
+    delete c;
+    return SW_OK;
+}
 
 extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, double beta, int cuda_device,
                                     sw_grid **out) {
@@ -150,6 +224,14 @@ static void free_all(sw_grid *g) {
     g->hcg = nullptr;
     if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
     g->cap_stream = nullptr;
+    if (g->xs) cudaStreamDestroy(g->xs);
+    if (g->ev_bnd) cudaEventDestroy(g->ev_bnd);
+    if (g->ev_halo) cudaEventDestroy(g->ev_halo);
+    if (g->dds) cudaFree(g->dds);
+    if (g->ddg) cudaFree(g->ddg);
+    g->xs = nullptr;
+    g->ev_bnd = g->ev_halo = nullptr;
+    g->dds = g->ddg = nullptr;
     if (g->partial) cudaFree(g->partial);
     if (g->cg) cudaFree(g->cg);
     if (g->flag) cudaFree(g->flag);
@@ -169,9 +251,11 @@ static sw_status alloc_arr(sw_grid *g, double **p) {
     return SW_OK;
 }
 
-extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int nranks) {
+extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int nranks, sw_comm *comm) {
     if (!g || !tile) return fail(SW_EINVAL, "NULL argument");
     if (g->decomposed) return fail(SW_ESTATE, "grid already decomposed");
+    if (comm && (comm->rank != rank || comm->nranks != nranks))
+        return fail(SW_EINVAL, "communicator rank / nranks differ from the decomposition's");
     const int d = g->dim, sa = d - 1;
     for (int a = 0; a < d; ++a) {
         if (tile[a] < 1 || g->ng[a] % tile[a] != 0)
@@ -233,6 +317,19 @@ extern "C" sw_status sw_decompose(sw_grid *g, const int tile[3], int rank, int n
     }
     CK(cudaMemset(g->flag, 0, sizeof(int)));
     CK(cudaMemset(g->cg, 0, sizeof(CgScalars)));
+    if (comm && nranks > 1) {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&g->xs, cudaStreamNonBlocking, hi));   // the halo goes first
+        CK(cudaEventCreateWithFlags(&g->ev_bnd, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->ev_halo, cudaEventDisableTiming));
+        if (cudaMalloc(&g->dds, sizeof(double) * 4) != cudaSuccess ||
+            cudaMalloc(&g->ddg, sizeof(double) * 4 * (size_t)nranks) != cudaSuccess) {
+            free_all(g);
+            return fail(SW_ENOMEM, "cudaMalloc of reduction buffers failed");
+        }
+        g->comm = comm;
+    }
     if (d == 2 && sweep2d_supported(G))
         make_maps2d(g->maps, g->X[0], g->X[1], g->B, g->F[0], g->F[1], g->pad[0], g->pad[1]);
     g->decomposed = true;
@@ -310,6 +407,8 @@ extern "C" sw_status sw_set_vector(sw_grid *g, sw_vector which, const double *sr
     double *d = vec_ptr(g, which);
     if (!d) return fail(SW_EINVAL, "bad vector id");
     if (which == SW_INVD) g->factored = true;
+    if (which == SW_X) g->xghost_ok = false;
+    if (which == SW_B) g->bghost_ok = false;
     return copy_interior(g, d, src, nullptr, true, (cudaStream_t)s);
 }
 
@@ -331,6 +430,8 @@ extern "C" sw_status sw_ghost_view(sw_grid *g, sw_vector which, double **dev_ptr
         if (st != SW_OK) return st;
     }
     *dev_ptr = vec_ptr(g, which);
+    if (which == SW_X) g->xghost_ok = false;   // the caller may write through the view
+    if (which == SW_B) g->bghost_ok = false;
     return *dev_ptr ? SW_OK : fail(SW_EINVAL, "bad vector id");
 }
 
@@ -447,63 +548,164 @@ static sw_status check_omega(const double *omega, int n_omega, int dim, double w
     return SW_OK;
 }
 
+// ------------------------------------------------------------------ multi-rank helpers
+// doubles per padded layer of the slab axis (x in 1D, y in 2D, z in 3D)
+static size_t layer_len(const sw_grid *g) { return g->dim == 1 ? 1 : (g->dim == 2 ? (size_t)g->G.P0 : (size_t)g->G.P01); }
+
+// refresh w ghost layers of padded array `arr` from the neighbouring ranks, ordered on s
+static sw_status exch(sw_grid *g, double *arr, int w, cudaStream_t s) {
+    if (!g->comm) return SW_OK;
+    CommErr e = comm_exchange(g->comm, arr, layer_len(g), g->G.n[g->dim - 1], w, s);
+    if (e.code) return fail(e.code == 1 ? SW_ENCCL : SW_ECUDA, e.msg);
+    return SW_OK;
+}
+
+// g->dds holds this rank's k (<= 2) double-double pairs: all-gather them and sum in rank order
+// into *o0 (and *o1), device scalars identical on every rank
+static sw_status allsum(sw_grid *g, int k, double *o0, double *o1, cudaStream_t s) {
+    CommErr e = comm_allgather(g->comm, g->dds, g->ddg, 2 * (size_t)k, s);
+    if (e.code) return fail(e.code == 1 ? SW_ENCCL : SW_ECUDA, e.msg);
+    k_rank_sum<<<1, 32, 0, s>>>(g->ddg, g->nranks, k, o0, o1 ? o1 : o0);
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
+// One decomposed sweep (x_old = X[cur] -> x_new = X[1-cur]) of the tile rows [r0, r0 + cnt) of
+// the slab axis.  A sub-range runs as a thinner slab: the geometry's slab extent and offsets are
+// those of the rows, every array pointer is shifted by r0 tile rows (the 2 layers beyond the rows
+// are real neighbouring rows or ghost layers of the padded arrays), TMA maps are encoded for the
+// shifted base.  Boxes read only x_old and write only their own nodes of x_new, so sub-ranges can
+// run in any order or concurrently with identical results.
+static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double *w8, cudaStream_t cs) {
+    const int sa = g->dim - 1;
+    Geo G = g->G;
+    const bool whole = (r0 == 0 && cnt == G.nt[sa]);
+    size_t dl = 0;
+    if (!whole) {
+        dl = (size_t)r0 * G.T[sa] * layer_len(g);
+        G.n[sa] = (int64_t)cnt * G.T[sa];
+        G.nt[sa] = cnt;
+        G.toff[sa] += r0;
+        G.off[sa] += (int64_t)r0 * G.T[sa];
+    }
+    const double *xo = g->X[g->cur] + dl, *bb = g->B + dl;
+    double *xn = g->X[1 - g->cur] + dl;
+    const double *F0 = g->F[0] ? g->F[0] + dl : nullptr, *F1 = g->F[1] ? g->F[1] + dl : nullptr,
+                 *F2 = g->F[2] ? g->F[2] + dl : nullptr;
+    if (g->dim == 2 && g->fast2d && g->maps.ok && (g->G.poisson || g->maps.fok)) {
+        CUtensorMap mx, mb, mf0, mf1;
+        if (whole) {
+            mx = g->maps.x[g->cur];
+            mb = g->maps.b;
+            if (!g->G.poisson) {
+                mf0 = g->maps.f[0];
+                mf1 = g->maps.f[1];
+            }
+        } else {
+            const int64_t rows = G.n[1] + 4;
+            if (!get_map(g, xo, WW, &mx, rows) || !get_map(g, bb, T2, &mb, rows) ||
+                (!g->G.poisson && (!get_map(g, F0, T2, &mf0, rows) || !get_map(g, F1, T2, &mf1, rows))))
+                return fail(SW_ECUDA, "cuTensorMapEncodeTiled failed");
+        }
+        cudaError_t e;
+        if (g->G.poisson)
+            e = launch_sweep2p(mx, mb, G, base, w8, bb, xn, g->flag, cs);
+        else
+            e = launch_sweep2v(mx, mb, mf0, mf1, G, base, w8, bb, F0, F1, xn, g->flag, cs);
+        g->launches++;
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2 launch: ") + cudaGetErrorString(e));
+        return SW_OK;
+    }
+    if (g->dim == 3 && g->fast2d && sweep3_supported(G)) {
+        Sweep3Args A3{};
+        A3.G = G;
+        A3.base = base;
+        for (int i = 0; i < 8; ++i) A3.omega[i] = w8[i];
+        A3.xin = xo;
+        A3.aux = bb;
+        A3.f0 = G.poisson ? nullptr : F0;
+        A3.f1 = G.poisson ? nullptr : F1;
+        A3.f2 = G.poisson ? nullptr : F2;
+        A3.out = xn;
+        A3.flag = g->flag;
+        A3.couple = 1;
+        cudaError_t e = launch_sweep3(A3, cs);
+        g->launches++;
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
+        return SW_OK;
+    }
+    KParams P = base_params(g);
+    P.G = G;
+    P.F[0] = F0;
+    P.F[1] = F1;
+    P.F[2] = F2;
+    P.mode = M_FWD;
+    P.rhs = R_SOR;
+    P.alpha_mode = A_OMEGA_AP;
+    P.base = base;
+    for (int i = 0; i < 8; ++i) P.omega[i] = w8[i];
+    P.xold = xo;
+    P.b = bb;
+    P.out = xn;
+    const int64_t tiles = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
+    switch (g->dim) {
+        case 1: k_generic<1><<<(unsigned)tiles, 32, 0, cs>>>(P); break;
+        case 2: k_generic<2><<<(unsigned)tiles, 96, 0, cs>>>(P); break;
+        default: k_generic<3><<<(unsigned)tiles, 128, 0, cs>>>(P); break;
+    }
+    g->launches++;
+    CK(cudaGetLastError());
+    return SW_OK;
+}
+
 extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, int nsweeps, int64_t *phase_inout,
                                   sw_stream_t s) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (!phase_inout || nsweeps < 0) return fail(SW_EINVAL, "bad phase / nsweeps");
-    if (g->nranks > 1 && nsweeps > 1) return fail(SW_EINVAL, "multi-rank: one sweep per call (exchange ghosts between)");
+    if (g->nranks > 1 && !g->comm && nsweeps > 1)
+        return fail(SW_EINVAL, "multi-rank without a communicator: one sweep per call (exchange ghosts between)");
     double w8[8];
     sw_status st = check_omega(omega, n_omega, g->dim, w8);
     if (st != SW_OK) return st;
     CK(cudaSetDevice(g->dev));
     cudaStream_t cs = (cudaStream_t)s;
+    const int sa = g->dim - 1, R = g->G.nt[sa];
+    const bool multi = g->comm && g->nranks > 1;
+    if (multi && !g->bghost_ok && nsweeps > 0) {   // partner nodes' right-hand sides across the slab faces
+        if ((st = exch(g, g->B, 2, cs)) != SW_OK) return st;
+        g->bghost_ok = true;
+    }
+    if (multi && !g->xghost_ok && nsweeps > 0 && (st = exch(g, g->X[g->cur], 2, cs)) != SW_OK) return st;
+    // boundary tile rows: those whose boxes read the ghost layers / write the layers the neighbours
+    // need (2 node layers deep); the rest is the interior that overlaps the exchange
+    const int nb = (2 + g->G.T[sa] - 1) / g->G.T[sa];
+    const bool split = multi && 2 * nb < R;
     for (int it = 0; it < nsweeps; ++it) {
-        int64_t k = *phase_inout;
-        int base = base_bits(g->dim, k);
-        const double *xo = g->X[g->cur];
-        double *xn = g->X[1 - g->cur];
-        if (g->dim == 2 && g->fast2d && g->maps.ok && g->G.poisson) {
-            cudaError_t e = launch_sweep2p(g->maps.x[g->cur], g->maps.b, g->G, base, w8, g->B, xn, g->flag, cs);
-            g->launches++;
-            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2p launch: ") + cudaGetErrorString(e));
-        } else if (g->dim == 2 && g->fast2d && g->maps.ok && g->maps.fok) {
-            cudaError_t e = launch_sweep2v(g->maps.x[g->cur], g->maps.b, g->maps.f[0], g->maps.f[1], g->G, base, w8,
-                                           g->B, g->F[0], g->F[1], xn, g->flag, cs);
-            g->launches++;
-            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2v launch: ") + cudaGetErrorString(e));
-        } else if (g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
-            Sweep3Args A3{};
-            A3.G = g->G;
-            A3.base = base;
-            for (int i = 0; i < 8; ++i) A3.omega[i] = w8[i];
-            A3.xin = xo;
-            A3.aux = g->B;
-            A3.f0 = g->G.poisson ? nullptr : g->F[0];
-            A3.f1 = g->G.poisson ? nullptr : g->F[1];
-            A3.f2 = g->G.poisson ? nullptr : g->F[2];
-            A3.out = xn;
-            A3.flag = g->flag;
-            A3.couple = 1;
-            cudaError_t e = launch_sweep3(A3, cs);
-            g->launches++;
-            if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
+        const int64_t k = *phase_inout;
+        const int base = base_bits(g->dim, k);
+        if (!multi) {
+            if ((st = sweep_rows(g, 0, R, base, w8, cs)) != SW_OK) return st;
+        } else if (!split) {
+            if ((st = sweep_rows(g, 0, R, base, w8, cs)) != SW_OK) return st;
+            if ((st = exch(g, g->X[1 - g->cur], 2, cs)) != SW_OK) return st;
         } else {
-            KParams P = base_params(g);
-            P.mode = M_FWD;
-            P.rhs = R_SOR;
-            P.alpha_mode = A_OMEGA_AP;
-            P.base = base;
-            for (int i = 0; i < 8; ++i) P.omega[i] = w8[i];
-            P.xold = xo;
-            P.b = g->B;
-            P.out = xn;
-            st = launch_generic(g, P, cs);
+            // boundary rows first, then the interior on the same stream while the high-priority
+            // stream moves the 2 new boundary layers to the neighbours
+            if ((st = sweep_rows(g, 0, nb, base, w8, cs)) != SW_OK) return st;
+            if ((st = sweep_rows(g, R - nb, nb, base, w8, cs)) != SW_OK) return st;
+            CK(cudaEventRecord(g->ev_bnd, cs));
+            if ((st = sweep_rows(g, nb, R - 2 * nb, base, w8, cs)) != SW_OK) return st;
+            CK(cudaStreamWaitEvent(g->xs, g->ev_bnd, 0));
+            if ((st = exch(g, g->X[1 - g->cur], 2, g->xs)) != SW_OK) return st;
+            CK(cudaEventRecord(g->ev_halo, g->xs));
+            CK(cudaStreamWaitEvent(cs, g->ev_halo, 0));
         }
-        if (st != SW_OK) return st;
         CK(cudaGetLastError());
         g->cur = 1 - g->cur;
         *phase_inout = k + 1;
     }
+    if (multi && nsweeps > 0) g->xghost_ok = true;
     return SW_OK;
 }
 
@@ -535,16 +737,28 @@ extern "C" sw_status sw_check_status(sw_grid *g, sw_stream_t s) {
 extern "C" sw_status sw_residual_norm(sw_grid *g, double *rel_out, sw_stream_t s) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (!rel_out) return fail(SW_EINVAL, "rel_out is NULL");
-    if (g->nranks > 1) return fail(SW_EINVAL, "sw_residual_norm is single-rank");
+    if (g->nranks > 1 && !g->comm) return fail(SW_EINVAL, "sw_residual_norm over several ranks needs a communicator");
     cudaStream_t cs = (cudaStream_t)s;
     int64_t N = g->G.n[0] * g->G.n[1] * g->G.n[2];
     int nb = grid_blocks(N, RED_THREADS);
+    sw_status st;
+    const bool multi = g->comm && g->nranks > 1;
+    if (multi && !g->xghost_ok) {
+        if ((st = exch(g, g->X[g->cur], 2, cs)) != SW_OK) return st;
+        g->xghost_ok = true;
+    }
     k_residual<<<nb, RED_THREADS, 0, cs>>>(g->G, g->F[0], g->F[1], g->F[2], g->X[g->cur], g->B, nullptr, g->partial);
     g->launches++;
     CK(cudaGetLastError());
-    sw_status st;
-    if ((st = finish(g, nb, 2, 0, &g->cg->rr, cs)) != SW_OK) return st;
-    if ((st = finish(g, nb, 2, 1, &g->cg->bb, cs)) != SW_OK) return st;
+    if (multi) {   // (r.r, b.b) pairs of every rank, summed in rank order
+        k_finish_dd_strided<<<1, RED_THREADS, 0, cs>>>(g->partial, nb, 2, 0, g->dds);
+        k_finish_dd_strided<<<1, RED_THREADS, 0, cs>>>(g->partial, nb, 2, 1, g->dds + 2);
+        g->launches += 2;
+        if ((st = allsum(g, 2, &g->cg->rr, &g->cg->bb, cs)) != SW_OK) return st;
+    } else {
+        if ((st = finish(g, nb, 2, 0, &g->cg->rr, cs)) != SW_OK) return st;
+        if ((st = finish(g, nb, 2, 1, &g->cg->bb, cs)) != SW_OK) return st;
+    }
     // one synchronisation for the scalars and the status flag
     if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars) + sizeof(int)));
     CgScalars &h = *g->hcg;
@@ -569,6 +783,7 @@ extern "C" sw_status sw_ilu0_factor(sw_grid *g, int64_t phase, sw_stream_t s) {
     P.base = base_bits(g->dim, phase);
     P.out = g->invD;
     if ((st = launch_generic(g, P, (cudaStream_t)s)) != SW_OK) return st;
+    if ((st = exch(g, g->invD, 1, (cudaStream_t)s)) != SW_OK) return st;   // partner layer of the solves
     g->factored = true;
     g->factor_phase = phase;
     return SW_OK;
@@ -688,11 +903,22 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     return launch_generic(g, P, s);
 }
 
+// All stages of one application z = P^-1 r.  With a communicator, the ghost layers each stage reads
+// are refreshed before it: r (1 layer) before the forward solve (the start-face chains recompute
+// the partner's y from its r); Y (1) before the PAPER pairing's backward solve; Y (1) and z (2)
+// before the coupled-set stages of the SYMMETRIC pairing.
 static sw_status tri_apply1(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
                             cudaStream_t s) {
+    const bool multi = g->comm && g->nranks > 1;
+    sw_status st;
+    if (multi && (st = exch(g, const_cast<double *>(r), 1, s)) != SW_OK) return st;
     for (int stage = 0; stage < tri_nstages(g, pairing); ++stage) {
-        sw_status st = tri_stage(g, ilu, omega, r, z, pairing, stage, s);
-        if (st != SW_OK) return st;
+        if (multi && stage == 1 && pairing == SW_PAIR_PAPER && (st = exch(g, g->Y, 1, s)) != SW_OK) return st;
+        if (multi && stage >= 2) {
+            if (stage == 2 && (st = exch(g, g->Y, 1, s)) != SW_OK) return st;
+            if ((st = exch(g, z, 2, s)) != SW_OK) return st;
+        }
+        if ((st = tri_stage(g, ilu, omega, r, z, pairing, stage, s)) != SW_OK) return st;
     }
     return SW_OK;
 }
@@ -706,7 +932,7 @@ static sw_status spmv_launch(sw_grid *g, const Rows &RW, int nr, const double *x
 // (SYMMETRIC pairing); positive definite when theta lambda_max(P^-1 A) < 2.
 static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
                            cudaStream_t s) {
-    if (g->nranks > 1) return fail(SW_EINVAL, "multi-rank: apply the preconditioner stage by stage");
+    if (g->nranks > 1 && !g->comm) return fail(SW_EINVAL, "multi-rank without a communicator: apply the preconditioner stage by stage");
     sw_status st = tri_apply1(g, ilu, omega, r, z, pairing, s);
     if (st != SW_OK || g->pc_steps <= 1) return st;
     if ((st = alloc_arr(g, &g->W1)) != SW_OK) return st;
@@ -714,6 +940,7 @@ static sw_status tri_apply(sw_grid *g, bool ilu, double omega, const double *r, 
     const Rows RW = make_rows(g->G);
     const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     for (int j = 1; j < g->pc_steps; ++j) {
+        if ((st = exch(g, z, 1, s)) != SW_OK) return st;
         if ((st = spmv_launch(g, RW, nr, z, g->W1, s, 0)) != SW_OK) return st;   // W1 = A z
         // W2 = r - theta A z (with zscale = theta folded in, z is already theta times the iterate)
         k_sub_r<<<nr, RED_THREADS, 0, s>>>(RW, r, g->zscale != 1.0 ? 1.0 : g->pc_theta, g->W1, g->W2);
@@ -781,7 +1008,7 @@ static sw_status mg_build(sw_grid *g, int levels, int axes) {
         if ((st = sw_create_grid(g->dim, nc, SW_COEF_FACES, bc, g->dev, &c)) != SW_OK) return st;
         g->mg.push_back(c);
         c->fast2d = g->fast2d;
-        if ((st = sw_decompose(c, tc, 0, 1)) != SW_OK) return st;
+        if ((st = sw_decompose(c, tc, 0, 1, nullptr)) != SW_OK) return st;
         if ((st = ensure_work(c)) != SW_OK) return st;
         for (int a = 0; a < g->dim; ++a) {
             const double *ff = (fine == g) ? (src_faces ? src_faces[a] : nullptr) : fine->F[a];
@@ -961,11 +1188,17 @@ extern "C" sw_status sw_ssor_apply(sw_grid *g, double omega, const double *r_dev
     return tri_apply(g, false, omega, r_dev, z_dev, pairing, (cudaStream_t)s);
 }
 
+static sw_status pcg_multi(sw_grid *g, sw_precond pc, double omega, sw_pairing pairing, double rtol, int maxit,
+                           int *iters_out, double *relres_out, cudaStream_t cs);
+
 extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pairing pairing, double rtol, int maxit,
                                   int *iters_out, double *relres_out, sw_stream_t s) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
-    if (g->nranks > 1) return fail(SW_EINVAL, "sw_pcg_solve is single-rank in this build");
     if (!iters_out || !relres_out || maxit < 1 || !(rtol > 0)) return fail(SW_EINVAL, "bad arguments");
+    if (g->nranks > 1) {
+        if (!g->comm) return fail(SW_EINVAL, "sw_pcg_solve over several ranks needs a communicator");
+        return pcg_multi(g, pc, omega, pairing, rtol, maxit, iters_out, relres_out, (cudaStream_t)s);
+    }
     sw_status st = ensure_work(g);
     if (st != SW_OK) return st;
     const cudaStream_t cs = (cudaStream_t)s;
@@ -1139,6 +1372,126 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     }
     cleanup();
     st = sw_check_status(g, s);
+    if (st != SW_OK) return st;
+    return fail(SW_ENOCONV, "PCG reached maxit");
+}
+
+// ------------------------------------------------------------------ multi-rank PCG
+// The same iteration as the single-rank solve (SURVEY §8(c) C-PCG, §8(e)): every reduction is this
+// rank's double-double partial, all-gathered on the device and summed in rank order (k_rank_sum),
+// so alpha, beta and the stop decision are identical on all ranks and never leave the device
+// except for the one readback of r.r per iteration.  Ghost layers: r and the preconditioner's
+// intermediates inside tri_apply1; z (1 layer) after the preconditioner, from which each rank
+// forms the neighbours' direction values p = z + beta p itself (k_ghost_pupdate, bitwise what
+// the neighbour computes), so the fused direction update + SpMV needs no further exchange.
+static sw_status pcg_multi(sw_grid *g, sw_precond pc, double omega, sw_pairing pairing, double rtol, int maxit,
+                           int *iters_out, double *relres_out, cudaStream_t cs) {
+    if (pc == SW_PC_MG) return fail(SW_EINVAL, "the multigrid preconditioner is single-rank");
+    sw_status st = ensure_work(g);
+    if (st != SW_OK) return st;
+    CK(cudaSetDevice(g->dev));
+    const Geo &G = g->G;
+    double *x = g->X[g->cur];
+    g->xghost_ok = false;
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)g->nelem, cs));
+    CK(cudaMemcpyAsync(g->R, g->B, sizeof(double) * (size_t)g->nelem, cudaMemcpyDeviceToDevice, cs));
+    if (pc == SW_PC_ILU0) {
+        if ((st = sw_ilu0_factor(g, 0, cs)) != SW_OK) return st;
+    } else {
+        g->factor_phase = 0;
+    }
+    double *z = (pc == SW_PC_NONE) ? g->R : g->Z;
+    const Rows RW = make_rows(G);
+    const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
+    const bool fc = !G.poisson;
+    if ((st = alloc_arr(g, &g->Pv2)) != SW_OK) return st;
+    const bool flex = g->pcg_flexible == 1 ||
+                      (g->pcg_flexible < 0 && pairing == SW_PAIR_PAPER && (pc == SW_PC_ILU0 || pc == SW_PC_SSOR));
+    if (flex && (st = alloc_arr(g, &g->Rold)) != SW_OK) return st;
+    if (!g->hcg) CK(cudaMallocHost(&g->hcg, sizeof(CgScalars) + sizeof(int)));
+    CgScalars &h = *g->hcg;
+    const size_t L = layer_len(g);
+    const int64_t nsa = G.n[g->dim - 1];
+    const size_t lay_lo = g->rank > 0 ? 1 : (size_t)-1, lay_hi = g->rank < g->nranks - 1 ? (size_t)(2 + nsa) : (size_t)-1;
+    const int gb = (int)std::min<size_t>((2 * L + 255) / 256, 1024);
+    auto red = [&](double *o0) -> sw_status {   // this rank's partials -> all ranks' sum in *o0
+        k_finish_dd<<<1, RED_THREADS, 0, cs>>>(g->partial, nr, g->dds);
+        g->launches++;
+        return allsum(g, 1, o0, nullptr, cs);
+    };
+    auto apply_pc = [&]() -> sw_status {
+        if (pc == SW_PC_NONE) return SW_OK;
+        return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, cs);
+    };
+    double *pcur = g->Pv, *pprev = g->Pv2;
+    // b.b, z0 = P^-1 r0, r.z, p = z (interior and the neighbours' layer)
+    k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->B, g->B, g->partial);
+    g->launches++;
+    if ((st = red(&g->cg->bb)) != SW_OK) return st;
+    if ((st = apply_pc()) != SW_OK) return st;
+    k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->R, z, g->partial);
+    g->launches++;
+    if ((st = red(&g->cg->rz)) != SW_OK) return st;
+    if ((st = exch(g, z, 1, cs)) != SW_OK) return st;
+    k_pupdate_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->beta, 1, z, pcur);
+    k_ghost_pupdate<<<gb, 256, 0, cs>>>(&g->cg->beta, 1, z, pcur, pcur, L, lay_lo, lay_hi);
+    g->launches += 2;
+    CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamSynchronize(cs));
+    const double bnorm = sqrt(h.bb);
+    *iters_out = 0;
+    *relres_out = 1.0;
+    if (bnorm == 0.0) { *relres_out = 0.0; return SW_OK; }
+    const double *F0 = g->F[0], *F1 = g->F[1], *F2 = g->F[2];
+    for (int it = 1; it <= maxit; ++it) {
+        if (it == 1) {
+            if ((st = spmv_launch(g, RW, nr, pcur, g->Q, cs, 0)) != SW_OK) return st;
+        } else {
+            std::swap(pcur, pprev);            // pprev = the old direction, pcur = where the new one goes
+            const double *bd = &g->cg->beta;
+            if (g->dim == 1) fc ? k_pspmv_dot_r<1, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                                : k_pspmv_dot_r<1, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            else if (g->dim == 2) fc ? k_pspmv_dot_r<2, true><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                                     : k_pspmv_dot_r<2, false><<<nr, RED_THREADS, 0, cs>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            else fc ? k_pspmv3_zm<true><<<nr, 256, 0, cs>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
+                    : k_pspmv3_zm<false><<<nr, 256, 0, cs>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            k_ghost_pupdate<<<gb, 256, 0, cs>>>(bd, 0, z, pprev, pcur, L, lay_lo, lay_hi);
+            g->launches += 2;
+            CK(cudaGetLastError());
+        }
+        if ((st = red(&g->cg->pq)) != SW_OK) return st;
+        k_cg_alpha<<<1, 1, 0, cs>>>(g->cg);
+        g->launches++;
+        if (flex) CK(cudaMemcpyAsync(g->Rold, g->R, sizeof(double) * (size_t)g->nelem, cudaMemcpyDeviceToDevice, cs));
+        k_axpy2_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, &g->cg->alpha, x, g->R, pcur, g->Q, g->partial);
+        g->launches++;
+        if ((st = red(&g->cg->rr)) != SW_OK) return st;
+        CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs));
+        CK(cudaStreamSynchronize(cs));
+        *iters_out = it;
+        *relres_out = sqrt(h.rr) / bnorm;
+        if (*relres_out < rtol) return sw_check_status(g, cs);
+        if (!(h.rr == h.rr)) return fail(SW_ENOCONV, "PCG produced NaN");
+        // z = P^-1 r, r.z (and z.(r+ - r)), beta; the neighbours' z layer
+        if ((st = apply_pc()) != SW_OK) return st;
+        k_dot_r<<<nr, RED_THREADS, 0, cs>>>(RW, g->R, z, g->partial);
+        k_finish_dd<<<1, RED_THREADS, 0, cs>>>(g->partial, nr, g->dds);
+        g->launches += 2;
+        if (flex) {
+            k_dot_diff_r<<<nr, RED_THREADS, 0, cs>>>(RW, z, g->R, g->Rold, g->partial);
+            k_finish_dd<<<1, RED_THREADS, 0, cs>>>(g->partial, nr, g->dds + 2);
+            g->launches += 2;
+            if ((st = allsum(g, 2, &g->cg->rz_new, &g->cg->zd, cs)) != SW_OK) return st;
+            k_cg_beta_flex<<<1, 1, 0, cs>>>(g->cg);
+        } else {
+            if ((st = allsum(g, 1, &g->cg->rz_new, nullptr, cs)) != SW_OK) return st;
+            k_cg_beta<<<1, 1, 0, cs>>>(g->cg);
+        }
+        g->launches++;
+        if ((st = exch(g, z, 1, cs)) != SW_OK) return st;
+        CK(cudaGetLastError());
+    }
+    st = sw_check_status(g, cs);
     if (st != SW_OK) return st;
     return fail(SW_ENOCONV, "PCG reached maxit");
 }

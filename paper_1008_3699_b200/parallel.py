@@ -3,11 +3,10 @@
 ghost layers of the iterate exchanged with rank +- 1 before every sweep ("halo points
 ... renewed (via communication) prior to a new iteration").
 
-The exchange works on any padded tensor whose axis 0 is the slab axis with 2 ghost
-layers per side (the device arrays of the C library viewed through torch, or plain CPU
-tensors in the gloo tests).  ``halo_plan`` says which layers go where; the transports
-are torch.distributed point-to-point ops (NCCL on GPUs, gloo on CPU) and, for tests
-that emulate several ranks inside one process, plain tensor copies.
+The library does this itself when its grid has a communicator (sw_comm: NCCL, or a HOST
+transport below); ``exchange_ghosts`` / ``exchange_ghosts_local`` are the caller-side
+equivalents for grids without one (the staged C calls), on any padded tensor whose axis 0
+is the slab axis with 2 ghost layers per side.  ``halo_plan`` says which layers go where.
 """
 from __future__ import annotations
 
@@ -85,155 +84,91 @@ def exchange_ghosts_local(ts: Sequence, n_locals: Sequence[int], width: int = GH
 
 
 # ---------------------------------------------------------------------------------------------
-# One PCG over several slabs.  The arithmetic runs in the library's kernels
-# (staged preconditioner, SpMV, fused axpy / dot); this driver only orders the calls, refreshes
-# ghost layers between them and sums the ranks' double-double partials in rank order.
+# Communicators for the library's own multi-rank path (sw_comm, include/sweep.h).  With one the
+# library exchanges the ghost layers and sums the reductions itself (NCCL on GPUs, one process per
+# GPU); these helpers only create it.  The HOST transports move the staged layers for processes or
+# threads that share one GPU (tests): the library calls them with pinned host buffers.
 
-def dd_sum(pairs) -> float:
-    """Sum (hi, lo) double-double pairs in the given order (TwoSum), rounded once."""
-    hi, lo = 0.0, 0.0
-    for h, l in pairs:
-        t = hi + h
-        bp = t - hi
-        err = (hi - (t - bp)) + (h - bp)
-        hi, lo = t, lo + err + l
-    return hi + lo
-
-
-class LocalComm:
-    """All ranks live in this process (virtual slabs, e.g. several Grids on one device)."""
-
-    def __init__(self, grids):
-        self.grids = list(grids)
-
-    def exchange(self, views, width):
-        exchange_ghosts_local(views, [g.n_local[-1] for g in self.grids], width)
-
-    def allsum(self, pairs):
-        return dd_sum(pairs)
-
-
-class DistComm:
-    """One rank per process: ghost layers by torch.distributed point-to-point (NCCL on GPUs),
-    reductions by all_gather of the (hi, lo) pairs and a rank-ordered sum on every rank."""
-
-    def __init__(self, grid, group=None, device=None):
-        import torch.distributed as dist
-        self.grids = [grid]
-        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        self.group = group
-        self.bufs = {}
-        self.device = device if device is not None else f"cuda:{grid.device}"
-
-    def exchange(self, views, width):
-        exchange_ghosts(views[0], self.grids[0].n_local[-1], self.rank, self.world, self.group, width, self.bufs)
-
-    def allsum(self, pairs):
-        import torch
-        import torch.distributed as dist
-        t = torch.tensor(pairs[0], dtype=torch.float64, device=self.device)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
-        return dd_sum([tuple(o.tolist()) for o in out])
-
-
-def pcg_slabs(comm, precond: int = 2, omega: float = 1.0, pairing: int = 0, rtol: float = 1e-8,
-              maxit: int = 10000, msteps: int = 1, theta: float = 0.5, flexible=None):
-    """Preconditioned CG from x0 = 0 on the right-hand side SW_B of every slab grid of `comm`
-    (same algorithm and stop test as sw_pcg_solve).  msteps > 1 applies the m-step form of the
-    preconditioner (sw_set_precond_steps: z_{j+1} = z_j + P^-1 (r - theta A z_j)) through the
-    staged solves, sw_apply_A and sw_axpby.  flexible: the Polak-Ribiere beta z+.(r+ - r)/(r.z)
-    (None: exactly when the preconditioner is ILU(0) or SSOR with the PAPER pairing, as
-    sw_pcg_solve).  Returns (iterations, relres, converged)."""
-    import torch
+def nccl_comm(device: int, group=None):
+    """NCCL communicator of the torch.distributed group's ranks (rank 0 makes the unique id and
+    broadcasts it through the group)."""
+    import torch.distributed as dist
 
     from . import binding as B
-    grids = comm.grids
-    dev = f"cuda:{grids[0].device}"
-    vecs = (B.X, B.B, B.R, B.Z, B.P, B.Q, B.Y, B.INVD) + ((B.W1, B.W2) if msteps > 1 else ())
-    V = {w: [g.view(w) for g in grids] for w in vecs}
-    ptr = {w: [t.data_ptr() for t in V[w]] for w in V}
-    dd = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in grids]
-    if flexible is None:
-        flexible = pairing == B.PAIR_PAPER and precond in (B.PC_ILU0, B.PC_SSOR)
-    if flexible:                             # r before its update, and r+ - r
-        rold = [torch.empty_like(t) for t in V[B.R]]
-        rdif = [torch.empty_like(t) for t in V[B.R]]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [B.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return B.Comm.nccl(obj[0], rank, world, device)
 
-    def reduce(fn):
-        for i, g in enumerate(grids):
-            fn(i, g)
-        torch.cuda.synchronize()
-        return comm.allsum([tuple(d.tolist()) for d in dd])
 
-    for i in range(len(grids)):
-        V[B.X][i].zero_()
-        V[B.R][i].copy_(V[B.B][i])
-    if precond == B.PC_ILU0:
-        for g in grids:
-            g.ilu0_factor(0)
-        comm.exchange(V[B.INVD], 1)
-    z = B.R if precond == B.PC_NONE else B.Z
+class GlooTransport:
+    """HOST transport over a torch.distributed (gloo) group: one process per rank."""
 
-    def apply1(src, dst):                    # dst = P^-1 src, stage by stage
-        comm.exchange(V[src], 1)
-        for st in range(grids[0].precond_stages(pairing)):
-            if st == 1 and pairing == B.PAIR_PAPER:
-                comm.exchange(V[B.Y], 1)
-            if st >= 2:
-                if st == 2:
-                    comm.exchange(V[B.Y], 1)
-                comm.exchange(V[dst], 2)
-            for i, g in enumerate(grids):
-                g.precond_apply_stage(precond, st, ptr[src][i], ptr[dst][i], omega, pairing)
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
 
-    def apply_pc():
-        if precond == B.PC_NONE:
-            return
-        apply1(B.R, B.Z)
-        for _ in range(msteps - 1):             # z += P^-1 (r - theta A z)
-            comm.exchange(V[B.Z], 1)
-            for i, g in enumerate(grids):
-                g.apply_A(ptr[B.Z][i], ptr[B.W1][i], dd[i].data_ptr())
-                g.axpby(1.0, ptr[B.R][i], -theta, ptr[B.W1][i], ptr[B.W2][i])
-            apply1(B.W2, B.W1)
-            for i, g in enumerate(grids):
-                g.axpby(1.0, ptr[B.Z][i], 1.0, ptr[B.W1][i], ptr[B.Z][i])
+    def exchange(self, send_lo, recv_lo, send_hi, recv_hi):
+        import torch
+        import torch.distributed as dist
+        ops = []
+        if send_lo is not None:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(send_lo), self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, torch.from_numpy(recv_lo), self.rank - 1, self.group))
+        if send_hi is not None:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(send_hi), self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, torch.from_numpy(recv_hi), self.rank + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
 
-    bb = reduce(lambda i, g: g.dot(ptr[B.B][i], ptr[B.B][i], dd[i].data_ptr()))
-    bnorm = bb ** 0.5
-    if bnorm == 0.0:
-        return 0, 0.0, True
-    apply_pc()
-    rz = reduce(lambda i, g: g.dot(ptr[B.R][i], ptr[z][i], dd[i].data_ptr()))
-    for i in range(len(grids)):
-        V[B.P][i].copy_(V[z][i])
-    relres = 1.0
-    for it in range(1, maxit + 1):
-        comm.exchange(V[B.P], 1)
-        pq = reduce(lambda i, g: g.apply_A(ptr[B.P][i], ptr[B.Q][i], dd[i].data_ptr()))
-        alpha = rz / pq
-        if flexible:
-            for i in range(len(grids)):
-                rold[i].copy_(V[B.R][i])
-        rr = reduce(lambda i, g: g.axpy2(alpha, ptr[B.X][i], ptr[B.R][i], ptr[B.P][i], ptr[B.Q][i],
-                                         dd[i].data_ptr()))
-        relres = rr ** 0.5 / bnorm
-        if relres < rtol:
-            for g in grids:
-                g.check()
-            return it, relres, True
-        if relres != relres:
-            raise FloatingPointError("PCG produced NaN")
-        apply_pc()
-        rzn = reduce(lambda i, g: g.dot(ptr[B.R][i], ptr[z][i], dd[i].data_ptr()))
-        if flexible:                         # (r+ - r) rounded first, then z.(r+ - r), as the oracle
-            for i, g in enumerate(grids):
-                g.axpby(1.0, ptr[B.R][i], -1.0, rold[i].data_ptr(), rdif[i].data_ptr())
-            beta = reduce(lambda i, g: g.dot(ptr[z][i], rdif[i].data_ptr(), dd[i].data_ptr())) / rz
-        else:
-            beta = rzn / rz
-        rz = rzn
-        for i, g in enumerate(grids):
-            g.xpby(ptr[z][i], beta, ptr[B.P][i])
-    return maxit, relres, False
+    def allgather(self, send, recv):
+        import torch
+        import torch.distributed as dist
+        out = [torch.empty(send.size, dtype=torch.uint8) for _ in range(self.world)]
+        dist.all_gather(out, torch.from_numpy(send.copy()), group=self.group)
+        recv[:] = torch.cat(out).numpy()
+
+
+class ThreadHub:
+    """In-process HOST transport: `world` ranks as threads of one process (each drives its own
+    grid on its own stream); every exchange / all-gather is a barrier-separated swap."""
+
+    def __init__(self, world: int):
+        import threading
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+    def endpoint(self, rank: int):
+        return _ThreadEndpoint(self, rank)
+
+
+class _ThreadEndpoint:
+    def __init__(self, hub: ThreadHub, rank: int):
+        self.hub, self.rank = hub, rank
+
+    def exchange(self, send_lo, recv_lo, send_hi, recv_hi):
+        h, r = self.hub, self.rank
+        h.slots[r] = (None if send_lo is None else send_lo.copy(), None if send_hi is None else send_hi.copy())
+        h.barrier.wait()
+        if recv_lo is not None:
+            recv_lo[:] = h.slots[r - 1][1]          # rank - 1 sends its upper layers
+        if recv_hi is not None:
+            recv_hi[:] = h.slots[r + 1][0]          # rank + 1 sends its lower layers
+        h.barrier.wait()
+
+    def allgather(self, send, recv):
+        h, r = self.hub, self.rank
+        h.slots[r] = send.copy()
+        h.barrier.wait()
+        n = send.size
+        for q in range(h.world):
+            recv[q * n:(q + 1) * n] = h.slots[q]
+        h.barrier.wait()
+
+
+def host_comm(rank: int, world: int, transport):
+    from . import binding as B
+    return B.Comm.host(rank, world, transport)
