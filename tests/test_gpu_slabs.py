@@ -45,6 +45,7 @@ def test_staged_sweep_over_slabs_matches_oracle(n, tile, nranks, var):
     sl = make_slabs(n, tile, nranks, faces)
     scatter(sl, B.X, x0)
     scatter(sl, B.B, b)
+    parallel.exchange_ghosts_local([g.view(B.B) for g in sl], [g.n_local[-1] for g in sl], 2)   # partners' b
     nsw = 2 ** len(n) + 1
     for k in range(nsw):
         parallel.exchange_ghosts_local([g.view(B.X) for g in sl], [g.n_local[-1] for g in sl], 2)
