@@ -7,8 +7,9 @@ fraction of the HBM roofline.  Workload at N=1 (config 4 of BASELINE.json, the
 b = h^2 f with f ~ U[-1,1) (seeded, gen.py), 64 x 64 boxes, omega = 2/(1+sin(pi h)).
 One step = one decomposed SOR sweep over the whole grid (schedule, ghost refresh,
 corner/edge coupled solves, interior wavefront, write-back: SURVEY §8(a) a2-a8).
-For N > 1 (torchrun): weak scaling, 16384 x (16384 N), row slabs of 256 tile rows per
-rank, ghost layers exchanged with NCCL before every sweep.
+For N > 1 (torchrun): --scaling weak (default; 16384 x 16384 N) or strong (16384^2 over N),
+row slabs per rank; the library's communicator (NCCL) moves the 2 ghost layers every sweep
+behind the interior tile rows; config 5 runs slab-sharded (sweep, ILU(0)- and SSOR-PCG).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -119,69 +120,90 @@ def rhs_slab(seed, rows, row0, nx, h):
     return (f * (h * h)).reshape(rows, nx)
 
 
+def make_comm(args, world, rank, dev):
+    """torch.distributed plumbing + the library's communicator (NCCL, one rank per GPU; or the
+    gloo host transport for several ranks sharing one GPU in tests)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1008_3699_b200 import parallel
+    if world == 1:
+        return None
+    if args.comm == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        return parallel.nccl_comm(dev)
+    dist.init_process_group("gloo")
+    return parallel.host_comm(rank, world, parallel.GlooTransport())
+
+
+def max_over_ranks(v, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1008_3699_b200 import binding, parallel
+    from paper_1008_3699_b200 import binding
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
     binding.load()
+    comm = make_comm(args, world, rank, dev)
     T = 64
-    ny = NX * world                        # weak scaling: 16384 x 16384 per GPU
-    n = (NX, ny)
-    h = 1.0 / (NX + 1)
+    NXl = args.nx
+    weak = args.scaling == "weak"
+    ny = NXl * world if weak else NXl     # weak: 16384 x 16384 per GPU; strong: 16384^2 split over N
+    n = (NXl, ny)
+    h = 1.0 / (NXl + 1)
     omega = 2.0 / (1.0 + np.sin(np.pi * h))
-    g = binding.Grid(2, n, binding.COEF_POISSON, 0.0, local).decompose((T, T), rank, world)
+    g = binding.Grid(2, n, binding.COEF_POISSON, 0.0, dev).decompose((T, T), rank, world, comm)
     nl_y = g.n_local[1]
     row0 = g.slab_offset
-    b = rhs_slab(args.seed, nl_y, row0, NX, h)
+    b = rhs_slab(args.seed, nl_y, row0, NXl, h)
     g.set_vector(binding.B, b)
-    g.set_vector(binding.X, np.zeros((nl_y, NX)))
+    g.set_vector(binding.X, np.zeros((nl_y, NXl)))
     stream = torch.cuda.current_stream()
-    if world > 1:
-        # b's ghost rows (partner nodes' right-hand sides) once; x's every sweep
-        parallel.exchange_ghosts(g.view(binding.B), nl_y, rank, world)
-    bufs = {}
-
-    def step(phase):
-        if world > 1:
-            parallel.exchange_ghosts(g.view(binding.X), nl_y, rank, world, bufs=bufs)
-        return g.sor_sweep([omega], 1, phase)
-
     phase = 0
-    clk = ClockSampler(local).__enter__()      # sampling from before the warm-up on
+    clk = ClockSampler(dev).__enter__()        # sampling from before the warm-up on
     time.sleep(0.3)                            # nvidia-smi's first samples
-    for _ in range(args.warmup):
-        phase = step(phase)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # warm-up: W sweeps (the first call also exchanges b's and x's ghost layers once)
+    phase = g.sor_sweep([omega], args.warmup, phase)
+    barrier(world)
     l0 = g.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     clk.start()
     ev0.record(stream)
-    for _ in range(args.steps):
-        phase = step(phase)
+    # K steps = K decomposed sweeps in one C call; with N ranks every sweep runs the slab's boundary
+    # tile rows, then the interior rows while the 2 new boundary layers go to the neighbours (NCCL)
+    phase = g.sor_sweep([omega], args.steps, phase)
     ev1.record(stream)
     torch.cuda.synchronize()
     clk.stop()
     clk.__exit__(None, None, None)
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     launches = g.launch_count() - l0
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    nodes_total = NX * ny
+    nodes_total = NXl * ny
     glups = nodes_total * args.steps / (ms * 1e-3) / 1e9
     ms_per_step = ms / args.steps
 
@@ -200,10 +222,11 @@ def run_ours(args):
     else:
         kern_ms = [ms_per_step]
     peak, peak_src = peaks()
-    per_launch_bytes = B_PER_LUP_POISSON * (NX * nl_y)
+    per_launch_bytes = B_PER_LUP_POISSON * (NXl * nl_y)
     # average launch duration over the timed region: every launch in it is the sweep kernel (one
     # per step on one GPU), so the events around the region give it directly; the separately
-    # timed launches (an event pair each) are reported beside it
+    # timed launches (an event pair each) are reported beside it.  N > 1: a step is three launches
+    # (two boundary row ranges, the interior) plus the exchange, so the whole step is the unit.
     kiso = float(np.mean(kern_ms))
     kavg = ms / launches if (world == 1 and launches == args.steps) else kiso
     achieved = per_launch_bytes / (kavg * 1e-3) / 1e9
@@ -211,59 +234,50 @@ def run_ours(args):
     tf = os.path.join(ROOT, "profiles", "sweep2p_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("bytes_per_launch")
+        traffic_src = ("stored: dram__bytes_read.sum + dram__bytes_write.sum of one k_sweep2p launch from the ncu "
+                       f"--set full capture {tj.get('source', 'profiles/sweep2p_traffic.json')} (not measured in this run)")
 
     # end-to-end through the public API with HOST buffers: one user job = upload b and x0 from
     # pinned host memory, 200 sweeps (config 4's count), download x; time with events
     e2e = None
     if not args.no_e2e:
-        # every rank uploads its slab (b, whose ghost rows are then exchanged, and x0), sweeps with
-        # the per-sweep ghost exchange, downloads its slab; the job time is the max over ranks
+        # every rank uploads its slab (b and x0), runs the sweeps (one C call; the library refreshes
+        # the ghost layers of b once and of x every sweep), downloads its slab; max over ranks
         hb = torch.from_numpy(b).pin_memory()
-        hx = torch.zeros((nl_y, NX), dtype=torch.float64).pin_memory()
-        hout = torch.empty((nl_y, NX), dtype=torch.float64).pin_memory()
+        hx = torch.zeros((nl_y, NXl), dtype=torch.float64).pin_memory()
+        hout = torch.empty((nl_y, NXl), dtype=torch.float64).pin_memory()
         nsw = 200
         times = []
         for rep in range(2):
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
+            barrier(world)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             g.set_vector(binding.B, hb)
             g.set_vector(binding.X, hx)
-            if world == 1:
-                g.sor_sweep([omega], nsw, 0)
-            else:
-                parallel.exchange_ghosts(g.view(binding.B), nl_y, rank, world)
-                ph = 0
-                for _ in range(nsw):
-                    ph = step(ph)
+            g.sor_sweep([omega], nsw, 0)
             g.get_vector(binding.X, hout)
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-        t = min(times)
-        if world > 1:
-            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t = float(tt.item())
-        e2e = {"value": round(NX * ny * nsw / (t * 1e-3) / 1e9, 3), "unit": "GLUP/s",
-               "h2d_bytes_per_step": int(2 * NX * ny * 8) // nsw, "d2h_bytes_per_step": int(NX * ny * 8) // nsw,
+        t = max_over_ranks(min(times), world)
+        e2e = {"value": round(NXl * ny * nsw / (t * 1e-3) / 1e9, 3), "unit": "GLUP/s",
+               "h2d_bytes_per_step": int(2 * NXl * ny * 8) // nsw, "d2h_bytes_per_step": int(NXl * ny * 8) // nsw,
                "step": f"one user job through the C ABI: b and x0 copied H2D from pinned host memory, {nsw} sweeps "
                        f"(config 4's count), x copied D2H; bytes per step = job bytes / {nsw}",
-               "h2d_bytes_per_job": int(2 * NX * ny * 8), "d2h_bytes_per_job": int(NX * ny * 8),
+               "h2d_bytes_per_job": int(2 * NXl * ny * 8), "d2h_bytes_per_job": int(NXl * ny * 8),
                "ms_per_job": round(t, 3)}
         if world == 1:
             # a stream of jobs (serving): the same job J times on two grids and two streams, so
             # that job j+1's copies overlap job j's sweeps; every copy of every job is inside the
             # timed region (first upload to last download)
             J = 8
-            g2 = binding.Grid(2, n, binding.COEF_POISSON, 0.0, local).decompose((T, T), rank, world)
+            g2 = binding.Grid(2, n, binding.COEF_POISSON, 0.0, dev).decompose((T, T), rank, world)
             grids = [g, g2]
             strs = [torch.cuda.Stream(), torch.cuda.Stream()]
-            houts = [hout, torch.empty((nl_y, NX), dtype=torch.float64).pin_memory()]
+            houts = [hout, torch.empty((nl_y, NXl), dtype=torch.float64).pin_memory()]
             tp = []
             for rep in range(2):
                 torch.cuda.synchronize()
@@ -286,20 +300,20 @@ def run_ours(args):
             g2.check()
             ok = bool(torch.equal(houts[0], houts[1]) and torch.equal(houts[0], hout))
             tpj = min(tp)
-            e2e.update({"value": round(J * NX * ny * nsw / (tpj * 1e-3) / 1e9, 3),
+            e2e.update({"value": round(J * NXl * ny * nsw / (tpj * 1e-3) / 1e9, 3),
                         "step": f"a stream of {J} user jobs through the C ABI on two grids / two CUDA streams (job j+1's "
                                 f"H2D copies overlap job j's sweeps); each job: b and x0 copied H2D from pinned host "
                                 f"memory, {nsw} sweeps (config 4's count), x copied D2H; timed from the first upload "
                                 f"to the last download; bytes per step = job bytes / {nsw}",
                         "jobs": J, "ms_per_job": round(tpj / J, 3), "outputs_identical": ok,
-                        "single_job": {"value": round(NX * ny * nsw / (t * 1e-3) / 1e9, 3), "ms": round(t, 3)}})
+                        "single_job": {"value": round(NXl * ny * nsw / (t * 1e-3) / 1e9, 3), "ms": round(t, 3)}})
             del g2, grids
 
     secondary = None
-    if world == 1 and not args.no_secondary:
+    if not args.no_secondary:
         del g
         torch.cuda.empty_cache()
-        secondary = run_secondary(args)
+        secondary = run_secondary(args) if world == 1 else run_secondary_slabs(args, world, rank, dev, comm)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -310,14 +324,20 @@ def run_ours(args):
             "metric": "lattice-point sweep updates/sec (GLUP/s), decomposed SOR sweep",
             "value": round(glups, 3), "unit": "GLUP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1) rhs, gen.py)",
-            "config": {"workload": "BASELINE config 4: 2D 5-point Poisson 16384 x 16384*N fp64, 64x64 boxes, "
-                                   "SOR omega_opt, row slabs per GPU",
-                       "n": [NX, ny], "tile": [T, T], "omega": omega, "parallelism": f"slab{world}",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1) rhs, gen.py)",
+            "config": {"workload": ("BASELINE config 4: 2D 5-point Poisson 16384 x 16384*N fp64 (weak scaling)"
+                                    if weak else "BASELINE config 4: 2D 5-point Poisson 16384 x 16384 fp64 split over N "
+                                                 "GPUs (strong scaling)") + ", 64x64 boxes, SOR omega_opt, row slabs per GPU",
+                       "n": [NXl, ny], "tile": [T, T], "omega": omega, "parallelism": f"slab{world}",
+                       "comm": None if world == 1 else f"in-library sw_comm ({args.comm}): 2 ghost layers per sweep, "
+                                                       f"exchanged behind the interior tile rows",
                        "l2": "inputs (2.1 GB per array) exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "k_sweep2p (decomposed SOR, 24 algorithmic B/LUP)", "peak_source": peak_src,
+                         "traffic_source": traffic_src if traffic is not None else None,
+                         "kernel": "k_sweep2p (decomposed SOR, 24 algorithmic B/LUP)" if world == 1 else
+                                   "one whole sweep per rank (k_sweep2p boundary + interior launches and the exchange)",
+                         "peak_source": peak_src,
                          "kernel_ms": round(kavg, 4), "kernel_ms_event_pair": round(kiso, 4)},
             "e2e": e2e,
             "gpu_launches": launches,
@@ -329,6 +349,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        del comm
         dist.destroy_process_group()
 
 
@@ -405,6 +426,15 @@ def run_secondary(args):
         dt = time.perf_counter() - t0
         out["c5_pcg_ilu0"] = {"n": [n3] * 3, "tile": [32, 8, 4], "iterations": it, "relres": rel, "converged": ok,
                               "seconds": round(dt, 3), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
+        # and SSOR(omega = 1, i.e. SGS; R-10)-PCG, the config's other preconditioner
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        it, rel, ok = g.pcg_solve(binding.PC_SSOR, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 5000)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["c5_pcg_ssor"] = {"n": [n3] * 3, "tile": [32, 8, 4], "omega": 1.0, "iterations": it, "relres": rel,
+                              "converged": ok, "seconds": round(dt, 3),
+                              "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
         g.mg_setup(7, 1, 0.35, 4, 1.0, 3)           # semi-coarsening in x and y (alpha_z = 0.01)
         g.mg_set_cycle(2)                           # W-cycle
         torch.cuda.synchronize()
@@ -481,6 +511,73 @@ def run_secondary(args):
     return out
 
 
+def k_slab_c5(seed, n3, z0, nz):
+    """Config 5's node diffusivities k = exp(0.5 N(0,1)) on the (n3 + 2)^3 ring grid (gen.lognormal_k),
+    cut to the layout sw_set_coefficients_k wants for the z slab [z0, z0 + nz): the one-node ring on
+    x and y, z coordinates z0 - 2 .. z0 + nz + 1 (ring rows outside 0 .. n3 + 1 are ignored: 1.0)."""
+    from paper_1008_3699_b200 import gen
+    m = n3 + 2
+    out = np.ones((nz + 4, m, m))
+    lo, hi = max(z0 - 1, 0), min(z0 + nz + 3, m)          # ring rows = coordinate + 1
+    rows = gen.normal(seed, gen.STREAM_LOGK, (hi - lo) * m * m, start=lo * m * m).reshape(hi - lo, m, m)
+    out[lo - (z0 - 1):hi - (z0 - 1)] = np.exp(0.5 * rows)
+    return out
+
+
+def run_secondary_slabs(args, world, rank, dev, comm):
+    """Config 5 slab-sharded over the N GPUs (BASELINE.json: "slab-sharded over 8 GPUs, SSOR- and
+    ILU(0)-preconditioned CG"): z slabs of 512 / N planes, boxes 32 x 8 x 4, the library's
+    communicator for the ghost layers and the rank-ordered reductions.  Sweep GLUP/s (all ranks'
+    nodes / max-over-ranks time), then ILU(0)- and SSOR(1)-PCG to 1e-8."""
+    import torch
+
+    from paper_1008_3699_b200 import binding, gen
+    n3 = 512
+    g = binding.Grid(3, (n3, n3, n3), binding.COEF_FACES, 0.0, dev).decompose((32, 8, 4), rank, world, comm)
+    z0, nz = g.slab_offset, g.n_local[2]
+    g.set_coefficients_k(k_slab_c5(args.seed, n3, z0, nz), (1.0, 0.1, 0.01))
+    b = gen.uniform(args.seed, gen.STREAM_RHS, nz * n3 * n3, start=z0 * n3 * n3).reshape(nz, n3, n3)
+    g.set_vector(binding.B, b / float((n3 + 1) ** 2))
+    out = {}
+    g.sor_sweep([1.0], 3, 0)
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.sor_sweep([1.0], 8, 3)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / 8
+    out["c5_sweep_slabs"] = {"n": [n3] * 3, "tile": [32, 8, 4], "ranks": world, "planes_per_rank": nz,
+                             "ms_per_sweep": round(ms, 3), "glups": round(n3 ** 3 / (ms * 1e-3) / 1e9, 2),
+                             "glups_per_gpu": round(n3 ** 3 / world / (ms * 1e-3) / 1e9, 2)}
+    if not args.no_c5_pcg:
+        for name, pc in (("ilu0", binding.PC_ILU0), ("ssor", binding.PC_SSOR)):
+            barrier(world)
+            t0 = time.perf_counter()
+            it, rel, ok = g.pcg_solve(pc, 1.0, binding.PAIR_SYMMETRIC, 1e-8, 5000)
+            torch.cuda.synchronize()
+            dt = max_over_ranks(time.perf_counter() - t0, world)
+            out[f"c5_pcg_{name}_slabs"] = {"ranks": world, "iterations": it, "relres": rel, "converged": ok,
+                                           "seconds": round(dt, 3), "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
+    del g
+    return out
+
+
+def host_cpu():
+    """CPU model and thread count of the host the oracle ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(seed, n, sweeps):
     """The oracle as it stands, single-threaded, on an n x n sample of the same workload."""
     import oracle as O
@@ -494,7 +591,7 @@ def cpu_baseline(seed, n, sweeps):
     dt = time.perf_counter() - t0
     return {"value": round(n * n * sweeps / dt / 1e9, 6), "unit": "GLUP/s", "cores": 1, "kind": "oracle",
             "sample": f"{sweeps} decomposed SOR sweeps on a {n}x{n} sub-grid (64x64 boxes), same per-node work",
-            "seconds": round(dt, 3)}
+            "seconds": round(dt, 3), "host": host_cpu()}
 
 
 def run_reference(args):
@@ -522,7 +619,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1) rhs, gen.py)",
             "config": {"workload": "BASELINE config 4 sweep, bounded CPU sample", "n": [n, n], "tile": [64, 64]},
             "cpu_baseline": {"value": round(v, 6), "unit": "GLUP/s", "cores": 1, "kind": "oracle",
-                             "sample": f"each step = 1 sweep of a {n}x{n} sub-grid of config 4"},
+                             "sample": f"each step = 1 sweep of a {n}x{n} sub-grid of config 4", "host": host_cpu()},
             "e2e": {"value": round(v, 6), "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -540,7 +637,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--no-c5-pcg", action="store_true", help="skip config 5's 512^3 PCG solve (about a minute)")
+    ap.add_argument("--no-c5-pcg", action="store_true", help="skip config 5's 512^3 PCG solves (about a minute)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="config 4 over N GPUs: weak = 16384 x 16384 per GPU, strong = 16384^2 split over N")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="N > 1 transport: nccl (one GPU per rank) or host (gloo staging; ranks may share a GPU, tests)")
+    ap.add_argument("--nx", type=int, default=NX, help="config 4 edge (tests only; the bench line is 16384)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -31,3 +31,16 @@ def test_bench_help_lists_the_driver_flags():
     assert out.returncode == 0
     for flag in ("--gpus", "--steps", "--warmup", "--impl"):
         assert flag in out.stdout
+
+
+def test_c5_slab_coefficients_match_the_single_grid_layout():
+    """bench.k_slab_c5 (config 5's k for one z slab, generated with counter offsets) equals the cut of
+    the single-grid array bench.py's one-GPU leg builds (gen.lognormal_k padded by one z layer)."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1008_3699_b200 import gen
+    n3 = 8
+    full = np.pad(gen.lognormal_k(3, (n3 + 2,) * 3, 0.5), [(1, 1), (0, 0), (0, 0)], constant_values=1.0)
+    for z0, nz in ((0, 4), (4, 4), (2, 2), (0, 8)):
+        assert np.array_equal(bench.k_slab_c5(3, n3, z0, nz), full[z0:z0 + nz + 4])
