@@ -356,93 +356,97 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         const double *__restrict__ f1b = (FACES ? A.f1 : A.xin) + gbase;
         const double *__restrict__ f2b = (FACES ? A.f2 : A.xin) + gbase;
         const bool need_x = !A.tri, need_aux = !A.tri || A.invd_mode;
-        const int NE = E0 * E1 * E2;
-        int l0 = tid % E0, l1 = (tid / E0) % E1, l2 = tid / (E0 * E1);
-        const int a0 = k3::NT % E0, a1 = (k3::NT / E0) % E1, a2 = k3::NT / (E0 * E1);
-        constexpr int KB = SW_KB;      // nodes per batch: all their loads are issued before any use
-        for (int e0 = tid; e0 < NE; e0 += KB * k3::NT) {
-            int cw_[KB], Lm[KB], o_[KB], mz[KB];
-            bool on[KB];
+        // Row-wise: a warp takes a row (local y, z) of the extended box and its lanes consecutive
+        // local x, so every address is the row's base plus the lane (one coalesced run per load)
+        // and the active / implicit-side / omega choices are row-uniform.  The column at local
+        // x = -1 (the partner layer across the x start face) is one extra node per row.
+        struct In {
+            double f[3][2], xn[3], xo, av;
+        };
+        auto load = [&](bool on, int o, int L, In &v) {
+            if (!on) return;
+            if (FACES) {
+                v.f[0][0] = __ldg(f0b + o); v.f[0][1] = __ldg(f0b + o + 1);
+                v.f[1][0] = __ldg(f1b + o); v.f[1][1] = __ldg(f1b + o + P0i);
+                v.f[2][0] = __ldg(f2b + o); v.f[2][1] = __ldg(f2b + o + P01i);
+            } else {
 #pragma unroll
-            for (int kb = 0; kb < KB; ++kb) {
-                const int L = (l0 < 1 ? 1 : 0) | (l1 < 1 ? 2 : 0) | (l2 < 1 ? 4 : 0);
-                Lm[kb] = L;
-                on[kb] = l2 < E2 && (L & cb) == L;
-                cw_[kb] = l2 < E2 ? l0 + RS * l1 + PS * l2 : -1;
-                // which coordinates are 0 (cut test) packed in 3 bits
-                mz[kb] = (l0 == 1 ? 1 : 0) | (l1 == 1 ? 2 : 0) | (l2 == 1 ? 4 : 0);
-                o_[kb] = on[kb] ? O0 + (l0 - 1) * d[0] + (l1 - 1) * d[1] + (l2 - 1) * d[2] : O0;
-                l0 += a0;
-                const int c0 = l0 >= E0;
-                l0 -= c0 ? E0 : 0;
-                l1 += a1 + c0;
-                const int c1 = l1 >= E1;
-                l1 -= c1 ? E1 : 0;
-                l2 += a2 + c1;
+                for (int a = 0; a < 3; ++a) v.f[a][0] = v.f[a][1] = 1.0;
             }
-            double f[KB][3][2], xn[KB][3], xo[KB], av[KB];
+            v.xo = __ldg(xb + o);
+            v.av = need_aux ? __ldg(ab + o) : 0.0;
 #pragma unroll
-            for (int kb = 0; kb < KB; ++kb) {
-                const int o = o_[kb];
-                if (!on[kb]) {                        // layer across an uncoupled face: never read
+            for (int a = 0; a < 3; ++a) {
+                const bool hi = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
+                v.xn[a] = need_x ? __ldg(xb + (hi ? o - Sgi[a] : o + Sgi[a])) : 0.0;
+            }
+        };
+        // r0 and the couplings alpha c toward the implicit sides (DESIGN R-7), zeros if inactive
+        auto put = [&](bool on, int e, int L, int mz, const In &v) {
+            double r0 = 0.0, c[3] = {0.0, 0.0, 0.0};
+            if (on) {
+                const double ap = (((v.f[0][0] + v.f[0][1]) + (v.f[1][0] + v.f[1][1])) + (v.f[2][0] + v.f[2][1])) + G.beta;
+                bool hi[3];
 #pragma unroll
-                    for (int a = 0; a < 3; ++a) f[kb][a][0] = f[kb][a][1] = xn[kb][a] = 0.0;
-                    xo[kb] = av[kb] = 0.0;
-                    continue;
-                }
-                if (FACES) {
-                    f[kb][0][0] = __ldg(f0b + o); f[kb][0][1] = __ldg(f0b + o + 1);
-                    f[kb][1][0] = __ldg(f1b + o); f[kb][1][1] = __ldg(f1b + o + P0i);
-                    f[kb][2][0] = __ldg(f2b + o); f[kb][2][1] = __ldg(f2b + o + P01i);
+                for (int a = 0; a < 3; ++a) hi[a] = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);
+                double al;
+                if (!A.tri) {
+                    const double w_ = A.omega[sb ^ L];             // the node's own box's direction bits
+                    al = div_rn(w_, ap);
+                    double ev = v.av;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) ev = fma(hi[a] ? v.f[a][0] : v.f[a][1], v.xn[a], ev);
+                    r0 = fma(al, ev, (1.0 - w_) * v.xo);
                 } else {
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) f[kb][a][0] = f[kb][a][1] = 1.0;
+                    al = A.invd_mode ? v.av : div_rn(A.omega[0], ap);
+                    r0 = A.rscale ? al * v.xo : A.coef * v.xo;
                 }
-                xo[kb] = __ldg(xb + o);
-                av[kb] = need_aux ? __ldg(ab + o) : 0.0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const bool hi = (((Lm[kb] >> a) & 1) != 0) != (((sb >> a) & 1) != 0);   // implicit side is global +a
-                    xn[kb][a] = need_x ? __ldg(xb + (hi ? o - Sgi[a] : o + Sgi[a])) : 0.0;
+                    // no coupling across an uncoupled start face: the oracle omits the term (physical
+                    // boundary) and the first pass of the transposed solve must not see the neighbour box
+                    const bool cut = !((L >> a) & 1) && ((mz >> a) & 1) && !((cb >> a) & 1);
+                    c[a] = cut ? 0.0 : al * (hi[a] ? v.f[a][1] : v.f[a][0]);
                 }
             }
+            X[e] = r0;
+            C0[e] = c[0];
+            C1[e] = c[1];
+            C2[e] = c[2];
+        };
+        const int warp = tid >> 5, lane = tid & 31;
+        const int NR = E1 * E2, NC = (T0 + 31) >> 5, NI = NR * NC;
+        // items (row, 32-wide x chunk), two per warp in flight
+        for (int it = warp; it < NI; it += 2 * (k3::NT / 32)) {
+            In v[2];
+            int e_[2], L_[2], mz_[2];
+            bool on_[2];
 #pragma unroll
-            for (int kb = 0; kb < KB; ++kb) {
-                const int e = cw_[kb];
-                if (e < 0) break;
-                const int L = Lm[kb];
-                double r0 = 0.0, c[3] = {0.0, 0.0, 0.0};
-                if (on[kb]) {
-                    const double(&fk)[3][2] = f[kb];
-                    const double ap = (((fk[0][0] + fk[0][1]) + (fk[1][0] + fk[1][1])) + (fk[2][0] + fk[2][1])) + G.beta;
-                    bool hi[3];
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) hi[a] = (((L >> a) & 1) != 0) != (((sb >> a) & 1) != 0);
-                    double al;
-                    if (!A.tri) {
-                        const double w_ = A.omega[sb ^ L];             // the node's own box's direction bits
-                        al = div_rn(w_, ap);
-                        double ev = av[kb];
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) ev = fma(hi[a] ? fk[a][0] : fk[a][1], xn[kb][a], ev);
-                        r0 = fma(al, ev, (1.0 - w_) * xo[kb]);
-                    } else {
-                        al = A.invd_mode ? av[kb] : div_rn(A.omega[0], ap);
-                        r0 = A.rscale ? al * xo[kb] : A.coef * xo[kb];
-                    }
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        // no coupling across an uncoupled start face: the oracle omits the term (physical
-                        // boundary) and the first pass of the transposed solve must not see the neighbour box
-                        const bool cut = !((L >> a) & 1) && ((mz[kb] >> a) & 1) && !((cb >> a) & 1);
-                        c[a] = cut ? 0.0 : al * (hi[a] ? fk[a][1] : fk[a][0]);
-                    }
-                }
-                X[e] = r0;
-                C0[e] = c[0];
-                C1[e] = c[1];
-                C2[e] = c[2];
+            for (int h = 0; h < 2; ++h) {
+                const int item = it + h * (k3::NT / 32);
+                const int row = item / NC, lx = (item % NC) * 32 + lane;
+                const int l1 = row % E1, l2 = row / E1;
+                const int L = (l1 < 1 ? 2 : 0) | (l2 < 1 ? 4 : 0);
+                const bool live = item < NI && lx < T0;
+                on_[h] = live && (L & cb) == L;
+                e_[h] = live ? (lx + 1) + RS * l1 + PS * l2 : -1;
+                L_[h] = L;
+                mz_[h] = (lx == 0 ? 1 : 0) | (l1 == 1 ? 2 : 0) | (l2 == 1 ? 4 : 0);
+                load(on_[h], O0 + lx * d[0] + (l1 - 1) * d[1] + (l2 - 1) * d[2], L, v[h]);
             }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (e_[h] >= 0) put(on_[h], e_[h], L_[h], mz_[h], v[h]);
+        }
+        // the column local x = -1 of every row
+        for (int row = tid; row < NR; row += k3::NT) {
+            const int l1 = row % E1, l2 = row / E1;
+            const int L = 1 | (l1 < 1 ? 2 : 0) | (l2 < 1 ? 4 : 0);
+            const bool on = (L & cb) == L;
+            const int mz = (l1 == 1 ? 2 : 0) | (l2 == 1 ? 4 : 0);
+            In v;
+            load(on, O0 - d[0] + (l1 - 1) * d[1] + (l2 - 1) * d[2], L, v);
+            put(on, RS * l1 + PS * l2, L, mz, v);
         }
         // the padding slots (x beyond E0 in every row, rows beyond E1 in every plane): zeros
         const int rp = RS - E0, pp = PS - RS * E1;
@@ -712,22 +716,18 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     SW_TADD(3, t_sets, t_levels);
 
     // ---------------------------------------------------------------- 4. write-back of the box
+    // row-wise like the prologue: a warp per (local y, z) row, lanes along x (one coalesced run)
     {
-        const int n = T0 * T1 * T2;
-        int l0 = tid % T0, l1 = (tid / T0) % T1, l2 = tid / (T0 * T1);
-        const int a0 = k3::NT % T0, a1 = (k3::NT / T0) % T1, a2 = k3::NT / (T0 * T1);
-        for (int e = tid; e < n; e += k3::NT) {
-            const int w0 = 2 + (((sb >> 0) & 1) ? T0 - 1 - l0 : l0);
-            const int w1 = 2 + (((sb >> 1) & 1) ? T1 - 1 - l1 : l1);
-            const int w2 = 2 + (((sb >> 2) & 1) ? T2 - 1 - l2 : l2);
-            A.out[gbase + w0 + (int64_t)w1 * P0 + (int64_t)w2 * P01] = X[wof(l0, l1, l2)];
-            l0 += a0;
-            const int c0 = l0 >= T0;
-            l0 -= c0 ? T0 : 0;
-            l1 += a1 + c0;
-            const int c1 = l1 >= T1;
-            l1 -= c1 ? T1 : 0;
-            l2 += a2 + c1;
+        const int warp = tid >> 5, lane = tid & 31;
+        const int NC = (T0 + 31) >> 5, NI = T1 * T2 * NC;
+        const int64_t d1 = ((sb >> 1) & 1) ? -P0 : P0, d2 = ((sb >> 2) & 1) ? -P01 : P01;
+        const int d0 = (sb & 1) ? -1 : 1;
+        double *const ob = A.out + gbase + (2 + ((sb & 1) ? T0 - 1 : 0)) + (2 + (((sb >> 1) & 1) ? T1 - 1 : 0)) * P0 +
+                           (2 + (((sb >> 2) & 1) ? T2 - 1 : 0)) * P01;
+        for (int item = warp; item < NI; item += k3::NT / 32) {
+            const int row = item / NC, lx = (item % NC) * 32 + lane;
+            const int l1 = row % T1, l2 = row / T1;
+            if (lx < T0) ob[lx * d0 + l1 * d1 + l2 * d2] = X[wof(lx, l1, l2)];
         }
     }
     SW_TMARK(t_end);
