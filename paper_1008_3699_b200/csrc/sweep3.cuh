@@ -432,7 +432,14 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                 e_[h] = live ? (lx + 1) + RS * l1 + PS * l2 : -1;
                 L_[h] = L;
                 mz_[h] = (lx == 0 ? 1 : 0) | (l1 == 1 ? 2 : 0) | (l2 == 1 ? 4 : 0);
+#ifdef SW_EXP_NOLOAD
+                if (on_[h]) {
+                    for (int a = 0; a < 3; ++a) v[h].f[a][0] = v[h].f[a][1] = 1.0 + 0.01 * a, v[h].xn[a] = 0.5;
+                    v[h].xo = 0.25; v[h].av = 0.125;
+                }
+#else
                 load(on_[h], O0 + lx * d[0] + (l1 - 1) * d[1] + (l2 - 1) * d[2], L, v[h]);
+#endif
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -513,7 +520,9 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     const int ncpl = __popc(cb);
     if (ncpl >= 2) {
         if (cb == 7) {
+#ifndef SW_EXP_NOCORNER
             if (lt < 32) corner8_coop(X, WS, SCR, lt, wof(0, 0, 0), st, sb, A.flag);
+#endif
         } else if (lt == 0) {
             const int w = wof(0, 0, 0);
             switch (cb) {
@@ -547,7 +556,11 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     // ---------------------------------------------------------------- 3. level loop (warp 0)
     if (fast_lines) {
         // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over d = j + k
+#ifdef SW_EXP_NOSHEET
+        if (false) {
+#else
         if (lt < 32 && (cb & 1)) {
+#endif
             const int j = lt % T1, k = lt / T1;
             const bool on = lt < T1 * T2;
             const int m = 1 | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
@@ -629,6 +642,9 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
             };
             // the edge lane's loads of x-edge set `need` wait until warp 1 has stored it
             auto wait_edge = [&](int need) {
+#ifdef SW_EXP_NOWAIT
+                return;
+#endif
                 if (conc_x && need < T0) {
                     int got;
                     do {
