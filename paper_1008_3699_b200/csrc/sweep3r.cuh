@@ -14,7 +14,7 @@
 //   warp 2     box q's corner set, y- and z-edge chains, x-face sheet (and its write-back), and the
 //              y/z-sheet pair data per chunk of columns;
 //   warps 3-4  producers: r0 and the couplings of box q+1, chunk by chunk of compact x-columns
-//              [0,9), [9,17), [17,25), [25,33), each chunk as soon as box q's wavefront has read its
+//              [0,2), [2,10), [10,18), [18,26), [26,33), each chunk as soon as box q's wavefront has read its
 //              columns for the last time (lane j + k = D reads column c last at step c - 1 + D).
 // Progress is exchanged through monotone counters in shared memory (st.release / ld.acquire; a box
 // q adds q * BASE), so every wait is a spin on a flag of the same CTA.  The x = 0 column of a box
@@ -42,21 +42,37 @@ __device__ __forceinline__ int ld_acq(const int *p) {
 __device__ __forceinline__ void st_rel(int *p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
-// every lane of the calling warp spins until *p >= v (a broadcast shared load)
-__device__ __forceinline__ void wait_ge(const int *p, int v) {
+// every lane of the calling warp spins until *p >= v (a broadcast shared load); with SW_TRACE the
+// cycles waited are added to *acc
+__device__ __forceinline__ void wait_ge(const int *p, int v, long long *acc = nullptr) {
     if (ld_acq(p) < v) {
+#ifdef SW_TRACE
+        const long long t0 = sw_clock();
+#endif
         do {
             __nanosleep(20);
         } while (ld_acq(p) < v);
+#ifdef SW_TRACE
+        if (acc) *acc += sw_clock() - t0;
+#endif
     }
     SW_JITTER_POINT();
 }
+#ifdef SW_TRACE
+#define SW_T3(var) const long long var = sw_clock()
+#define SW_T3ADD(slot, a) tr[slot] += sw_clock() - (a)
+#else
+#define SW_T3(var)
+#define SW_T3ADD(slot, a)
+#endif
 
-// first compact column of chunk k (chunk 0 = compact [0, 1 + CW): local x = -1 .. CW - 1)
+// first compact column of chunk k: chunk 0 = compact [0, 2) (local x = -1, 0: everything the corner,
+// the y / z edges and the x-sheet need, so they can start early), then CW columns per chunk
 __device__ __forceinline__ int chunk_start(int k, int E0) {
-    const int c = k == 0 ? 0 : 1 + k3r::CW * k;
+    const int c = k == 0 ? 0 : 2 + k3r::CW * (k - 1);
     return c < E0 ? c : E0;
 }
+__device__ __forceinline__ int chunk_count(int E0) { return 1 + (E0 - 2 + k3r::CW - 1) / k3r::CW; }
 
 struct Box3i {
     int sb, cb;
@@ -126,7 +142,7 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NS = T0 + T1 + T2 - 2;        // wavefront steps
     const int D = T1 + T2 - 2;              // largest j + k of a line
-    const int nch = (E0 - 1 + k3r::CW - 1) / k3r::CW;
+    const int nch = chunk_count(E0);
     const int64_t P0 = G.P0, P01 = G.P01;
     // boxes of this CTA: b = blockIdx.x + q gridDim.x
     const int nq = (int)((nbox - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -143,6 +159,8 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
         s_xe = 0;
     }
     __syncthreads();
+    long long tr[16] = {0};                 // SW_TRACE: per-role wait / busy cycles (lane 0 of each role)
+    SW_T3(t_begin);
 
     if (warp >= k3r::PW0) {
         // ============================================================ producers
@@ -169,7 +187,7 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
             for (int k = 0; k < nch; ++k) {
                 const int c0 = chunk_start(k, E0), c1 = chunk_start(k + 1, E0), ncol = c1 - c0;
                 // box q-1's wavefront has read columns < c1 for the last time
-                if (q > 0) wait_ge(&s_wf, (q - 1) * k3r::BASE + min(c1 + D, NS));
+                if (q > 0) wait_ge(&s_wf, (q - 1) * k3r::BASE + min(c1 + D, NS), &tr[0]);
                 const int n = E1 * E2 * ncol;
                 constexpr int KB = 2;
                 for (int n0 = pt; n0 < n; n0 += KB * k3r::NPT) {
@@ -279,8 +297,9 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                 }
                 if (fl) atomicOr(A.flag, 1);
             };
-            wait_ge(&s_prod, qb + 1);                                   // chunk 0 of box q
+            wait_ge(&s_prod, qb + 1, &tr[2]);                           // chunk 0 of box q
             __syncwarp();
+            SW_T3(t_sets0);
             // x-sheet pair data (x = 0 column): 1 / pivot, m_ab, m_ba
             if (cb & 1) {
                 int fl = 0;
@@ -318,6 +337,8 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                 if ((cb & 5) == 5) edge_chain_w<5>(X, WS, lane, T1, wof(0, 1, 0), st[1], st, sb, A.flag);
                 if ((cb & 3) == 3) edge_chain_w<3>(X, WS, lane, T2, wof(0, 0, 1), st[2], st, sb, A.flag);
             }
+            SW_T3ADD(4, t_sets0);
+            SW_T3(t_sheet0);
             // the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over d = j + k, and the
             // write-back of the box's x = 0 column (the wavefront starts at x = 1)
             if (cb & 1) {
@@ -349,13 +370,14 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                 }
                 __syncwarp();
             }
+            SW_T3ADD(5, t_sheet0);
             if (lane == 0) {
                 st_rel(&s_pd, qb + 1);
                 st_rel(&s_set, q + 1);
             }
             // the other chunks' pair data, as the producers deliver them
             for (int k = 1; k < nch; ++k) {
-                wait_ge(&s_prod, qb + k + 1);
+                wait_ge(&s_prod, qb + k + 1, &tr[3]);
                 __syncwarp();
                 pair_data(chunk_start(k, E0) - 1, chunk_start(k + 1, E0) - 1);
                 __syncwarp();
@@ -369,9 +391,9 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
             const int sb = bx.sb, cb = bx.cb;
             const int qb = q * k3r::BASE;
             if ((cb & 6) != 6) continue;
-            wait_ge(&s_set, q + 1);                 // the corner set (set 0) is in place
+            wait_ge(&s_set, q + 1, &tr[6]);         // the corner set (set 0) is in place
             for (int k = 0; k < nch; ++k) {
-                wait_ge(&s_prod, qb + k + 1);
+                wait_ge(&s_prod, qb + k + 1, &tr[7]);
                 __syncwarp();
                 const int t0 = max(chunk_start(k, E0) - 1, 1), t1 = min(chunk_start(k + 1, E0) - 1, T0);
                 Fac4 F;
@@ -397,7 +419,7 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
             const int sb = bx.sb, cb = bx.cb;
             const int qb = q * k3r::BASE;
             const bool conc_x = (cb & 6) == 6;
-            wait_ge(&s_set, q + 1);
+            wait_ge(&s_set, q + 1, &tr[9]);
             __syncwarp();
             const int nl = T1 * T2;
             const bool on = lane < nl;
@@ -426,7 +448,7 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                 if (s + 1 >= ready && ready < E0) {
                     int kk = 1;
                     while (chunk_start(kk + 1, E0) <= s + 1 && kk + 1 < nch) ++kk;
-                    wait_ge(&s_pd, qb + kk + 1);
+                    wait_ge(&s_pd, qb + kk + 1, &tr[10]);
                     ready = chunk_start(kk + 1, E0);
                 }
                 const int i = s - j - k;
@@ -459,7 +481,7 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                 pz = zpair ? pv : v.ez;
             };
             auto wait_edge = [&](int need) {
-                if (conc_x && need < T0) wait_ge(&s_xe, qb + need);
+                if (conc_x && need < T0) wait_ge(&s_xe, qb + need, &tr[11]);
             };
             Ld va, vb;
             __syncwarp();
@@ -481,6 +503,18 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
             if (lane == 0) st_rel(&s_wf, qb + NS);
         }
     }
+#ifdef SW_TRACE
+    // roles: 0 producer wait, 1 producer total, 2/3 warp 2 waits, 4 sets, 5 sheet, 6/7 warp 1 waits,
+    // 9/10/11 wavefront waits, 12 wavefront total, 13 warp 2 total, 14 warp 1 total, 15 boxes
+    const long long tot = sw_clock() - t_begin;
+    if (lane == 0 && (warp <= 2 || tid == k3r::PW0 * 32)) {
+        const int role_tot = warp == 0 ? 12 : (warp == 1 ? 14 : (warp == 2 ? 13 : 1));
+        tr[role_tot] = tot;
+        if (warp == 0) tr[15] = nq;
+        for (int i = 0; i < 16; ++i)
+            if (tr[i]) atomicAdd(&sw_trace_sum[i], (unsigned long long)tr[i]);
+    }
+#endif
 }
 
 inline bool sweep3r_supported(const Geo &G) {
@@ -489,15 +523,21 @@ inline bool sweep3r_supported(const Geo &G) {
 
 template <bool FACES, int SHAPE>
 inline void launch_sweep3r_t(const Sweep3Args &A, size_t smem, int64_t nbox, cudaStream_t s) {
-    static int ctas = 0;
-    if (!ctas) {
-        cudaFuncSetAttribute(k_sweep3r<FACES, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 148, per = 0;
+    static int sms = 0;
+    static size_t last_smem = 0;
+    static int per = 1;
+    if (!sms) {
+        cudaFuncSetAttribute(k_sweep3r<FACES, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep3r<FACES, SHAPE>, k3r::NT, smem);
-        ctas = sms * (per > 0 ? per : 1);
     }
+    if (smem != last_smem) {        // persistent grid: every resident CTA slot of the device
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep3r<FACES, SHAPE>, k3r::NT, smem);
+        if (per < 1) per = 1;
+        last_smem = smem;
+    }
+    const int64_t ctas = (int64_t)sms * per;
     const int64_t grid = nbox < ctas ? nbox : ctas;
     k_sweep3r<FACES, SHAPE><<<(unsigned)grid, k3r::NT, smem, s>>>(A, nbox);
 }
