@@ -524,13 +524,16 @@ inline bool sweep3r_supported(const Geo &G) {
 template <bool FACES, int SHAPE>
 inline void launch_sweep3r_t(const Sweep3Args &A, size_t smem, int64_t nbox, cudaStream_t s) {
     static int sms = 0;
-    static size_t last_smem = 0;
+    static size_t last_smem = 0, attr_smem = 0;
     static int per = 1;
     if (!sms) {
-        cudaFuncSetAttribute(k_sweep3r<FACES, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (smem > attr_smem) {
+        cudaFuncSetAttribute(k_sweep3r<FACES, SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_smem = smem;
     }
     if (smem != last_smem) {        // persistent grid: every resident CTA slot of the device
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep3r<FACES, SHAPE>, k3r::NT, smem);
