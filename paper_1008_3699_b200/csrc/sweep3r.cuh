@@ -42,6 +42,15 @@ __device__ __forceinline__ int ld_acq(const int *p) {
 __device__ __forceinline__ void st_rel(int *p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
+// Progress of the wavefront (a write-after-read hand-off: the producers may overwrite columns the
+// wavefront has finished reading).  A release store here would compile to MEMBAR.ALL.CTA, which
+// waits for the wavefront's outstanding global stores of the results; the reads it must order
+// are shared loads whose values were consumed by the steps that preceded the store (register
+// dependences: every load of a released column fed a shuffle or FMA of an earlier, completed
+// step), so a relaxed store suffices.
+__device__ __forceinline__ void st_progress(int *p, int v) {
+    asm volatile("st.relaxed.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 // every lane of the calling warp spins until *p >= v (a broadcast shared load); with SW_TRACE the
 // cycles waited are added to *acc
 __device__ __forceinline__ void wait_ge(const int *p, int v, long long *acc = nullptr) {
@@ -49,8 +58,10 @@ __device__ __forceinline__ void wait_ge(const int *p, int v, long long *acc = nu
 #ifdef SW_TRACE
         const long long t0 = sw_clock();
 #endif
+        unsigned ns = 32;
         do {
-            __nanosleep(20);
+            __nanosleep(ns);
+            ns = ns < 512 ? 2 * ns : 512;
         } while (ld_acq(p) < v);
 #ifdef SW_TRACE
         if (acc) *acc += sw_clock() - t0;
@@ -362,18 +373,25 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                     }
                     __syncwarp();
                 }
-                if (on) {
-                    const int64_t d1 = ((sb >> 1) & 1) ? -P0 : P0, d2 = ((sb >> 2) & 1) ? -P01 : P01;
-                    double *const ob = A.out + bx.gbase + (2 + ((sb & 1) ? T0 - 1 : 0)) +
-                                       (2 + (((sb >> 1) & 1) ? T1 - 1 : 0)) * P0 + (2 + (((sb >> 2) & 1) ? T2 - 1 : 0)) * P01;
-                    ob[j * d1 + k * d2] = X[w];
-                }
                 __syncwarp();
             }
             SW_T3ADD(5, t_sheet0);
+            // the x = 0 column's values: read before the release (they stay in place until the
+            // wavefront of box q is past column 1), stored to global after it (a release would
+            // otherwise wait for these global stores)
+            double x0v = 0.0;
+            const bool wr0 = (cb & 1) && lane < T1 * T2;
+            if (wr0) x0v = X[wof(0, lane % T1, lane / T1)];
+            __syncwarp();
             if (lane == 0) {
                 st_rel(&s_pd, qb + 1);
                 st_rel(&s_set, q + 1);
+            }
+            if (wr0) {
+                const int64_t d1 = ((sb >> 1) & 1) ? -P0 : P0, d2 = ((sb >> 2) & 1) ? -P01 : P01;
+                double *const ob = A.out + bx.gbase + (2 + ((sb & 1) ? T0 - 1 : 0)) +
+                                   (2 + (((sb >> 1) & 1) ? T1 - 1 : 0)) * P0 + (2 + (((sb >> 2) & 1) ? T2 - 1 : 0)) * P01;
+                ob[(lane % T1) * d1 + (lane / T1) * d2] = x0v;
             }
             // the other chunks' pair data, as the producers deliver them
             for (int k = 1; k < nch; ++k) {
@@ -496,11 +514,11 @@ __global__ void __launch_bounds__(k3r::NT, 4) k_sweep3r(Sweep3Args A, int64_t nb
                 ld(s + 2, va);
                 step(s + 1, vb);
                 __syncwarp();
-                if (lane == 0) st_rel(&s_wf, qb + s + 2);
+                if (lane == 0) st_progress(&s_wf, qb + s + 2);
             }
             if (s < NS) step(s, va);
             __syncwarp();
-            if (lane == 0) st_rel(&s_wf, qb + NS);
+            if (lane == 0) st_progress(&s_wf, qb + NS);
         }
     }
 #ifdef SW_TRACE
