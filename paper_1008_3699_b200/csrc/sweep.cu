@@ -19,7 +19,6 @@
 #include "sweep2v.cuh"
 #include "tri2t.cuh"
 #include "sweep3.cuh"
-#include "sweep3r.cuh"
 #include "tri3t.cuh"
 #include "mg.cuh"
 #include "comm.cuh"
@@ -82,7 +81,6 @@ struct sw_grid {
     int64_t factor_phase = 0;
     int64_t launches = 0;
     int fast2d = 1;
-    int roll3 = 1;                         // 3D: the rolling warp-specialised kernel where it applies (SW_NO_ROLL=1: k_sweep3)
     Maps2d maps;
     struct MapEntry {
         const void *ptr;
@@ -208,8 +206,6 @@ extern "C" sw_status sw_create_grid(int dim, const int64_t n[3], sw_coef kind, d
     g->dev = cuda_device;
     const char *env = getenv("SW_DISABLE_FAST2D");   // 1: the level-synchronous generic kernel only
     if (env && env[0] == '1') g->fast2d = 0;
-    const char *nr = getenv("SW_NO_ROLL");
-    if (nr && nr[0] == '1') g->roll3 = 0;
     *out = g;
     return SW_OK;
 }
@@ -634,7 +630,7 @@ static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double 
         A3.out = xn;
         A3.flag = g->flag;
         A3.couple = 1;
-        cudaError_t e = g->roll3 && sweep3r_supported(G) ? launch_sweep3r(A3, cs) : launch_sweep3(A3, cs);
+        cudaError_t e = launch_sweep3(A3, cs);
         g->launches++;
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
         return SW_OK;
@@ -856,7 +852,7 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
         } else {
             A3.base = rev; A3.rscale = 0; A3.coef = coef; A3.couple = pairing == SW_PAIR_PAPER; A3.out = z;
         }
-        cudaError_t e = g->roll3 && sweep3r_supported(g->G) ? launch_sweep3r(A3, s) : launch_sweep3(A3, s);
+        cudaError_t e = launch_sweep3(A3, s);
         g->launches++;
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3 launch: ") + cudaGetErrorString(e));
         return SW_OK;

@@ -416,13 +416,15 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
         };
         const int warp = tid >> 5, lane = tid & 31;
         const int NR = E1 * E2, NC = (T0 + 31) >> 5, NI = NR * NC;
-        // items (row, 32-wide x chunk), two per warp in flight
-        for (int it = warp; it < NI; it += 2 * (k3::NT / 32)) {
-            In v[2];
-            int e_[2], L_[2], mz_[2];
-            bool on_[2];
+        // items (row, 32-wide x chunk), two per warp in flight (3 / 4 / 6: 22.5 / 20.4 / 16.7 against
+        // 23.2 GLUP/s at 512^3: more loads in flight do not shorten the prologue)
+        constexpr int RB = 2;
+        for (int it = warp; it < NI; it += RB * (k3::NT / 32)) {
+            In v[RB];
+            int e_[RB], L_[RB], mz_[RB];
+            bool on_[RB];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < RB; ++h) {
                 const int item = it + h * (k3::NT / 32);
                 const int row = item / NC, lx = (item % NC) * 32 + lane;
                 const int l1 = row % E1, l2 = row / E1;
@@ -432,17 +434,10 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
                 e_[h] = live ? (lx + 1) + RS * l1 + PS * l2 : -1;
                 L_[h] = L;
                 mz_[h] = (lx == 0 ? 1 : 0) | (l1 == 1 ? 2 : 0) | (l2 == 1 ? 4 : 0);
-#ifdef SW_EXP_NOLOAD
-                if (on_[h]) {
-                    for (int a = 0; a < 3; ++a) v[h].f[a][0] = v[h].f[a][1] = 1.0 + 0.01 * a, v[h].xn[a] = 0.5;
-                    v[h].xo = 0.25; v[h].av = 0.125;
-                }
-#else
                 load(on_[h], O0 + lx * d[0] + (l1 - 1) * d[1] + (l2 - 1) * d[2], L, v[h]);
-#endif
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < RB; ++h)
                 if (e_[h] >= 0) put(on_[h], e_[h], L_[h], mz_[h], v[h]);
         }
         // the column local x = -1 of every row
@@ -520,9 +515,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     const int ncpl = __popc(cb);
     if (ncpl >= 2) {
         if (cb == 7) {
-#ifndef SW_EXP_NOCORNER
             if (lt < 32) corner8_coop(X, WS, SCR, lt, wof(0, 0, 0), st, sb, A.flag);
-#endif
         } else if (lt == 0) {
             const int w = wof(0, 0, 0);
             switch (cb) {
@@ -556,11 +549,7 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
     // ---------------------------------------------------------------- 3. level loop (warp 0)
     if (fast_lines) {
         // (a) the x-face sheet (pairs (0, j, k) / (-1, j, k)), a 2D recurrence over d = j + k
-#ifdef SW_EXP_NOSHEET
-        if (false) {
-#else
         if (lt < 32 && (cb & 1)) {
-#endif
             const int j = lt % T1, k = lt / T1;
             const bool on = lt < T1 * T2;
             const int m = 1 | (j == 0 ? (cb & 2) : 0) | (k == 0 ? (cb & 4) : 0);
@@ -642,9 +631,6 @@ __global__ void __launch_bounds__(k3::NT, 4) k_sweep3(Sweep3Args A) {
             };
             // the edge lane's loads of x-edge set `need` wait until warp 1 has stored it
             auto wait_edge = [&](int need) {
-#ifdef SW_EXP_NOWAIT
-                return;
-#endif
                 if (conc_x && need < T0) {
                     int got;
                     do {
