@@ -69,6 +69,8 @@ def lib():
         L.or_faces_from_k.argtypes = [I, P, P, P, P]
         L.or_node_info.argtypes = [P, I64, I, P, P]
         L.or_base_bits.argtypes = [I, I64, I]
+        L.or_eik_sweep.argtypes = [P, I64, I, P, D, P, P]
+        L.or_eik_classical.argtypes = [P, I, P, D, P]
     return _lib
 
 
@@ -284,3 +286,23 @@ def scc_stats(pb: Problem, phase: int = 0, override: int = -1):
     L.or_scc_stats.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
     _check(L.or_scc_stats(ctypes.byref(g), int(phase), int(override), hist, nnz), "scc_stats")
     return {s: (hist[s], nnz[s]) for s in range(1, 9) if hist[s]}
+
+
+# ---------------------------------------------------------------- eikonal
+def eik_sweep(pb: Problem, f, h: float, u_old, phase: int = 0, override: int = -1):
+    """One decomposed fast-sweeping pass for |grad u| = f (Godunov update, coupled sets solved
+    exactly by ordered fixing; DESIGN R-E1..R-E3).  2D / 1D."""
+    g = pb.struct()
+    u = np.empty(pb.shape)
+    _check(lib().or_eik_sweep(ctypes.byref(g), int(phase), int(override), _ptr(_arr(f, pb.shape)), float(h),
+                              _ptr(_arr(u_old, pb.shape)), _ptr(u)), "eik_sweep")
+    return u
+
+
+def eik_classical(pb: Problem, corner: int, f, h: float, u):
+    """Textbook in-place fast-sweeping pass from `corner` (Zhao 2005); ignores boxes."""
+    g = pb.struct()
+    uu = np.array(_arr(u, pb.shape), copy=True)
+    _check(lib().or_eik_classical(ctypes.byref(g), int(corner), _ptr(_arr(f, pb.shape)), float(h), _ptr(uu)),
+           "eik_classical")
+    return uu

@@ -708,3 +708,174 @@ int or_scc_stats(const or_grid *g, int64_t phase, int ov, int64_t hist[9], int64
     ctx_free(&x);
     return st;
 }
+
+/* ------------------------------------------------------- eikonal
+ * Parallel fast sweeping for the eikonal equation |grad u| = f on the multi-frontal
+ * schedule.  The paper names this application and defers it to a
+ * supplementary paper that is not available here, so the local update is the standard
+ * fast-sweeping rule (Godunov upwind discretisation, Zhao 2005), reading R-E1 of
+ * DESIGN.md:
+ *   a = min of the two x-neighbours, b = min of the two y-neighbours (a node outside the
+ *   grid counts +inf), fh = f_p * h,
+ *   ubar = +inf                                   if min(a, b) = +inf
+ *        = min(a, b) + fh                         if |a - b| >= fh
+ *        = ((a + b) + sqrt(2 fh^2 - (a - b)^2)) / 2   otherwise,
+ *   evaluated as d = a - b, disc = fma(-d, d, 2 (fh fh)), 0.5 ((a + b) + sqrt(disc));
+ *   u_p <- min(u_p, ubar).
+ * Sources carry u = 0 and keep it (min(0, ubar >= 0) = 0); every other node starts +inf.
+ * The decomposed sweep takes neighbours' NEW values on the start side of the node's box
+ * and OLD values on the end side (exactly the implicit / explicit split of the SOR sweep,
+ * reading R-E2), so the coupled sets at start-start faces are the SOR sweep's SCCs.  A
+ * coupled set is solved exactly (reading R-E3) by the ordered (Dijkstra-like) procedure
+ * the causality of the Godunov update allows: every unfixed member gets the candidate
+ * min(u_old, ubar) with fixed members at their values and unfixed ones at +inf; the member
+ * with the smallest candidate (ties: lowest global index) is fixed; repeat.  The smallest
+ * member of the exact solution cannot depend on larger members, so this is the exact
+ * solution of the set's equations.  1D uses a alone: ubar = a + fh.  2D (and 1D) only. */
+static double eik_godunov(int dim, double a, double b, double fh) {
+    if (dim == 1) return a + fh;           /* (+inf + fh = +inf) */
+    double m = a < b ? a : b;
+    if (m == INFINITY) return INFINITY;
+    if (fabs(a - b) >= fh) return m + fh;  /* (also when exactly one of a, b is +inf) */
+    double d = a - b;
+    double disc = fma(-d, d, 2.0 * (fh * fh));
+    return 0.5 * ((a + b) + sqrt(disc));
+}
+
+/* value of neighbour q of p as the decomposed sweep sees it: +inf outside the grid; inside
+ * a set: the fixed value or +inf; otherwise new (implicit for p) or old */
+static double eik_nb(const ctx_t *x, const int64_t p[3], int a, int sd, const double *uold, const double *unew,
+                     const unsigned char *done, const int64_t *mem, const int *fixed, const double *val, int k,
+                     int *err) {
+    const or_grid *g = x->g;
+    int64_t q[3] = {p[0], p[1], p[2]};
+    q[a] += sd;
+    if (!inside(g, q)) return INFINITY;
+    int64_t qi = lin(g, q);
+    for (int m = 0; m < k; ++m)
+        if (mem[m] == qi) return fixed[m] ? val[m] : INFINITY;
+    if (is_implicit(x, p, a, sd)) {
+        if (!done[qi]) *err = OR_EORDER;
+        return unew[qi];
+    }
+    return uold[qi];
+}
+
+/* One decomposed eikonal sweep at phase k (2D / 1D): uold -> unew, slowness f > 0, spacing h. */
+int or_eik_sweep(const or_grid *g, int64_t phase, int ov, const double *f, double h, const double *uold,
+                 double *unew) {
+    if (g->dim > 2) return OR_EINVAL;
+    ctx_t x;
+    int st = ctx_init(&x, g, phase, ov);
+    int64_t N = n_nodes(g);
+    int64_t *dval = NULL, *order = NULL, *cnt = NULL;
+    unsigned char *done = NULL;
+    if (st != OR_OK) goto out;
+    dval = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+    order = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+    done = (unsigned char *)calloc((size_t)N, 1);
+    if (!dval || !order || !done) { st = OR_ENOMEM; goto out; }
+    int64_t dmax = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t c[3];
+        coords_of(g, i, c);
+        dval[i] = wave_d(&x, c);
+        if (dval[i] > dmax) dmax = dval[i];
+    }
+    cnt = (int64_t *)calloc((size_t)(dmax + 2), sizeof(int64_t));
+    if (!cnt) { st = OR_ENOMEM; goto out; }
+    for (int64_t i = 0; i < N; ++i) cnt[dval[i] + 1]++;
+    for (int64_t d = 0; d <= dmax; ++d) cnt[d + 1] += cnt[d];
+    for (int64_t i = 0; i < N; ++i) order[cnt[dval[i]]++] = i;
+    for (int64_t t = 0; t < N; ++t) {
+        int64_t i = order[t];
+        if (done[i]) continue;
+        /* the coupled set of i: closure under mutual implicit neighbours (as trisolve) */
+        int64_t mem[8];
+        int k = 1;
+        mem[0] = i;
+        for (int hh = 0; hh < k; ++hh) {
+            int64_t p[3];
+            coords_of(g, mem[hh], p);
+            for (int a = 0; a < g->dim; ++a)
+                for (int sd = -1; sd <= 1; sd += 2) {
+                    int64_t q[3] = {p[0], p[1], p[2]};
+                    q[a] += sd;
+                    if (!inside(g, q)) continue;
+                    if (is_implicit(&x, p, a, sd) && is_implicit(&x, q, a, -sd)) {
+                        int64_t qi = lin(g, q);
+                        int seen = 0;
+                        for (int m = 0; m < k; ++m) seen |= (mem[m] == qi);
+                        if (!seen) {
+                            if (k == 8) { st = OR_EORDER; goto out; }
+                            mem[k++] = qi;
+                        }
+                    }
+                }
+        }
+        for (int a1 = 1; a1 < k; ++a1)
+            for (int b1 = a1; b1 > 0 && mem[b1 - 1] > mem[b1]; --b1) {
+                int64_t tmp = mem[b1]; mem[b1] = mem[b1 - 1]; mem[b1 - 1] = tmp;
+            }
+        int fixed[8] = {0};
+        double val[8];
+        for (int round = 0; round < k; ++round) {
+            int best = -1;
+            double cbest = 0.0;
+            for (int m = 0; m < k; ++m) {
+                if (fixed[m]) continue;
+                int64_t p[3];
+                coords_of(g, mem[m], p);
+                int err = OR_OK;
+                double av = INFINITY, bv = INFINITY;
+                for (int sd = -1; sd <= 1; sd += 2) {
+                    double v = eik_nb(&x, p, 0, sd, uold, unew, done, mem, fixed, val, k, &err);
+                    if (v < av) av = v;
+                    if (g->dim > 1) {
+                        double w = eik_nb(&x, p, 1, sd, uold, unew, done, mem, fixed, val, k, &err);
+                        if (w < bv) bv = w;
+                    }
+                }
+                if (err != OR_OK) { st = err; goto out; }
+                double ub = eik_godunov(g->dim, av, bv, f[mem[m]] * h);
+                double c = uold[mem[m]] < ub ? uold[mem[m]] : ub;
+                if (best < 0 || c < cbest) { best = m; cbest = c; }
+            }
+            fixed[best] = 1;
+            val[best] = cbest;
+        }
+        for (int m = 0; m < k; ++m) {
+            unew[mem[m]] = val[m];
+            done[mem[m]] = 1;
+        }
+    }
+out:
+    free(dval); free(order); free(done); free(cnt);
+    ctx_free(&x);
+    return st;
+}
+
+/* Classical fast sweeping (Zhao 2005): the textbook in-place Gauss-Seidel loop nest from
+ * corner `corner_bits` (bit a set = axis a descending), u <- min(u, ubar) with the current
+ * values of all neighbours.  Ignores boxes; independent of or_eik_sweep's machinery. */
+int or_eik_classical(const or_grid *g, int corner_bits, const double *f, double h, double *u) {
+    if (g->dim > 2) return OR_EINVAL;
+    int64_t n0 = g->n[0], n1 = g->n[1];
+    for (int64_t jj = 0; jj < n1; ++jj) {
+        int64_t j = ((corner_bits >> 1) & 1) ? n1 - 1 - jj : jj;
+        for (int64_t ii = 0; ii < n0; ++ii) {
+            int64_t i = (corner_bits & 1) ? n0 - 1 - ii : ii;
+            int64_t p = i + n0 * j;
+            double a = INFINITY, b = INFINITY;
+            if (i > 0 && u[p - 1] < a) a = u[p - 1];
+            if (i < n0 - 1 && u[p + 1] < a) a = u[p + 1];
+            if (g->dim > 1) {
+                if (j > 0 && u[p - n0] < b) b = u[p - n0];
+                if (j < n1 - 1 && u[p + n0] < b) b = u[p + n0];
+            }
+            double ub = eik_godunov(g->dim, a, b, f[p] * h);
+            if (ub < u[p]) u[p] = ub;
+        }
+    }
+    return OR_OK;
+}
