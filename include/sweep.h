@@ -270,6 +270,26 @@ sw_status sw_xpby(sw_grid *g, const double *z_dev, double beta, double *p_dev, s
 sw_status sw_axpby(sw_grid *g, double a, const double *x_dev, double b, const double *y_dev, double *out_dev,
                    sw_stream_t s);
 
+/* ---- eikonal equation |grad u| = f by decomposed fast sweeping (PAPER:2593-2599
+ * names the application, its supplementary paper is not available).  2D, boxes of at most 64 x 64,
+ * any number of ranks (the same slab decomposition and communicator as the SOR sweep).  The local
+ * update is the Godunov upwind rule of fast sweeping (Zhao 2005; DESIGN R-E1):
+ *   a = min(u_W, u_E), b = min(u_S, u_N) (+inf outside the domain), fh = f_p h,
+ *   ubar = min(a,b) + fh if |a - b| >= fh, else ((a + b) + sqrt(2 fh^2 - (a - b)^2)) / 2,
+ *   u_p <- min(u_p, ubar);
+ * each box sweeps from its start corner on the SOR schedule (new values on the start side, old on
+ * the end side, R-E2), the coupled nodes at start-start faces (pairs, the 4-node corner) solved
+ * exactly by ordered fixing (R-E3).  The iterate is SW_X: set it with sw_set_vector (+inf
+ * everywhere, 0 at the sources) before the first sweep; sources keep 0.
+ * sw_set_slowness: f over the local slab (x fastest), finite and > 0 (SW_EINVAL otherwise), grid
+ *   spacing h > 0; copied (host pointer); with a communicator the 2 ghost layers are exchanged.
+ * sw_eikonal_sweep: nsweeps passes from phase *phase_inout (then += nsweeps).
+ * sw_eikonal_changes: number of nodes (over all ranks with a communicator) the last pass changed
+ *   (0 = converged: the discrete viscosity solution); synchronises. */
+sw_status sw_set_slowness(sw_grid *g, const double *f_host, double h, sw_stream_t s);
+sw_status sw_eikonal_sweep(sw_grid *g, int nsweeps, int64_t *phase_inout, sw_stream_t s);
+sw_status sw_eikonal_changes(sw_grid *g, int64_t *changed_out, sw_stream_t s);
+
 /* Synchronise `s` and report a deferred device-side error (singular coupled system). */
 sw_status sw_check_status(sw_grid *g, sw_stream_t s);
 

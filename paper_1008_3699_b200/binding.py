@@ -82,6 +82,9 @@ def load():
     L.sw_axpy2.argtypes = [P_, D, P_, P_, P_, P_, P_, P_]
     L.sw_xpby.argtypes = [P_, P_, D, P_, P_]
     L.sw_axpby.argtypes = [P_, D, P_, D, P_, P_, P_]
+    L.sw_set_slowness.argtypes = [P_, P_, D, P_]
+    L.sw_eikonal_sweep.argtypes = [P_, I, ctypes.POINTER(I64), P_]
+    L.sw_eikonal_changes.argtypes = [P_, ctypes.POINTER(I64), P_]
     L.sw_check_status.argtypes = [P_, P_]
     L.sw_launch_count.argtypes = [P_]
     L.sw_launch_count.restype = I64
@@ -408,6 +411,24 @@ class Grid:
         """out = a x + b y (interior; products and sum rounded separately)."""
         _check(load().sw_axpby(self.h, float(a), ctypes.c_void_p(x_ptr), float(b), ctypes.c_void_p(y_ptr),
                                ctypes.c_void_p(out_ptr), _stream(stream)), "sw_axpby")
+
+    # -------------------------------------------------------------- eikonal (SURVEY §8(f) N4)
+    def set_slowness(self, f, h: float, stream=None):
+        """Slowness f > 0 over the local slab (numpy, slow axis first) and the grid spacing h."""
+        a = np.ascontiguousarray(np.asarray(f, dtype=np.float64))
+        assert a.size == int(np.prod(self.n_local)), (a.shape, self.n_local)
+        _check(load().sw_set_slowness(self.h, _host_ptr(a), float(h), _stream(stream)), "sw_set_slowness")
+        return self
+
+    def eikonal_sweep(self, nsweeps: int = 1, phase: int = 0, stream=None) -> int:
+        ph = ctypes.c_int64(int(phase))
+        _check(load().sw_eikonal_sweep(self.h, int(nsweeps), ctypes.byref(ph), _stream(stream)), "sw_eikonal_sweep")
+        return ph.value
+
+    def eikonal_changes(self, stream=None) -> int:
+        c = ctypes.c_int64()
+        _check(load().sw_eikonal_changes(self.h, ctypes.byref(c), _stream(stream)), "sw_eikonal_changes")
+        return c.value
 
     def check(self, stream=None):
         _check(load().sw_check_status(self.h, _stream(stream)), "sw_check_status")

@@ -22,6 +22,7 @@
 #include "tri3t.cuh"
 #include "mg.cuh"
 #include "comm.cuh"
+#include "eik2.cuh"
 
 using namespace sw;
 
@@ -57,6 +58,8 @@ struct sw_grid {
     double *F[3] = {nullptr, nullptr, nullptr};
     double *invD = nullptr, *R = nullptr, *Z = nullptr, *Pv = nullptr, *Q = nullptr, *Y = nullptr;
     double *W1 = nullptr, *W2 = nullptr;   // m-step preconditioner work (allocated when pc_steps > 1)
+    double *S = nullptr;                   // eikonal slowness (sw_set_slowness)
+    double eik_h = 0.0;
     double *Pv2 = nullptr;                 // second PCG direction buffer (fused direction update + SpMV)
     double *Rold = nullptr;                // flexible PCG: r before the update
     int pcg_flexible = -1;                 // sw_set_pcg_flexible: -1 auto (PAPER pairing), 0, 1
@@ -217,7 +220,7 @@ static void free_all(sw_grid *g) {
     g->mg.clear();
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
                        &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2,
-                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY, &g->Rold};
+                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY, &g->Rold, &g->S};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->hcg) cudaFreeHost(g->hcg);
@@ -577,7 +580,10 @@ static sw_status allsum(sw_grid *g, int k, double *o0, double *o1, cudaStream_t 
 // are real neighbouring rows or ghost layers of the padded arrays), TMA maps are encoded for the
 // shifted base.  Boxes read only x_old and write only their own nodes of x_new, so sub-ranges can
 // run in any order or concurrently with identical results.
-static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double *w8, cudaStream_t cs) {
+enum SweepKind { SK_SOR = 0, SK_EIK = 1 };
+
+static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double *w8, cudaStream_t cs,
+                           int kind = SK_SOR) {
     const int sa = g->dim - 1;
     Geo G = g->G;
     const bool whole = (r0 == 0 && cnt == G.nt[sa]);
@@ -593,6 +599,19 @@ static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double 
     double *xn = g->X[1 - g->cur] + dl;
     const double *F0 = g->F[0] ? g->F[0] + dl : nullptr, *F1 = g->F[1] ? g->F[1] + dl : nullptr,
                  *F2 = g->F[2] ? g->F[2] + dl : nullptr;
+    if (kind == SK_EIK) {                  // decomposed fast-sweeping pass
+        Eik2Args E;
+        E.G = G;
+        E.base = base;
+        E.h = g->eik_h;
+        E.uo = xo;
+        E.S = g->S + dl;
+        E.un = xn;
+        cudaError_t e = launch_eik2(E, cs);
+        g->launches++;
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("eik2 launch: ") + cudaGetErrorString(e));
+        return SW_OK;
+    }
     if (g->dim == 2 && g->fast2d && g->maps.ok && (g->G.poisson || g->maps.fok)) {
         CUtensorMap mx, mb, mf0, mf1;
         if (whole) {
@@ -659,20 +678,14 @@ static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double 
     return SW_OK;
 }
 
-extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, int nsweeps, int64_t *phase_inout,
-                                  sw_stream_t s) {
-    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
-    if (!phase_inout || nsweeps < 0) return fail(SW_EINVAL, "bad phase / nsweeps");
-    if (g->nranks > 1 && !g->comm && nsweeps > 1)
-        return fail(SW_EINVAL, "multi-rank without a communicator: one sweep per call (exchange ghosts between)");
-    double w8[8];
-    sw_status st = check_omega(omega, n_omega, g->dim, w8);
-    if (st != SW_OK) return st;
-    CK(cudaSetDevice(g->dev));
-    cudaStream_t cs = (cudaStream_t)s;
+// nsweeps passes of `kind` from phase *phase_inout; multi-rank: boundary tile rows first, the 2 new
+// boundary layers to the neighbours on the high-priority stream behind the interior rows
+static sw_status run_sweeps(sw_grid *g, int kind, const double *w8, int nsweeps, int64_t *phase_inout,
+                            cudaStream_t cs) {
+    sw_status st;
     const int sa = g->dim - 1, R = g->G.nt[sa];
     const bool multi = g->comm && g->nranks > 1;
-    if (multi && !g->bghost_ok && nsweeps > 0) {   // partner nodes' right-hand sides across the slab faces
+    if (multi && kind == SK_SOR && !g->bghost_ok && nsweeps > 0) {   // partner nodes' right-hand sides
         if ((st = exch(g, g->B, 2, cs)) != SW_OK) return st;
         g->bghost_ok = true;
     }
@@ -685,17 +698,17 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
         const int64_t k = *phase_inout;
         const int base = base_bits(g->dim, k);
         if (!multi) {
-            if ((st = sweep_rows(g, 0, R, base, w8, cs)) != SW_OK) return st;
+            if ((st = sweep_rows(g, 0, R, base, w8, cs, kind)) != SW_OK) return st;
         } else if (!split) {
-            if ((st = sweep_rows(g, 0, R, base, w8, cs)) != SW_OK) return st;
+            if ((st = sweep_rows(g, 0, R, base, w8, cs, kind)) != SW_OK) return st;
             if ((st = exch(g, g->X[1 - g->cur], 2, cs)) != SW_OK) return st;
         } else {
             // boundary rows first, then the interior on the same stream while the high-priority
             // stream moves the 2 new boundary layers to the neighbours
-            if ((st = sweep_rows(g, 0, nb, base, w8, cs)) != SW_OK) return st;
-            if ((st = sweep_rows(g, R - nb, nb, base, w8, cs)) != SW_OK) return st;
+            if ((st = sweep_rows(g, 0, nb, base, w8, cs, kind)) != SW_OK) return st;
+            if ((st = sweep_rows(g, R - nb, nb, base, w8, cs, kind)) != SW_OK) return st;
             CK(cudaEventRecord(g->ev_bnd, cs));
-            if ((st = sweep_rows(g, nb, R - 2 * nb, base, w8, cs)) != SW_OK) return st;
+            if ((st = sweep_rows(g, nb, R - 2 * nb, base, w8, cs, kind)) != SW_OK) return st;
             CK(cudaStreamWaitEvent(g->xs, g->ev_bnd, 0));
             if ((st = exch(g, g->X[1 - g->cur], 2, g->xs)) != SW_OK) return st;
             CK(cudaEventRecord(g->ev_halo, g->xs));
@@ -706,6 +719,74 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
         *phase_inout = k + 1;
     }
     if (multi && nsweeps > 0) g->xghost_ok = true;
+    return SW_OK;
+}
+
+extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, int nsweeps, int64_t *phase_inout,
+                                  sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!phase_inout || nsweeps < 0) return fail(SW_EINVAL, "bad phase / nsweeps");
+    if (g->nranks > 1 && !g->comm && nsweeps > 1)
+        return fail(SW_EINVAL, "multi-rank without a communicator: one sweep per call (exchange ghosts between)");
+    double w8[8];
+    sw_status st = check_omega(omega, n_omega, g->dim, w8);
+    if (st != SW_OK) return st;
+    CK(cudaSetDevice(g->dev));
+    return run_sweeps(g, SK_SOR, w8, nsweeps, phase_inout, (cudaStream_t)s);
+}
+
+// ------------------------------------------------------------------ eikonal
+static sw_status finish(sw_grid *g, int nparts, int stride, int off, double *dst, cudaStream_t s);
+
+extern "C" sw_status sw_set_slowness(sw_grid *g, const double *f_host, double h, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->dim != 2) return fail(SW_EINVAL, "the eikonal sweep is 2D");
+    if (!f_host || !(h > 0.0)) return fail(SW_EINVAL, "slowness NULL or h <= 0");
+    const int64_t N = g->G.n[0] * g->G.n[1];
+    for (int64_t i = 0; i < N; ++i)
+        if (!(f_host[i] > 0.0) || f_host[i] == INFINITY) return fail(SW_EINVAL, "slowness must be finite and > 0");
+    sw_status st;
+    if ((st = alloc_arr(g, &g->S)) != SW_OK) return st;
+    if ((st = copy_interior(g, g->S, f_host, nullptr, true, (cudaStream_t)s)) != SW_OK) return st;
+    if ((st = exch(g, g->S, 2, (cudaStream_t)s)) != SW_OK) return st;    // the partner layers' slowness
+    g->eik_h = h;
+    CK(cudaStreamSynchronize((cudaStream_t)s));
+    return SW_OK;
+}
+
+extern "C" sw_status sw_eikonal_sweep(sw_grid *g, int nsweeps, int64_t *phase_inout, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!phase_inout || nsweeps < 0) return fail(SW_EINVAL, "bad phase / nsweeps");
+    if (!g->S) return fail(SW_ESTATE, "sw_set_slowness must precede sw_eikonal_sweep");
+    if (!eik2_supported(g->G)) return fail(SW_EINVAL, "eikonal sweep: 2D boxes of at most 64 x 64 nodes");
+    if (g->nranks > 1 && !g->comm && nsweeps > 1)
+        return fail(SW_EINVAL, "multi-rank without a communicator: one sweep per call (exchange ghosts between)");
+    CK(cudaSetDevice(g->dev));
+    return run_sweeps(g, SK_EIK, nullptr, nsweeps, phase_inout, (cudaStream_t)s);
+}
+
+extern "C" sw_status sw_eikonal_changes(sw_grid *g, int64_t *changed_out, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (!changed_out) return fail(SW_EINVAL, "changed_out is NULL");
+    cudaStream_t cs = (cudaStream_t)s;
+    const int64_t N = g->G.n[0] * g->G.n[1] * g->G.n[2];
+    const int nb = grid_blocks(N, RED_THREADS);
+    k_count_ne<<<nb, RED_THREADS, 0, cs>>>(g->G, g->X[g->cur], g->X[1 - g->cur], (double *)g->partial);
+    g->launches++;
+    CK(cudaGetLastError());
+    sw_status st;
+    double *dst = &g->cg->zd;          // scratch scalar
+    if (g->comm && g->nranks > 1) {
+        k_finish_dd<<<1, RED_THREADS, 0, cs>>>(g->partial, nb, g->dds);
+        g->launches++;
+        if ((st = allsum(g, 1, dst, nullptr, cs)) != SW_OK) return st;
+    } else if ((st = finish(g, nb, 1, 0, dst, cs)) != SW_OK) {
+        return st;
+    }
+    double v = 0.0;
+    CK(cudaMemcpyAsync(&v, dst, sizeof(double), cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamSynchronize(cs));
+    *changed_out = (int64_t)v;
     return SW_OK;
 }
 
