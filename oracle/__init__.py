@@ -71,6 +71,8 @@ def lib():
         L.or_base_bits.argtypes = [I, I64, I]
         L.or_eik_sweep.argtypes = [P, I64, I, P, D, P, P]
         L.or_eik_classical.argtypes = [P, I, P, D, P]
+        L.or_sweep9.argtypes = [P, P, P, P, I, I64, I, P, P, P, P]
+        L.or_sor9_frontal.argtypes = [P, P, P, D, I, P, P, P]
     return _lib
 
 
@@ -306,3 +308,33 @@ def eik_classical(pb: Problem, corner: int, f, h: float, u):
     _check(lib().or_eik_classical(ctypes.byref(g), int(corner), _ptr(_arr(f, pb.shape)), float(h), _ptr(uu)),
            "eik_classical")
     return uu
+
+
+# ------------------------------------------------------------ nine-point molecule
+def diag_shape(n):
+    """numpy shape of a diagonal coefficient array ((n1 + 1) x (n0 + 1)) for a 2D grid n = (n0, n1)."""
+    return (n[1] + 1, n[0] + 1)
+
+
+def sweep9(pb: Problem, diag, omega, x_old, b, phase: int = 0, override: int = -1, return_minpiv=False):
+    """One decomposed nine-point SOR sweep (reading R-N3).  diag = (dd, da): SW-NE
+    and SE-NW coefficients, shape diag_shape(n); pb.faces are the axis faces (None = 1)."""
+    g = pb.struct()
+    dd = _arr(diag[0], diag_shape(pb.n))
+    da = _arr(diag[1], diag_shape(pb.n))
+    w = _omega_arr(omega)
+    xn = np.empty(pb.shape)
+    mp = ctypes.c_double(np.inf)
+    _check(lib().or_sweep9(ctypes.byref(g), _ptr(dd), _ptr(da), _ptr(w), len(w), int(phase), int(override),
+                           _ptr(_arr(x_old, pb.shape)), _ptr(_arr(b, pb.shape)), _ptr(xn), ctypes.byref(mp)), "sweep9")
+    return (xn, mp.value) if return_minpiv else xn
+
+
+def sor9_frontal(pb: Problem, diag, omega: float, x_old, b, corner: int = 0):
+    """Textbook frontal nine-point SOR from `corner` (one box; new W, S, SW, old E, N, NE, SE, NW)."""
+    g = pb.struct()
+    xn = np.empty(pb.shape)
+    _check(lib().or_sor9_frontal(ctypes.byref(g), _ptr(_arr(diag[0], diag_shape(pb.n))),
+                                 _ptr(_arr(diag[1], diag_shape(pb.n))), float(omega), int(corner),
+                                 _ptr(_arr(x_old, pb.shape)), _ptr(_arr(b, pb.shape)), _ptr(xn)), "sor9_frontal")
+    return xn

@@ -879,3 +879,191 @@ int or_eik_classical(const or_grid *g, int corner_bits, const double *f, double 
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------ nine-point molecule
+ * "the extension of our algorithm for nine-point or higher order central stencils is
+ * straightforward ... the size of local systems to be solved will be also increased"
+ * (PAPER:702-707).  2D operator (A u)_p = a_P u_p - sum_{8 neighbours q} c_pq u_q with
+ * the axis faces of the grid (face[0], face[1]) and two diagonal coefficient arrays of
+ * shape (n0+1) x (n1+1):
+ *   dd[c] couples (c_x-1, c_y-1) and c       (SW-NE diagonal of the cell with corner c)
+ *   da[c] couples (c_x-1, c_y) and (c_x, c_y-1)   (SE-NW diagonal)
+ * a_P = ((F_W + F_E) + (F_S + F_N)) + ((D_SW + D_NE) + (D_SE + D_NW)) + beta.
+ * Reading R-N3: the paper's classification, extended to diagonal neighbours --
+ * q is IMPLICIT (new value) for p iff q lies on the start side of p's box along every axis
+ * in which they differ, else explicit (old value).  For the five-point stencil this is the
+ * SOR sweep above; for nine points a box takes W, S, SW new and E, N, NE, SE, NW old (the
+ * frontal order: SE and NW sit on p's own front), and at a start corner the four boxes'
+ * corner nodes become mutually implicit along the diagonals too: the corner set grows from
+ * the 4-cycle to a dense 4 x 4 (the "increased local systems").  Neighbour order of every
+ * sum: W, E, S, N, SW, SE, NW, NE; per-node formula and coupled-set elimination as R-7/R-8. */
+static const int NB9[8][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}, {-1, -1}, {1, -1}, {-1, 1}, {1, 1}};
+
+static double coef9(const or_grid *g, const double *dd, const double *da, const int64_t c[3], int k) {
+    int dx = NB9[k][0], dy = NB9[k][1];
+    if (dy == 0) return face_between(g, c, 0, dx);
+    if (dx == 0) return face_between(g, c, 1, dy);
+    int64_t m0 = g->n[0] + 1;
+    if (dx == dy) {                               /* SW (-1,-1) or NE (+1,+1): dd at the upper corner */
+        int64_t cx = c[0] + (dx > 0), cy = c[1] + (dy > 0);
+        return dd[cx + m0 * cy];
+    }
+    /* SE (+1,-1): da[(x+1, y)];  NW (-1,+1): da[(x, y+1)] */
+    int64_t cx = c[0] + (dx > 0), cy = c[1] + (dy > 0);
+    return da[cx + m0 * cy];
+}
+
+static double a_p9(const or_grid *g, const double *dd, const double *da, const int64_t c[3]) {
+    double s = (coef9(g, dd, da, c, 0) + coef9(g, dd, da, c, 1)) + (coef9(g, dd, da, c, 2) + coef9(g, dd, da, c, 3));
+    double t = (coef9(g, dd, da, c, 4) + coef9(g, dd, da, c, 7)) + (coef9(g, dd, da, c, 5) + coef9(g, dd, da, c, 6));
+    return (s + t) + g->beta;
+}
+
+static int implicit9(const ctx_t *x, const int64_t p[3], int k) {
+    int dx = NB9[k][0], dy = NB9[k][1];
+    return (dx == 0 || is_implicit(x, p, 0, dx)) && (dy == 0 || is_implicit(x, p, 1, dy));
+}
+
+/* One decomposed nine-point SOR sweep at phase k (2D). */
+int or_sweep9(const or_grid *g, const double *dd, const double *da, const double *omega, int n_omega, int64_t phase,
+              int ov, const double *xold, const double *b, double *xnew, double *minpiv) {
+    if (g->dim != 2) return OR_EINVAL;
+    ctx_t x;
+    int st = ctx_init(&x, g, phase, ov);
+    int64_t N = n_nodes(g);
+    double *alpha = (double *)malloc(sizeof(double) * (size_t)N);
+    double *r0 = (double *)malloc(sizeof(double) * (size_t)N);
+    int64_t *dval = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+    int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+    unsigned char *done = (unsigned char *)calloc((size_t)N, 1);
+    int64_t *cnt = NULL;
+    if (st != OR_OK) goto out;
+    if (!alpha || !r0 || !dval || !order || !done) { st = OR_ENOMEM; goto out; }
+    /* explicit parts: r0 = fma(alpha, b + sum_explicit c u_old, (1 - w) u_old) */
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t c[3];
+        coords_of(g, i, c);
+        double w = omega[n_omega == 1 ? 0 : dir_bits(&x, c)];
+        double al = w / a_p9(g, dd, da, c);
+        double e = b[i];
+        for (int k = 0; k < 8; ++k) {
+            int64_t q[3] = {c[0] + NB9[k][0], c[1] + NB9[k][1], c[2]};
+            if (!inside(g, q) || implicit9(&x, c, k)) continue;
+            e = fma(coef9(g, dd, da, c, k), xold[lin(g, q)], e);
+        }
+        alpha[i] = al;
+        r0[i] = fma(al, e, (1.0 - w) * xold[i]);
+    }
+    /* fronts: implicit neighbours lie on earlier fronts or in the node's coupled set */
+    int64_t dmax = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t c[3];
+        coords_of(g, i, c);
+        dval[i] = wave_d(&x, c);
+        if (dval[i] > dmax) dmax = dval[i];
+    }
+    cnt = (int64_t *)calloc((size_t)(dmax + 2), sizeof(int64_t));
+    if (!cnt) { st = OR_ENOMEM; goto out; }
+    for (int64_t i = 0; i < N; ++i) cnt[dval[i] + 1]++;
+    for (int64_t d = 0; d <= dmax; ++d) cnt[d + 1] += cnt[d];
+    for (int64_t i = 0; i < N; ++i) order[cnt[dval[i]]++] = i;
+    for (int64_t t = 0; t < N; ++t) {
+        int64_t i = order[t];
+        if (done[i]) continue;
+        int64_t mem[8];
+        int k = 1;
+        mem[0] = i;
+        for (int h = 0; h < k; ++h) {              /* closure under mutual implicit neighbours */
+            int64_t p[3];
+            coords_of(g, mem[h], p);
+            for (int kk = 0; kk < 8; ++kk) {
+                int64_t q[3] = {p[0] + NB9[kk][0], p[1] + NB9[kk][1], p[2]};
+                if (!inside(g, q) || !implicit9(&x, p, kk)) continue;
+                int back = -1;
+                for (int k2 = 0; k2 < 8; ++k2)
+                    if (NB9[k2][0] == -NB9[kk][0] && NB9[k2][1] == -NB9[kk][1]) back = k2;
+                if (!implicit9(&x, q, back)) continue;
+                int64_t qi = lin(g, q);
+                int seen = 0;
+                for (int m = 0; m < k; ++m) seen |= (mem[m] == qi);
+                if (!seen) {
+                    if (k == 8) { st = OR_EORDER; goto out; }
+                    mem[k++] = qi;
+                }
+            }
+        }
+        for (int a1 = 1; a1 < k; ++a1)
+            for (int b1 = a1; b1 > 0 && mem[b1 - 1] > mem[b1]; --b1) {
+                int64_t tmp = mem[b1]; mem[b1] = mem[b1 - 1]; mem[b1 - 1] = tmp;
+            }
+        double M[8][8], rhs[8], u[8];
+        for (int p = 0; p < k; ++p) {
+            int64_t pc[3];
+            coords_of(g, mem[p], pc);
+            for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
+            double acc = r0[mem[p]];
+            for (int kk = 0; kk < 8; ++kk) {
+                int64_t qc[3] = {pc[0] + NB9[kk][0], pc[1] + NB9[kk][1], pc[2]};
+                if (!inside(g, qc) || !implicit9(&x, pc, kk)) continue;
+                int64_t qi = lin(g, qc);
+                double m = alpha[mem[p]] * coef9(g, dd, da, pc, kk);
+                int inscc = -1;
+                for (int q = 0; q < k; ++q)
+                    if (mem[q] == qi) inscc = q;
+                if (inscc >= 0) {
+                    M[p][inscc] = -m;
+                } else {
+                    if (!done[qi]) { st = OR_EORDER; goto out; }
+                    acc = fma(m, xnew[qi], acc);
+                }
+            }
+            rhs[p] = acc;
+        }
+        if (k == 1) {
+            u[0] = rhs[0];
+        } else {
+            st = ge_solve(k, M, rhs, u, minpiv);
+            if (st != OR_OK) goto out;
+        }
+        for (int p = 0; p < k; ++p) {
+            xnew[mem[p]] = u[p];
+            done[mem[p]] = 1;
+        }
+    }
+out:
+    free(alpha); free(r0); free(dval); free(order); free(done); free(cnt);
+    ctx_free(&x);
+    return st;
+}
+
+/* Textbook frontal nine-point SOR from corner `corner_bits`, one box: fronts d = distance from
+ * the corner in order; every node of front d from W, S, SW of the new iterate (earlier fronts)
+ * and E, N, NE, SE, NW of the old one (its own and later fronts):
+ *   u_p = (1 - w) u_p + (w / a_P) (b_p + sum_q c_pq u_q)      (plain sums, no fma).
+ * Independent of or_sweep9's machinery; ignores boxes. */
+int or_sor9_frontal(const or_grid *g, const double *dd, const double *da, double omega, int corner_bits,
+                    const double *xold, const double *b, double *xnew) {
+    if (g->dim != 2) return OR_EINVAL;
+    int64_t n0 = g->n[0], n1 = g->n[1];
+    int sx = corner_bits & 1, sy = (corner_bits >> 1) & 1;
+    for (int64_t d = 0; d <= (n0 - 1) + (n1 - 1); ++d)
+        for (int64_t jj = 0; jj < n1; ++jj) {
+            int64_t ii = d - jj;
+            if (ii < 0 || ii >= n0) continue;
+            int64_t i = sx ? n0 - 1 - ii : ii, j = sy ? n1 - 1 - jj : jj;
+            int64_t c[3] = {i, j, 0};
+            double s = b[lin(g, c)];
+            for (int k = 0; k < 8; ++k) {
+                int dx = NB9[k][0], dy = NB9[k][1];
+                int64_t q[3] = {i + dx, j + dy, 0};
+                if (!inside(g, q)) continue;
+                /* in sweep coordinates: the neighbour is new iff it lies back along every differing axis */
+                int ldx = sx ? -dx : dx, ldy = sy ? -dy : dy;
+                int isnew = (ldx <= 0 && ldy <= 0);
+                s += coef9(g, dd, da, c, k) * (isnew ? xnew[lin(g, q)] : xold[lin(g, q)]);
+            }
+            int64_t p = lin(g, c);
+            xnew[p] = (1.0 - omega) * xold[p] + (omega / a_p9(g, dd, da, c)) * s;
+        }
+    return OR_OK;
+}
