@@ -270,6 +270,20 @@ sw_status sw_xpby(sw_grid *g, const double *z_dev, double beta, double *p_dev, s
 sw_status sw_axpby(sw_grid *g, double a, const double *x_dev, double b, const double *y_dev, double *out_dev,
                    sw_stream_t s);
 
+/* ---- nine-point molecule ("extension ... for nine-point or higher
+ * order central stencils is straightforward ... the size of local systems ... increased").  2D:
+ * (A u)_p = a_P u_p - sum over the 8 neighbours c_pq u_q with the grid's axis faces (unit for
+ * SW_COEF_POISSON) and two diagonal coefficient arrays over the cell corners c (0..n per axis,
+ * x fastest, (n0 + 1) (n1 + 1) values each, GLOBAL arrays on every rank):
+ *   dd[c] couples (c_x - 1, c_y - 1) and c;  da[c] couples (c_x - 1, c_y) and (c_x, c_y - 1);
+ * a_P = ((W + E) + (S + N)) + ((SW + NE) + (SE + NW)) + beta.  After sw_set_diagonals the grid's
+ * sw_sor_sweep is the nine-point decomposed sweep (DESIGN R-N3: a neighbour is new iff it lies on
+ * the start side of the node's box along every axis where they differ; the coupled set at a start
+ * corner becomes a dense 4 x 4); boxes of at most 64 x 64; multi-rank as the five-point sweep.  The
+ * preconditioner, residual and PCG calls stay five-point only (SW_ESTATE on such a grid).
+ * SW_EINVAL for dim != 2 or a negative / non-finite coefficient. */
+sw_status sw_set_diagonals(sw_grid *g, const double *dd_host, const double *da_host, sw_stream_t s);
+
 /* ---- eikonal equation |grad u| = f by decomposed fast sweeping (PAPER:2593-2599
  * names the application, its supplementary paper is not available).  2D, boxes of at most 64 x 64,
  * any number of ranks (the same slab decomposition and communicator as the SOR sweep).  The local

@@ -82,6 +82,7 @@ def load():
     L.sw_axpy2.argtypes = [P_, D, P_, P_, P_, P_, P_, P_]
     L.sw_xpby.argtypes = [P_, P_, D, P_, P_]
     L.sw_axpby.argtypes = [P_, D, P_, D, P_, P_, P_]
+    L.sw_set_diagonals.argtypes = [P_, P_, P_, P_]
     L.sw_set_slowness.argtypes = [P_, P_, D, P_]
     L.sw_eikonal_sweep.argtypes = [P_, I, ctypes.POINTER(I64), P_]
     L.sw_eikonal_changes.argtypes = [P_, ctypes.POINTER(I64), P_]
@@ -411,6 +412,17 @@ class Grid:
         """out = a x + b y (interior; products and sum rounded separately)."""
         _check(load().sw_axpby(self.h, float(a), ctypes.c_void_p(x_ptr), float(b), ctypes.c_void_p(y_ptr),
                                ctypes.c_void_p(out_ptr), _stream(stream)), "sw_axpby")
+
+    # -------------------------------------------------------------- nine-point molecule (SURVEY §8(f) N3)
+    def set_diagonals(self, dd, da, stream=None):
+        """Diagonal coefficients of the nine-point operator: GLOBAL arrays of shape (n1 + 1, n0 + 1)
+        (dd couples c - (1, 1) and c; da couples (c_x - 1, c_y) and (c_x, c_y - 1)); sw_sor_sweep then
+        runs the nine-point decomposed sweep."""
+        a = np.ascontiguousarray(np.asarray(dd, dtype=np.float64))
+        b = np.ascontiguousarray(np.asarray(da, dtype=np.float64))
+        assert a.shape == b.shape == (self.n[1] + 1, self.n[0] + 1), a.shape
+        _check(load().sw_set_diagonals(self.h, _host_ptr(a), _host_ptr(b), _stream(stream)), "sw_set_diagonals")
+        return self
 
     # -------------------------------------------------------------- eikonal (SURVEY §8(f) N4)
     def set_slowness(self, f, h: float, stream=None):

@@ -23,6 +23,7 @@
 #include "mg.cuh"
 #include "comm.cuh"
 #include "eik2.cuh"
+#include "sweep9.cuh"
 
 using namespace sw;
 
@@ -59,6 +60,8 @@ struct sw_grid {
     double *invD = nullptr, *R = nullptr, *Z = nullptr, *Pv = nullptr, *Q = nullptr, *Y = nullptr;
     double *W1 = nullptr, *W2 = nullptr;   // m-step preconditioner work (allocated when pc_steps > 1)
     double *S = nullptr;                   // eikonal slowness (sw_set_slowness)
+    double *Dd = nullptr, *Da = nullptr;   // nine-point diagonal coefficients (sw_set_diagonals)
+    bool nine = false;
     double eik_h = 0.0;
     double *Pv2 = nullptr;                 // second PCG direction buffer (fused direction update + SpMV)
     double *Rold = nullptr;                // flexible PCG: r before the update
@@ -220,7 +223,7 @@ static void free_all(sw_grid *g) {
     g->mg.clear();
     double **ptrs[] = {&g->X[0], &g->X[1], &g->B, &g->F[0], &g->F[1], &g->F[2], &g->invD,
                        &g->R,    &g->Z,    &g->Pv, &g->Q,   &g->Y,    &g->W1, &g->W2,
-                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY, &g->Rold, &g->S};
+                       &g->MGR,  &g->MGX,  &g->MT1, &g->MT2, &g->Pv2, &g->MGW, &g->MGY, &g->Rold, &g->S, &g->Dd, &g->Da};
     for (double **p : ptrs)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (g->hcg) cudaFreeHost(g->hcg);
@@ -580,7 +583,7 @@ static sw_status allsum(sw_grid *g, int k, double *o0, double *o1, cudaStream_t 
 // are real neighbouring rows or ghost layers of the padded arrays), TMA maps are encoded for the
 // shifted base.  Boxes read only x_old and write only their own nodes of x_new, so sub-ranges can
 // run in any order or concurrently with identical results.
-enum SweepKind { SK_SOR = 0, SK_EIK = 1 };
+enum SweepKind { SK_SOR = 0, SK_EIK = 1, SK_SOR9 = 2 };
 
 static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double *w8, cudaStream_t cs,
                            int kind = SK_SOR) {
@@ -599,6 +602,24 @@ static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double 
     double *xn = g->X[1 - g->cur] + dl;
     const double *F0 = g->F[0] ? g->F[0] + dl : nullptr, *F1 = g->F[1] ? g->F[1] + dl : nullptr,
                  *F2 = g->F[2] ? g->F[2] + dl : nullptr;
+    if (kind == SK_SOR9) {                 // nine-point molecule
+        Sweep9Args S9;
+        S9.G = G;
+        S9.base = base;
+        for (int i = 0; i < 4; ++i) S9.omega[i] = w8[i];
+        S9.xo = xo;
+        S9.b = bb;
+        S9.f0 = G.poisson ? nullptr : F0;
+        S9.f1 = G.poisson ? nullptr : F1;
+        S9.dd = g->Dd + dl;
+        S9.da = g->Da + dl;
+        S9.xn = xn;
+        S9.flag = g->flag;
+        cudaError_t e = launch_sweep9(S9, cs);
+        g->launches++;
+        if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep9 launch: ") + cudaGetErrorString(e));
+        return SW_OK;
+    }
     if (kind == SK_EIK) {                  // decomposed fast-sweeping pass
         Eik2Args E;
         E.G = G;
@@ -732,7 +753,39 @@ extern "C" sw_status sw_sor_sweep(sw_grid *g, const double *omega, int n_omega, 
     sw_status st = check_omega(omega, n_omega, g->dim, w8);
     if (st != SW_OK) return st;
     CK(cudaSetDevice(g->dev));
-    return run_sweeps(g, SK_SOR, w8, nsweeps, phase_inout, (cudaStream_t)s);
+    if (g->nine && !sweep9_supported(g->G)) return fail(SW_EINVAL, "nine-point sweep: 2D boxes of at most 64 x 64");
+    return run_sweeps(g, g->nine ? SK_SOR9 : SK_SOR, w8, nsweeps, phase_inout, (cudaStream_t)s);
+}
+
+// ------------------------------------------------------------------ nine-point molecule
+extern "C" sw_status sw_set_diagonals(sw_grid *g, const double *dd_host, const double *da_host, sw_stream_t s) {
+    if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->dim != 2) return fail(SW_EINVAL, "the nine-point molecule is 2D");
+    if (!dd_host || !da_host) return fail(SW_EINVAL, "diagonal array is NULL");
+    const Geo &G = g->G;
+    const int64_t m0 = G.ng[0] + 1, m1 = G.ng[1] + 1;
+    for (int64_t i = 0; i < m0 * m1; ++i)
+        if (!(dd_host[i] >= 0.0) || !(da_host[i] >= 0.0) || dd_host[i] == INFINITY || da_host[i] == INFINITY)
+            return fail(SW_EINVAL, "diagonal coefficients must be finite and >= 0");
+    sw_status st;
+    if ((st = alloc_arr(g, &g->Dd)) != SW_OK || (st = alloc_arr(g, &g->Da)) != SW_OK) return st;
+    std::vector<double> hb((size_t)g->nelem);
+    const double *src[2] = {dd_host, da_host};
+    double *dst[2] = {g->Dd, g->Da};
+    for (int a = 0; a < 2; ++a) {
+        std::fill(hb.begin(), hb.end(), 0.0);
+        // corner c (0..n per axis, global) of the slab rows c_y in [off - 2, off + n_local + 2]
+        for (int64_t cy = G.off[1] - 2; cy <= G.off[1] + G.n[1] + 1; ++cy) {
+            if (cy < 0 || cy >= m1) continue;
+            for (int64_t cxx = 0; cxx < m0; ++cxx)
+                hb[(size_t)gidx(G, cxx, cy, 0)] = src[a][cxx + m0 * cy];
+        }
+        CK(cudaMemcpyAsync(dst[a], hb.data(), sizeof(double) * (size_t)g->nelem, cudaMemcpyHostToDevice,
+                           (cudaStream_t)s));
+        CK(cudaStreamSynchronize((cudaStream_t)s));
+    }
+    g->nine = true;
+    return SW_OK;
 }
 
 // ------------------------------------------------------------------ eikonal
@@ -817,6 +870,7 @@ extern "C" sw_status sw_check_status(sw_grid *g, sw_stream_t s) {
 
 extern "C" sw_status sw_residual_norm(sw_grid *g, double *rel_out, sw_stream_t s) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
+    if (g->nine) return fail(SW_ESTATE, "nine-point grids support the SOR sweep only");
     if (!rel_out) return fail(SW_EINVAL, "rel_out is NULL");
     if (g->nranks > 1 && !g->comm) return fail(SW_EINVAL, "sw_residual_norm over several ranks needs a communicator");
     cudaStream_t cs = (cudaStream_t)s;
@@ -879,6 +933,7 @@ static int tri_nstages(const sw_grid *g, sw_pairing pairing) { return pairing ==
 
 static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, double *z, sw_pairing pairing,
                            int stage, cudaStream_t s) {
+    if (g->nine) return fail(SW_ESTATE, "nine-point grids support the SOR sweep only");
     sw_status st = ensure_work(g);
     if (st != SW_OK) return st;
     if (ilu && !g->factored) return fail(SW_ESTATE, "sw_ilu0_factor must precede sw_ilu_apply");
@@ -1276,6 +1331,7 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
                                   int *iters_out, double *relres_out, sw_stream_t s) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
     if (!iters_out || !relres_out || maxit < 1 || !(rtol > 0)) return fail(SW_EINVAL, "bad arguments");
+    if (g->nine) return fail(SW_ESTATE, "nine-point grids support the SOR sweep only");
     if (g->nranks > 1) {
         if (!g->comm) return fail(SW_EINVAL, "sw_pcg_solve over several ranks needs a communicator");
         return pcg_multi(g, pc, omega, pairing, rtol, maxit, iters_out, relres_out, (cudaStream_t)s);

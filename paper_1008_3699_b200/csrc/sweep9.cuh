@@ -1,0 +1,193 @@
+// sweep9.cuh -- decomposed SOR sweep of the nine-point molecule, 2D (PAPER:702-707:
+// "the extension of our algorithm for nine-point or higher order central stencils is straightforward
+// ... the size of local systems to be solved will be also increased").  Reading R-N3: a neighbour q
+// is implicit (new value) for p iff it lies on the start side of p's box along every axis in which
+// they differ -- the paper's rule, extended to the diagonals.  A box then takes W, S, SW new and E,
+// N, NE, SE, NW old (SE and NW sit on p's own front), pairs of nodes across coupled start faces are
+// solved together as in the five-point sweep, and the four nodes at a start corner form one dense
+// 4 x 4 system (the five-point sweep's 4-cycle plus the two diagonals).  Per node the oracle's
+// operations in its order (or_sweep9): a_P = ((W + E) + (S + N)) + ((SW + NE) + (SE + NW)) + beta,
+// r0 = fma(w / a_P, b + sum_explicit c u_old, (1 - w) u_old), implicit terms and the coupled-set
+// elimination (no pivoting, ascending global index) in neighbour order W, E, S, N, SW, SE, NW, NE:
+// bitwise equal results.
+//
+// One CTA of 64 threads per box (T0, T1 <= 64): the old values of the box and its 2-node halo in
+// shared memory in LOCAL coordinates (local +a points away from the box's start corner), a second
+// window receives the new values; front d = x + y of the own nodes, thread t takes node (t, d - t)
+// with its partner(s) across coupled start faces, one barrier per front; coefficients and b are read
+// from global memory (L1 / L2).
+#pragma once
+#include "common.cuh"
+#include "sweep2p.cuh"
+
+namespace sw {
+
+namespace s9 {
+constexpr int NT = 64;
+__constant__ int NBX[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+__constant__ int NBY[8] = {0, 0, -1, 1, -1, -1, 1, 1};
+}  // namespace s9
+
+struct Sweep9Args {
+    Geo G;
+    int base;
+    double omega[4];
+    const double *xo, *b, *f0, *f1;   // padded; f0 / f1 null = unit axis faces
+    const double *dd, *da;            // padded diagonal coefficients (corner-indexed, R-N3)
+    double *xn;
+    int *flag;
+};
+
+inline size_t sweep9_smem(const Geo &G) { return 2 * sizeof(double) * (size_t)(G.T[0] + 4) * (G.T[1] + 4); }
+
+inline bool sweep9_supported(const Geo &G) {
+    return G.dim == 2 && G.T[0] <= s9::NT && G.T[1] <= s9::NT && sweep9_smem(G) <= 227 * 1024;
+}
+
+__global__ void __launch_bounds__(s9::NT) k_sweep9(Sweep9Args A) {
+    extern __shared__ __align__(16) double s9m[];
+    SW_JITTER_POINT();
+    const Geo &G = A.G;
+    const int T0 = G.T[0], T1 = G.T[1], WX = T0 + 4;
+    double *const XO = s9m, *const XN = s9m + WX * (T1 + 4);
+    const int tx = blockIdx.x % G.nt[0], ty = blockIdx.x / G.nt[0];
+    const int64_t R0 = tx, R1 = ty + G.toff[1];
+    const int sx = ((A.base >> 0) & 1) ^ (int)(R0 & 1);
+    const int sy = ((A.base >> 1) & 1) ^ (int)(R1 & 1);
+    const bool cx = sx ? (R0 < G.ntg[0] - 1) : (R0 > 0);
+    const bool cy = sy ? (R1 < G.ntg[1] - 1) : (R1 > 0);
+    const int64_t X0 = R0 * T0, Y0 = R1 * T1;
+    auto gxo = [&](int lx) { return X0 + (sx ? T0 - 1 - lx : lx); };
+    auto gyo = [&](int ly) { return Y0 + (sy ? T1 - 1 - ly : ly); };
+    auto wi = [&](int lx, int ly) { return (ly + 2) * WX + (lx + 2); };
+    auto inside = [&](int64_t gx, int64_t gy) { return gx >= 0 && gx < G.ng[0] && gy >= 0 && gy < G.ng[1]; };
+    // coefficient of global neighbour k of global node (gx, gy)
+    auto coef = [&](int k, int64_t gx, int64_t gy) -> double {
+        const int dx = s9::NBX[k], dy = s9::NBY[k];
+        const int64_t cxg = gx + (dx > 0), cyg = gy + (dy > 0);
+        if (dy == 0) return A.f0 ? A.f0[gidx(G, cxg, gy, 0)] : 1.0;
+        if (dx == 0) return A.f1 ? A.f1[gidx(G, gx, cyg, 0)] : 1.0;
+        return (dx == dy ? A.dd : A.da)[gidx(G, cxg, cyg, 0)];
+    };
+    // box offset of a local coordinate and the start side of that box in local coordinates
+    // (A's box starts at local 0 and moves +; every neighbouring box's start side is +)
+    auto side = [&](int l, int T) { return (l >= 0 && l < T) ? -1 : +1; };
+    // q (local) implicit for p (local): on p's start side along every axis where they differ
+    auto implicit = [&](int px, int py, int qx, int qy) {
+        const int sxp = side(px, T0), syp = side(py, T1);
+        const bool okx = qx == px || (sxp < 0 ? qx < px : qx > px);
+        const bool oky = qy == py || (syp < 0 ? qy < py : qy > py);
+        return okx && oky;
+    };
+    // stage in the old window (0 outside the domain: Dirichlet data are folded into b)
+    for (int e = threadIdx.x; e < WX * (T1 + 4); e += s9::NT) {
+        const int lx = e % WX - 2, ly = e / WX - 2;
+        const int64_t gx = gxo(lx), gy = gyo(ly);
+        XO[e] = inside(gx, gy) ? A.xo[gidx(G, gx, gy, 0)] : 0.0;
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    int fl = 0;
+    for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
+        const int x = t, y = d - t;
+        if (x < T0 && y >= 0 && y < T1) {
+            int mx[4], my[4], k = 1;
+            mx[0] = x;
+            my[0] = y;
+            if (x == 0 && y == 0 && cx && cy) {
+                mx[1] = -1; my[1] = 0; mx[2] = 0; my[2] = -1; mx[3] = -1; my[3] = -1;
+                k = 4;
+            } else if (x == 0 && cx) {
+                mx[1] = -1; my[1] = y;
+                k = 2;
+            } else if (y == 0 && cy) {
+                mx[1] = x; my[1] = -1;
+                k = 2;
+            }
+            int64_t gi[4];
+            for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
+            for (int a1 = 1; a1 < k; ++a1)
+                for (int b1 = a1; b1 > 0 && gi[b1 - 1] > gi[b1]; --b1) {
+                    int64_t tg = gi[b1]; gi[b1] = gi[b1 - 1]; gi[b1 - 1] = tg;
+                    int tt = mx[b1]; mx[b1] = mx[b1 - 1]; mx[b1 - 1] = tt;
+                    tt = my[b1]; my[b1] = my[b1 - 1]; my[b1 - 1] = tt;
+                }
+            double M[4][4], rhs[4], u[4];
+            for (int p = 0; p < k; ++p) {
+                const int px = mx[p], py = my[p];
+                const int64_t gx = gxo(px), gy = gyo(py);
+                double c8[8];
+                for (int kk = 0; kk < 8; ++kk) c8[kk] = coef(kk, gx, gy);
+                const double ap = ((c8[0] + c8[1]) + (c8[2] + c8[3])) + ((c8[4] + c8[7]) + (c8[5] + c8[6])) + G.beta;
+                // the node's own box's direction bits: A's, flipped along axes where it lies outside A
+                const int bits = (sx ^ (px < 0 || px >= T0 ? 1 : 0)) | ((sy ^ (py < 0 || py >= T1 ? 1 : 0)) << 1);
+                const double w = A.omega[bits];
+                const double al = div_rn(w, ap);
+                double e = A.b[gidx(G, gx, gy, 0)];
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int64_t qgx = gx + s9::NBX[kk], qgy = gy + s9::NBY[kk];
+                    if (!inside(qgx, qgy)) continue;
+                    const int qx = px + (sx ? -s9::NBX[kk] : s9::NBX[kk]), qy = py + (sy ? -s9::NBY[kk] : s9::NBY[kk]);
+                    if (implicit(px, py, qx, qy)) continue;
+                    e = fma(c8[kk], XO[wi(qx, qy)], e);
+                }
+                double acc = fma(al, e, (1.0 - w) * XO[wi(px, py)]);
+                for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int64_t qgx = gx + s9::NBX[kk], qgy = gy + s9::NBY[kk];
+                    if (!inside(qgx, qgy)) continue;
+                    const int qx = px + (sx ? -s9::NBX[kk] : s9::NBX[kk]), qy = py + (sy ? -s9::NBY[kk] : s9::NBY[kk]);
+                    if (!implicit(px, py, qx, qy)) continue;
+                    const double m = al * c8[kk];
+                    int in = -1;
+                    for (int q = 0; q < k; ++q)
+                        if (mx[q] == qx && my[q] == qy) in = q;
+                    if (in >= 0) M[p][in] = -m;
+                    else acc = fma(m, XN[wi(qx, qy)], acc);
+                }
+                rhs[p] = acc;
+            }
+            if (k == 1) {
+                u[0] = rhs[0];
+            } else {                                       // the oracle's ge_solve (R-8)
+                double inv[4];
+                for (int p = 0; p < k; ++p) {
+                    const double piv = M[p][p];
+                    fl |= !(fabs(piv) >= 1e-14);
+                    inv[p] = div_rn(1.0, piv);
+                    for (int q = p + 1; q < k; ++q) {
+                        const double l = M[q][p] * inv[p];
+                        for (int j = p + 1; j < k; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
+                        rhs[q] = fma(-l, rhs[p], rhs[q]);
+                    }
+                }
+                for (int p = k - 1; p >= 0; --p) {
+                    double s = rhs[p];
+                    for (int j = p + 1; j < k; ++j) s = fma(-M[p][j], u[j], s);
+                    u[p] = s * inv[p];
+                }
+            }
+            for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
+        }
+        __syncthreads();
+    }
+    if (fl) atomicOr(A.flag, 1);
+    for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
+        const int lx = e % T0, ly = e / T0;
+        A.xn[gidx(G, gxo(lx), gyo(ly), 0)] = XN[wi(lx, ly)];
+    }
+}
+
+inline cudaError_t launch_sweep9(const Sweep9Args &A, cudaStream_t s) {
+    const size_t sm = sweep9_smem(A.G);
+    static size_t attr = 0;
+    if (sm > attr) {
+        cudaFuncSetAttribute(k_sweep9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = sm;
+    }
+    const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1]);
+    k_sweep9<<<tiles, s9::NT, sm, s>>>(A);
+    return cudaGetLastError();
+}
+
+}  // namespace sw

@@ -15,7 +15,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUITES = ["tests/test_gpu_parity.py", "tests/test_gpu_degenerate.py", "tests/test_gpu_msteps.py", "tests/test_gpu_eikonal.py"]
+SUITES = ["tests/test_gpu_parity.py", "tests/test_gpu_degenerate.py", "tests/test_gpu_msteps.py", "tests/test_gpu_eikonal.py",
+          "tests/test_gpu_ninepoint.py"]
 
 
 @pytest.mark.parametrize("seed", [1, 7, 12345])
