@@ -706,7 +706,7 @@ static sw_status run_sweeps(sw_grid *g, int kind, const double *w8, int nsweeps,
     sw_status st;
     const int sa = g->dim - 1, R = g->G.nt[sa];
     const bool multi = g->comm && g->nranks > 1;
-    if (multi && kind == SK_SOR && !g->bghost_ok && nsweeps > 0) {   // partner nodes' right-hand sides
+    if (multi && kind != SK_EIK && !g->bghost_ok && nsweeps > 0) {   // partner nodes' right-hand sides
         if ((st = exch(g, g->B, 2, cs)) != SW_OK) return st;
         g->bghost_ok = true;
     }
