@@ -448,6 +448,42 @@ def run_secondary(args):
                             "ms_per_iteration": round(dt / max(it, 1) * 1e3, 3)}
     del g
     torch.cuda.empty_cache()
+    # ---- SURVEY §8(f) N3 / N4 on config 3's grid (4096^2, 64 x 64 boxes): the nine-point sweep
+    # (Mehrstellen Laplacian, 56 algorithmic B/LUP: x r/w, b, 2 axis + 2 diagonal coefficient arrays)
+    # and the eikonal fast-sweeping pass (24 B/LUP: u r/w, slowness), per-pass time and HBM fraction
+    n = 4096
+    g9 = binding.Grid(2, (n, n), binding.COEF_FACES).decompose((64, 64))
+    F9 = [np.full(tuple(reversed((n + (a == 0), n + (a == 1)))), 4.0) for a in range(2)]
+    g9.set_faces_global(F9)
+    del F9
+    g9.set_diagonals(np.ones((n + 1, n + 1)), np.ones((n + 1, n + 1)))
+    g9.set_vector(binding.B, gen.uniform_field(args.seed, gen.STREAM_RHS, (n, n)) / float((n + 1) ** 2))
+    ms = _time_sweeps(g9, [1.0], 20)
+    out["n3_sweep9"] = {"n": [n, n], "tile": [64, 64], "stencil": "Mehrstellen 9-point", "ms_per_sweep": round(ms, 4),
+                        "glups": round(n * n / (ms * 1e-3) / 1e9, 2), "algorithmic_B_per_lup": 56,
+                        "frac_of_measured_hbm": round(56 * n * n / (ms * 1e-3) / 1e9 / peaks()[0], 3)}
+    del g9
+    ge = binding.Grid(2, (n, n)).decompose((64, 64))
+    ge.set_slowness(0.5 + gen.uniform_field(args.seed, gen.STREAM_TEST, (n, n)) ** 2, 1.0 / n)
+    u0 = np.full((n, n), np.inf)
+    u0[n // 3, n // 2] = 0.0
+    ge.set_vector(binding.X, u0)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ph = ge.eikonal_sweep(8, 0)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 8
+    t0 = time.perf_counter()
+    while ge.eikonal_changes() > 0 and ph < 4000:
+        ph = ge.eikonal_sweep(8, ph)
+    out["n4_eikonal"] = {"n": [n, n], "tile": [64, 64], "ms_per_pass": round(ms, 4),
+                         "glups": round(n * n / (ms * 1e-3) / 1e9, 2), "algorithmic_B_per_lup": 24,
+                         "frac_of_measured_hbm": round(24 * n * n / (ms * 1e-3) / 1e9 / peaks()[0], 3),
+                         "passes_to_fixed_point": ph, "seconds_to_fixed_point": round(time.perf_counter() - t0, 3)}
+    del ge, u0
     # ---- config 1: 1D Poisson n = 1024, 4 boxes, SOR at omega_opt until relres < 1e-8
     n1 = 1024
     g1d = binding.Grid(1, (n1,)).decompose((256,))
