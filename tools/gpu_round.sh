@@ -8,7 +8,7 @@ mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 lscpu > $OUT/lscpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAILED; tail -20 $OUT/build.log; exit 1; }
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 180 > $OUT/pytest_gpu.log 2>&1; echo "pytest gpu exit $?"; tail -3 $OUT/pytest_gpu.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 1500 > $OUT/pytest_gpu.log 2>&1; echo "pytest gpu exit $?"; tail -3 $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?"; tail -2 $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?"; cat $OUT/bench.json
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref exit $?"; cat $OUT/bench_ref.json
