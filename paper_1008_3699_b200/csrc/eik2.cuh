@@ -5,20 +5,22 @@
 // SOR sweep's 2-member pairs and 4-member corner) solved exactly by ordered fixing (R-E3): the same
 // operations in the same order as the oracle's or_eik_sweep, so the result is bitwise equal.
 //
-// One CTA of 64 threads per box (T0, T1 <= 64).  Shared memory holds the old values of the box
-// and its 2-node halo in LOCAL coordinates (local +a points away from the box's start corner; a
-// node outside the domain reads +inf) and the slowness of the active nodes (own and partner
-// layers).  Level d = x + y of the own nodes: thread t takes own node (t, d - t); a node on a
-// coupled start face solves its set with the partner layer; results go in place (the window then
-// holds new values on every node's start side and old values on its end side, exactly the split
-// the method prescribes); one barrier per level; write-back of the box.
+// One CTA of 256 threads per box (T0, T1 <= 64).  All threads stage in the old values of the box and
+// its 2-node halo in LOCAL coordinates (local +a points away from the box's start corner; a node
+// outside the domain reads +inf) and the slowness of the active nodes (own and partner layers).
+// Level d = x + y of the own nodes: thread t < 64 takes own node (t, d - t) -- directly from the
+// window when it is in no coupled set, else with its partner layer by ordered fixing; results go
+// in place (the window then holds new values on every node's start side and old values on its end
+// side, exactly the split the method prescribes); a named barrier of the 64 level threads per
+// level; write-back of the box by all threads.
 #pragma once
 #include "common.cuh"
 
 namespace sw {
 
 namespace ek {
-constexpr int NT = 64;
+constexpr int NT = 256;   // threads per CTA: stage-in / write-back by all, the levels by the first LT
+constexpr int LT = 64;    // one thread per box column (T0 <= 64)
 }
 
 struct Eik2Args {
@@ -47,10 +49,10 @@ inline size_t eik2_smem(const Geo &G) {
 }
 
 inline bool eik2_supported(const Geo &G) {
-    return G.dim == 2 && G.T[0] <= ek::NT && G.T[1] <= ek::NT && eik2_smem(G) <= 227 * 1024;
+    return G.dim == 2 && G.T[0] <= ek::LT && G.T[1] <= ek::LT && eik2_smem(G) <= 227 * 1024;
 }
 
-__global__ void __launch_bounds__(ek::NT) k_eik2(Eik2Args A) {
+__global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
     extern __shared__ __align__(16) double esm[];
     SW_JITTER_POINT();
     const Geo &G = A.G;
@@ -70,21 +72,69 @@ __global__ void __launch_bounds__(ek::NT) k_eik2(Eik2Args A) {
     auto uw = [&](int lx, int ly) -> double & { return U[(ly + 2) * WX + (lx + 2)]; };
     auto fw = [&](int lx, int ly) -> double { return F[(ly + 1) * FX + (lx + 1)]; };
     // ---- stage in (old values, +inf outside the domain; slowness of the active region)
+#pragma unroll 4
     for (int e = threadIdx.x; e < WX * (T1 + 4); e += ek::NT) {
         const int lx = e % WX - 2, ly = e / WX - 2;
         const int64_t gx = gxo(lx), gy = gyo(ly);
         const bool in = gx >= 0 && gx < G.ng[0] && gy >= 0 && gy < G.ng[1];
-        U[e] = in ? A.uo[gidx(G, gx, gy, 0)] : eik_inf();
-        if (lx >= -1 && lx < T0 && ly >= -1 && ly < T1)
-            F[(ly + 1) * FX + (lx + 1)] = in ? A.S[gidx(G, gx, gy, 0)] : 1.0;
+        const bool act = lx >= -1 && lx < T0 && ly >= -1 && ly < T1;
+        const int64_t gi = in ? gidx(G, gx, gy, 0) : 0;
+        const double uv = in ? __ldg(A.uo + gi) : eik_inf();
+        const double sv = (in && act) ? __ldg(A.S + gi) : 1.0;
+        U[e] = uv;
+        if (act) F[(ly + 1) * FX + (lx + 1)] = sv;
     }
     __syncthreads();
+    if (threadIdx.x >= ek::LT) {           // the other warps rejoin for the write-back
+        __syncthreads();
+        for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
+            const int lx = e % T0, ly = e / T0;
+            A.un[gidx(G, gxo(lx), gyo(ly), 0)] = uw(lx, ly);
+        }
+        return;
+    }
     // ---- levels
     const int t = threadIdx.x;
     for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
         const int x = t, y = d - t;
-        if (x < T0 && y >= 0 && y < T1) {
-            // members of the node's set in local coordinates
+        const bool single = !((x == 0 && cx) || (y == 0 && cy));
+        if (x < T0 && y >= 0 && y < T1 && single) {
+            // a node outside every coupled set: its window neighbours are new on its start side,
+            // old elsewhere (in place, level order), exactly the oracle's values
+            const double a = fmin(uw(x - 1, y), uw(x + 1, y)), b = fmin(uw(x, y - 1), uw(x, y + 1));
+            const double ub = eik_godunov_d(a, b, __dmul_rn(fw(x, y), A.h));
+            const double uo = uw(x, y);
+            uw(x, y) = uo < ub ? uo : ub;
+        } else if (x < T0 && y >= 0 && y < T1 && !(x == 0 && y == 0 && cx && cy)) {
+            // a pair across one coupled start face, ordered fixing written out (R-E3): both
+            // candidates with the other member at +inf, the smaller (ties: lower global index) is
+            // fixed, the other recomputed with it
+            const bool xf = x == 0 && cx;
+            const int qx = xf ? -1 : x, qy = xf ? y : -1;
+            auto cand = [&](int px, int py, int ox, int oy, double ov) {
+                const double w0 = (px - 1 == ox && py == oy) ? ov : uw(px - 1, py);
+                const double w1 = (px + 1 == ox && py == oy) ? ov : uw(px + 1, py);
+                const double v0 = (px == ox && py - 1 == oy) ? ov : uw(px, py - 1);
+                const double v1 = (px == ox && py + 1 == oy) ? ov : uw(px, py + 1);
+                const double ub = eik_godunov_d(fmin(w0, w1), fmin(v0, v1), __dmul_rn(fw(px, py), A.h));
+                const double uo = uw(px, py);
+                return uo < ub ? uo : ub;
+            };
+            const double cp = cand(x, y, qx, qy, eik_inf()), cq = cand(qx, qy, x, y, eik_inf());
+            const int64_t gp = gyo(y) * G.ng[0] + gxo(x), gq = gyo(qy) * G.ng[0] + gxo(qx);
+            const bool pfirst = gp < gq ? !(cq < cp) : (cp < cq);
+            double up, uq;
+            if (pfirst) {
+                up = cp;
+                uq = cand(qx, qy, x, y, up);
+            } else {
+                uq = cq;
+                up = cand(x, y, qx, qy, uq);
+            }
+            uw(x, y) = up;
+            uw(qx, qy) = uq;
+        } else if (x < T0 && y >= 0 && y < T1) {
+            // the corner set (4 members) in local coordinates, generic ordered fixing
             int mx[4], my[4], k = 1;
             mx[0] = x;
             my[0] = y;
@@ -138,8 +188,10 @@ __global__ void __launch_bounds__(ek::NT) k_eik2(Eik2Args A) {
             }
             for (int m = 0; m < k; ++m) uw(mx[m], my[m]) = val[m];
         }
-        __syncthreads();
+        asm volatile("bar.sync 1, %0;" ::"r"(ek::LT) : "memory");   // the level threads only
+        SW_JITTER_POINT();
     }
+    __syncthreads();                          // with the waiting warps
     // ---- write-back of the box
     for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
         const int lx = e % T0, ly = e / T0;

@@ -11,11 +11,13 @@
 // elimination (no pivoting, ascending global index) in neighbour order W, E, S, N, SW, SE, NW, NE:
 // bitwise equal results.
 //
-// One CTA of 64 threads per box (T0, T1 <= 64): the old values of the box and its 2-node halo in
-// shared memory in LOCAL coordinates (local +a points away from the box's start corner), a second
-// window receives the new values; front d = x + y of the own nodes, thread t takes node (t, d - t)
-// with its partner(s) across coupled start faces, one barrier per front; coefficients and b are read
-// from global memory (L1 / L2).
+// One CTA of 256 threads per box (T0, T1 <= 64): the old values of the box and its 2-node halo in
+// shared memory in LOCAL coordinates (local +a points away from the box's start corner); all threads
+// then compute alpha and the explicit part r0 of every node of local [-1, T)^2 (own nodes and partner
+// layers) into a second window and an alpha window; front d = x + y of the own nodes: thread t < 64
+// takes node (t, d - t) (its implicit neighbours are local W, S, SW) or, on a coupled start face,
+// its set with the partner layer; a named barrier of the 64 front threads per front; write-back by
+// all threads.  Implicit couplings are read from global memory (L1 / L2).
 #pragma once
 #include "common.cuh"
 #include "sweep2p.cuh"
@@ -23,7 +25,8 @@
 namespace sw {
 
 namespace s9 {
-constexpr int NT = 64;
+constexpr int NT = 256;   // threads per CTA: the prologue and write-back by all, the fronts by the first LT
+constexpr int LT = 64;    // one thread per box column (T0 <= 64)
 __constant__ int NBX[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
 __constant__ int NBY[8] = {0, 0, -1, 1, -1, -1, 1, 1};
 }  // namespace s9
@@ -38,18 +41,28 @@ struct Sweep9Args {
     int *flag;
 };
 
-inline size_t sweep9_smem(const Geo &G) { return 2 * sizeof(double) * (size_t)(G.T[0] + 4) * (G.T[1] + 4); }
-
-inline bool sweep9_supported(const Geo &G) {
-    return G.dim == 2 && G.T[0] <= s9::NT && G.T[1] <= s9::NT && sweep9_smem(G) <= 227 * 1024;
+// region 0: the x_old window over local [-2, T + 2), later the coupled-set coefficients (8 per node
+// of the start-face layers, 16 (T0 + T1) doubles); then (r0, later the new values) over local
+// [-2, T + 2) and alpha over local [-1, T)
+__host__ __device__ inline int sweep9_r0(int T0, int T1) {
+    const int w = (T0 + 4) * (T1 + 4), c = 16 * (T0 + T1);
+    return w > c ? w : c;
+}
+inline size_t sweep9_smem(const Geo &G) {
+    return sizeof(double) * ((size_t)sweep9_r0(G.T[0], G.T[1]) + (size_t)(G.T[0] + 4) * (G.T[1] + 4) +
+                             (size_t)(G.T[0] + 1) * (G.T[1] + 1));
 }
 
-__global__ void __launch_bounds__(s9::NT) k_sweep9(Sweep9Args A) {
+inline bool sweep9_supported(const Geo &G) {
+    return G.dim == 2 && G.T[0] <= s9::LT && G.T[1] <= s9::LT && sweep9_smem(G) <= 227 * 1024;
+}
+
+__global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     extern __shared__ __align__(16) double s9m[];
     SW_JITTER_POINT();
     const Geo &G = A.G;
-    const int T0 = G.T[0], T1 = G.T[1], WX = T0 + 4;
-    double *const XO = s9m, *const XN = s9m + WX * (T1 + 4);
+    const int T0 = G.T[0], T1 = G.T[1], WX = T0 + 4, AX = T0 + 1;
+    double *const XO = s9m, *const XN = s9m + sweep9_r0(T0, T1), *const AW = XN + WX * (T1 + 4);
     const int tx = blockIdx.x % G.nt[0], ty = blockIdx.x / G.nt[0];
     const int64_t R0 = tx, R1 = ty + G.toff[1];
     const int sx = ((A.base >> 0) & 1) ^ (int)(R0 & 1);
@@ -60,34 +73,112 @@ __global__ void __launch_bounds__(s9::NT) k_sweep9(Sweep9Args A) {
     auto gxo = [&](int lx) { return X0 + (sx ? T0 - 1 - lx : lx); };
     auto gyo = [&](int ly) { return Y0 + (sy ? T1 - 1 - ly : ly); };
     auto wi = [&](int lx, int ly) { return (ly + 2) * WX + (lx + 2); };
+    auto ai = [&](int lx, int ly) { return (ly + 1) * AX + (lx + 1); };
     auto inside = [&](int64_t gx, int64_t gy) { return gx >= 0 && gx < G.ng[0] && gy >= 0 && gy < G.ng[1]; };
     // coefficient of global neighbour k of global node (gx, gy)
     auto coef = [&](int k, int64_t gx, int64_t gy) -> double {
         const int dx = s9::NBX[k], dy = s9::NBY[k];
         const int64_t cxg = gx + (dx > 0), cyg = gy + (dy > 0);
-        if (dy == 0) return A.f0 ? A.f0[gidx(G, cxg, gy, 0)] : 1.0;
-        if (dx == 0) return A.f1 ? A.f1[gidx(G, gx, cyg, 0)] : 1.0;
-        return (dx == dy ? A.dd : A.da)[gidx(G, cxg, cyg, 0)];
+        if (dy == 0) return A.f0 ? __ldg(A.f0 + gidx(G, cxg, gy, 0)) : 1.0;
+        if (dx == 0) return A.f1 ? __ldg(A.f1 + gidx(G, gx, cyg, 0)) : 1.0;
+        return __ldg((dx == dy ? A.dd : A.da) + gidx(G, cxg, cyg, 0));
     };
-    // box offset of a local coordinate and the start side of that box in local coordinates
-    // (A's box starts at local 0 and moves +; every neighbouring box's start side is +)
+    // start side of the box containing local coordinate l (A starts at local 0 and moves +;
+    // every neighbouring box's start side is +); q implicit for p iff on p's start side along every
+    // axis where they differ (R-N3)
     auto side = [&](int l, int T) { return (l >= 0 && l < T) ? -1 : +1; };
-    // q (local) implicit for p (local): on p's start side along every axis where they differ
     auto implicit = [&](int px, int py, int qx, int qy) {
         const int sxp = side(px, T0), syp = side(py, T1);
         const bool okx = qx == px || (sxp < 0 ? qx < px : qx > px);
         const bool oky = qy == py || (syp < 0 ? qy < py : qy > py);
         return okx && oky;
     };
-    // stage in the old window (0 outside the domain: Dirichlet data are folded into b)
+    auto lnb = [&](int p, int kk, int &qx, int &qy, int px, int py) {
+        qx = px + (sx ? -s9::NBX[kk] : s9::NBX[kk]);
+        qy = py + (sy ? -s9::NBY[kk] : s9::NBY[kk]);
+        (void)p;
+    };
+    // ---- stage in the old window (0 outside the domain: Dirichlet data are folded into b)
+#pragma unroll 4
     for (int e = threadIdx.x; e < WX * (T1 + 4); e += s9::NT) {
         const int lx = e % WX - 2, ly = e / WX - 2;
         const int64_t gx = gxo(lx), gy = gyo(ly);
-        XO[e] = inside(gx, gy) ? A.xo[gidx(G, gx, gy, 0)] : 0.0;
+        XO[e] = inside(gx, gy) ? __ldg(A.xo + gidx(G, gx, gy, 0)) : 0.0;
     }
     __syncthreads();
+    // ---- explicit parts of every node of local [-1, T)^2 inside the domain (own nodes and the
+    // partner layers): alpha = w / a_P, r0 = fma(alpha, b + sum_explicit c u_old, (1 - w) u_old)
+    for (int e = threadIdx.x; e < AX * (T1 + 1); e += s9::NT) {
+        const int px = e % AX - 1, py = e / AX - 1;
+        const int64_t gx = gxo(px), gy = gyo(py);
+        if (!inside(gx, gy)) continue;
+        double c8[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) c8[kk] = coef(kk, gx, gy);
+        const double bv = __ldg(A.b + gidx(G, gx, gy, 0));
+        const double ap = ((c8[0] + c8[1]) + (c8[2] + c8[3])) + ((c8[4] + c8[7]) + (c8[5] + c8[6])) + G.beta;
+        const int bits = (sx ^ (px < 0 ? 1 : 0)) | ((sy ^ (py < 0 ? 1 : 0)) << 1);
+        const double w = A.omega[bits];
+        const double al = div_rn(w, ap);
+        double ev = bv;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
+            int qx, qy;
+            lnb(0, kk, qx, qy, px, py);
+            if (implicit(px, py, qx, qy)) continue;
+            ev = fma(c8[kk], XO[wi(qx, qy)], ev);
+        }
+        XN[wi(px, py)] = fma(al, ev, (1.0 - w) * XO[wi(px, py)]);
+        AW[ai(px, py)] = al;
+    }
+    __syncthreads();
+    // ---- the 8 coefficients of every node that can be in a coupled set (local x in {-1, 0} or
+    // local y in {-1, 0}), into the x_old window's space (dead from here on)
+    const int nslot = 2 * (T1 + 1) + 2 * (T0 - 1);
+    double *const CS = XO;
+    auto slot = [&](int lx, int ly) {
+        return lx <= 0 ? (lx + 1) * (T1 + 1) + (ly + 1) : 2 * (T1 + 1) + (ly + 1) * (T0 - 1) + (lx - 1);
+    };
+    for (int e = threadIdx.x; e < nslot * 8; e += s9::NT) {
+        const int sl = e >> 3, kk = e & 7;
+        int lx, ly;
+        if (sl < 2 * (T1 + 1)) {
+            lx = sl / (T1 + 1) - 1;
+            ly = sl % (T1 + 1) - 1;
+        } else {
+            const int r = sl - 2 * (T1 + 1);
+            lx = r % (T0 - 1) + 1;
+            ly = r / (T0 - 1) - 1;
+        }
+        const int64_t gx = gxo(lx), gy = gyo(ly);
+        CS[e] = inside(gx, gy) ? coef(kk, gx, gy) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x >= s9::LT) {            // the other warps rejoin for the write-back
+        __syncthreads();
+        for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
+            const int lx = e % T0, ly = e / T0;
+            A.xn[gidx(G, gxo(lx), gyo(ly), 0)] = XN[wi(lx, ly)];
+        }
+        return;
+    }
     const int t = threadIdx.x;
     int fl = 0;
+    // implicit neighbours of an own node outside the sets: local W, S, SW, always in this order in
+    // the oracle's global neighbour order; their coefficients come two fronts ahead (a register ring)
+    const int kW = sx ? 1 : 0, kS = sy ? 3 : 2, kSW = 4 + sx + 2 * sy;
+    double ring[2][3];
+    auto fetch = [&](int yy, double (&c)[3]) {
+        if (t < T0 && yy < T1) {
+            const int64_t gx = gxo(t), gy = gyo(yy);
+            c[0] = coef(kW, gx, gy);
+            c[1] = coef(kS, gx, gy);
+            c[2] = coef(kSW, gx, gy);
+        }
+    };
+    fetch(0, ring[0]);
+    fetch(1, ring[1]);
     for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
         const int x = t, y = d - t;
         if (x < T0 && y >= 0 && y < T1) {
@@ -104,53 +195,48 @@ __global__ void __launch_bounds__(s9::NT) k_sweep9(Sweep9Args A) {
                 mx[1] = x; my[1] = -1;
                 k = 2;
             }
-            int64_t gi[4];
-            for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
-            for (int a1 = 1; a1 < k; ++a1)
-                for (int b1 = a1; b1 > 0 && gi[b1 - 1] > gi[b1]; --b1) {
-                    int64_t tg = gi[b1]; gi[b1] = gi[b1 - 1]; gi[b1 - 1] = tg;
-                    int tt = mx[b1]; mx[b1] = mx[b1 - 1]; mx[b1 - 1] = tt;
-                    tt = my[b1]; my[b1] = my[b1 - 1]; my[b1 - 1] = tt;
-                }
-            double M[4][4], rhs[4], u[4];
-            for (int p = 0; p < k; ++p) {
-                const int px = mx[p], py = my[p];
-                const int64_t gx = gxo(px), gy = gyo(py);
-                double c8[8];
-                for (int kk = 0; kk < 8; ++kk) c8[kk] = coef(kk, gx, gy);
-                const double ap = ((c8[0] + c8[1]) + (c8[2] + c8[3])) + ((c8[4] + c8[7]) + (c8[5] + c8[6])) + G.beta;
-                // the node's own box's direction bits: A's, flipped along axes where it lies outside A
-                const int bits = (sx ^ (px < 0 || px >= T0 ? 1 : 0)) | ((sy ^ (py < 0 || py >= T1 ? 1 : 0)) << 1);
-                const double w = A.omega[bits];
-                const double al = div_rn(w, ap);
-                double e = A.b[gidx(G, gx, gy, 0)];
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int64_t qgx = gx + s9::NBX[kk], qgy = gy + s9::NBY[kk];
-                    if (!inside(qgx, qgy)) continue;
-                    const int qx = px + (sx ? -s9::NBX[kk] : s9::NBX[kk]), qy = py + (sy ? -s9::NBY[kk] : s9::NBY[kk]);
-                    if (implicit(px, py, qx, qy)) continue;
-                    e = fma(c8[kk], XO[wi(qx, qy)], e);
-                }
-                double acc = fma(al, e, (1.0 - w) * XO[wi(px, py)]);
-                for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int64_t qgx = gx + s9::NBX[kk], qgy = gy + s9::NBY[kk];
-                    if (!inside(qgx, qgy)) continue;
-                    const int qx = px + (sx ? -s9::NBX[kk] : s9::NBX[kk]), qy = py + (sy ? -s9::NBY[kk] : s9::NBY[kk]);
-                    if (!implicit(px, py, qx, qy)) continue;
-                    const double m = al * c8[kk];
-                    int in = -1;
-                    for (int q = 0; q < k; ++q)
-                        if (mx[q] == qx && my[q] == qy) in = q;
-                    if (in >= 0) M[p][in] = -m;
-                    else acc = fma(m, XN[wi(qx, qy)], acc);
-                }
-                rhs[p] = acc;
-            }
             if (k == 1) {
-                u[0] = rhs[0];
-            } else {                                       // the oracle's ge_solve (R-8)
-                double inv[4];
+                // (a neighbour outside the domain holds 0 and is skipped, as in the oracle)
+                const int64_t gx = gxo(x), gy = gyo(y);
+                const double al = AW[ai(x, y)];
+                const double(&c)[3] = ring[y & 1];
+                double acc = XN[wi(x, y)];
+                if (inside(gx + s9::NBX[kW], gy)) acc = fma(al * c[0], XN[wi(x - 1, y)], acc);
+                if (inside(gx, gy + s9::NBY[kS])) acc = fma(al * c[1], XN[wi(x, y - 1)], acc);
+                if (inside(gx + s9::NBX[kSW], gy + s9::NBY[kSW])) acc = fma(al * c[2], XN[wi(x - 1, y - 1)], acc);
+                XN[wi(x, y)] = acc;
+            } else {
+                int64_t gi[4];
+                for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
+                for (int a1 = 1; a1 < k; ++a1)
+                    for (int b1 = a1; b1 > 0 && gi[b1 - 1] > gi[b1]; --b1) {
+                        int64_t tg = gi[b1]; gi[b1] = gi[b1 - 1]; gi[b1 - 1] = tg;
+                        int tt = mx[b1]; mx[b1] = mx[b1 - 1]; mx[b1 - 1] = tt;
+                        tt = my[b1]; my[b1] = my[b1 - 1]; my[b1 - 1] = tt;
+                    }
+                double M[4][4], rhs[4], u[4];
+                for (int p = 0; p < k; ++p) {
+                    const int px = mx[p], py = my[p];
+                    const int64_t gx = gxo(px), gy = gyo(py);
+                    const double al = AW[ai(px, py)];
+                    double acc = XN[wi(px, py)];
+                    for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
+                    const double *cs = CS + 8 * slot(px, py);
+                    for (int kk = 0; kk < 8; ++kk) {
+                        if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
+                        int qx, qy;
+                        lnb(0, kk, qx, qy, px, py);
+                        if (!implicit(px, py, qx, qy)) continue;
+                        const double m = al * cs[kk];
+                        int in = -1;
+                        for (int q = 0; q < k; ++q)
+                            if (mx[q] == qx && my[q] == qy) in = q;
+                        if (in >= 0) M[p][in] = -m;
+                        else acc = fma(m, XN[wi(qx, qy)], acc);
+                    }
+                    rhs[p] = acc;
+                }
+                double inv[4];                             // the oracle's ge_solve (R-8)
                 for (int p = 0; p < k; ++p) {
                     const double piv = M[p][p];
                     fl |= !(fabs(piv) >= 1e-14);
@@ -162,16 +248,19 @@ __global__ void __launch_bounds__(s9::NT) k_sweep9(Sweep9Args A) {
                     }
                 }
                 for (int p = k - 1; p >= 0; --p) {
-                    double s = rhs[p];
-                    for (int j = p + 1; j < k; ++j) s = fma(-M[p][j], u[j], s);
-                    u[p] = s * inv[p];
+                    double sacc = rhs[p];
+                    for (int j = p + 1; j < k; ++j) sacc = fma(-M[p][j], u[j], sacc);
+                    u[p] = sacc * inv[p];
                 }
+                for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
             }
-            for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
         }
-        __syncthreads();
+        if (x < T0 && y >= 0 && y < T1) fetch(y + 2, ring[y & 1]);   // two fronts ahead
+        asm volatile("bar.sync 1, %0;" ::"r"(s9::LT) : "memory");
+        SW_JITTER_POINT();
     }
     if (fl) atomicOr(A.flag, 1);
+    __syncthreads();                          // with the waiting warps
     for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
         const int lx = e % T0, ly = e / T0;
         A.xn[gidx(G, gxo(lx), gyo(ly), 0)] = XN[wi(lx, ly)];
