@@ -182,19 +182,10 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
         const int x = t, y = d - t;
         if (x < T0 && y >= 0 && y < T1) {
-            int mx[4], my[4], k = 1;
-            mx[0] = x;
-            my[0] = y;
-            if (x == 0 && y == 0 && cx && cy) {
-                mx[1] = -1; my[1] = 0; mx[2] = 0; my[2] = -1; mx[3] = -1; my[3] = -1;
-                k = 4;
-            } else if (x == 0 && cx) {
-                mx[1] = -1; my[1] = y;
-                k = 2;
-            } else if (y == 0 && cy) {
-                mx[1] = x; my[1] = -1;
-                k = 2;
-            }
+            // (no arrays on the common paths: dynamically indexed arrays would live in local memory)
+            const bool corner = x == 0 && y == 0 && cx && cy;
+            const bool xpair = !corner && x == 0 && cx, ypair = !corner && !xpair && y == 0 && cy;
+            const int k = corner ? 4 : ((xpair || ypair) ? 2 : 1);
             if (k == 1) {
                 // (a neighbour outside the domain holds 0 and is skipped, as in the oracle)
                 const int64_t gx = gxo(x), gy = gyo(y);
@@ -205,7 +196,46 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 if (inside(gx, gy + s9::NBY[kS])) acc = fma(al * c[1], XN[wi(x, y - 1)], acc);
                 if (inside(gx + s9::NBX[kSW], gy + s9::NBY[kSW])) acc = fma(al * c[2], XN[wi(x - 1, y - 1)], acc);
                 XN[wi(x, y)] = acc;
+            } else if (k == 2) {
+                // a pair across one coupled start face, in registers: members in ascending global
+                // index, rows (1, -m01; -m10, 1), the oracle's ge_solve for K = 2 written out
+                const int px2 = xpair ? -1 : x, py2 = xpair ? y : -1;
+                const bool sw01 = gyo(py2) * G.ng[0] + gxo(px2) < gyo(y) * G.ng[0] + gxo(x);
+                const int ax = sw01 ? px2 : x, ay = sw01 ? py2 : y;
+                const int bx = sw01 ? x : px2, by = sw01 ? y : py2;
+                auto row = [&](int px, int py, int ox, int oy, double &moff) {
+                    const int64_t gx = gxo(px), gy = gyo(py);
+                    const double al = AW[ai(px, py)];
+                    const double *cs = CS + 8 * slot(px, py);
+                    double acc = XN[wi(px, py)];
+                    moff = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
+                        int qx, qy;
+                        lnb(0, kk, qx, qy, px, py);
+                        if (!implicit(px, py, qx, qy)) continue;
+                        const double m = al * cs[kk];
+                        if (qx == ox && qy == oy) moff = -m;
+                        else acc = fma(m, XN[wi(qx, qy)], acc);
+                    }
+                    return acc;
+                };
+                double m01, m10;
+                const double r0a = row(ax, ay, bx, by, m01), r0b = row(bx, by, ax, ay, m10);
+                const double inv0 = div_rn(1.0, 1.0);
+                const double l = m10 * inv0;
+                const double m11 = fma(-l, m01, 1.0);
+                const double rb = fma(-l, r0a, r0b);
+                fl |= !(fabs(m11) >= 1e-14);
+                const double inv1 = div_rn(1.0, m11);
+                const double ub = rb * inv1;
+                const double ua = fma(-m01, ub, r0a) * inv0;
+                XN[wi(ax, ay)] = ua;
+                XN[wi(bx, by)] = ub;
             } else {
+                // the corner set: the four start-corner nodes, a dense 4 x 4 (once per box)
+                int mx[4] = {0, -1, 0, -1}, my[4] = {0, 0, -1, -1};
                 int64_t gi[4];
                 for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
                 for (int a1 = 1; a1 < k; ++a1)
