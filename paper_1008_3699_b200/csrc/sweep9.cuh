@@ -15,9 +15,9 @@
 // shared memory in LOCAL coordinates (local +a points away from the box's start corner); all threads
 // then compute alpha and the explicit part r0 of every node of local [-1, T)^2 (own nodes and partner
 // layers) into a second window and an alpha window; front d = x + y of the own nodes: thread t < 64
-// takes node (t, d - t) (its implicit neighbours are local W, S, SW) or, on a coupled start face,
-// its set with the partner layer; a named barrier of the 64 front threads per front; write-back by
-// all threads.  Implicit couplings are read from global memory (L1 / L2).
+// takes node (t, d - t) unless it is on a coupled start face (its implicit neighbours are local W,
+// S, SW); a third warp solves the front's coupled sets (the x- and y-face pairs, the corner); a named
+// barrier of those 96 threads per front; write-back by all threads.  Implicit couplings are read from global memory (L1 / L2).
 #pragma once
 #include "common.cuh"
 #include "sweep2p.cuh"
@@ -26,7 +26,9 @@ namespace sw {
 
 namespace s9 {
 constexpr int NT = 256;   // threads per CTA: the prologue and write-back by all, the fronts by the first LT
-constexpr int LT = 64;    // one thread per box column (T0 <= 64)
+constexpr int LT = 64;    // one thread per box column (T0 <= 64): the nodes outside the coupled sets
+constexpr int FT = 96;    // threads on the fronts: LT + one warp for the coupled sets (lanes 0 / 1: the
+                          // x- / y-face pair of the front, lane 2: the corner set)
 __constant__ int NBX[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
 __constant__ int NBY[8] = {0, 0, -1, 1, -1, -1, 1, 1};
 }  // namespace s9
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         CS[e] = inside(gx, gy) ? coef(kk, gx, gy) : 0.0;
     }
     __syncthreads();
-    if (threadIdx.x >= s9::LT) {            // the other warps rejoin for the write-back
+    if (threadIdx.x >= s9::FT) {            // the other warps rejoin for the write-back
         __syncthreads();
         for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
             const int lx = e % T0, ly = e / T0;
@@ -168,21 +170,30 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     // implicit neighbours of an own node outside the sets: local W, S, SW, always in this order in
     // the oracle's global neighbour order; their coefficients come two fronts ahead (a register ring)
     const int kW = sx ? 1 : 0, kS = sy ? 3 : 2, kSW = 4 + sx + 2 * sy;
-    double ring[2][3];
-    auto fetch = [&](int yy, double (&c)[3]) {
+    // (two named register triples, rotated: a dynamically indexed ring would live in local memory)
+    double cw0 = 0.0, cs0 = 0.0, cd0 = 0.0, cw1 = 0.0, cs1 = 0.0, cd1 = 0.0;
+    auto fetch = [&](int yy, double &a, double &b, double &c) {
         if (t < T0 && yy < T1) {
             const int64_t gx = gxo(t), gy = gyo(yy);
-            c[0] = coef(kW, gx, gy);
-            c[1] = coef(kS, gx, gy);
-            c[2] = coef(kSW, gx, gy);
+            a = coef(kW, gx, gy);
+            b = coef(kS, gx, gy);
+            c = coef(kSW, gx, gy);
         }
     };
-    fetch(0, ring[0]);
-    fetch(1, ring[1]);
+    fetch(0, cw0, cs0, cd0);
+    fetch(1, cw1, cs1, cd1);
     for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
-        const int x = t, y = d - t;
-        if (x < T0 && y >= 0 && y < T1) {
-            // (no arrays on the common paths: dynamically indexed arrays would live in local memory)
+        // fronts: threads < LT the nodes outside the coupled sets (one branch-free path); one more
+        // warp the sets of the front, so the two kinds never diverge inside a warp
+        const int x = t < s9::LT ? t : ((t - s9::LT) == 1 ? d : 0);
+        const int y = t < s9::LT ? d - t : ((t - s9::LT) == 1 ? 0 : d);
+        const bool member = (x == 0 && cx) || (y == 0 && cy);
+        const int lane = t - s9::LT;
+        const bool valid = x < T0 && y >= 0 && y < T1 &&
+                           (t < s9::LT ? !member
+                                       : (lane == 0 ? (cx && !(d == 0 && cy))
+                                                    : (lane == 1 ? (cy && !(d == 0 && cx)) : (lane == 2 && d == 0 && cx && cy))));
+        if (valid) {
             const bool corner = x == 0 && y == 0 && cx && cy;
             const bool xpair = !corner && x == 0 && cx, ypair = !corner && !xpair && y == 0 && cy;
             const int k = corner ? 4 : ((xpair || ypair) ? 2 : 1);
@@ -190,11 +201,10 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 // (a neighbour outside the domain holds 0 and is skipped, as in the oracle)
                 const int64_t gx = gxo(x), gy = gyo(y);
                 const double al = AW[ai(x, y)];
-                const double(&c)[3] = ring[y & 1];
                 double acc = XN[wi(x, y)];
-                if (inside(gx + s9::NBX[kW], gy)) acc = fma(al * c[0], XN[wi(x - 1, y)], acc);
-                if (inside(gx, gy + s9::NBY[kS])) acc = fma(al * c[1], XN[wi(x, y - 1)], acc);
-                if (inside(gx + s9::NBX[kSW], gy + s9::NBY[kSW])) acc = fma(al * c[2], XN[wi(x - 1, y - 1)], acc);
+                if (inside(gx + s9::NBX[kW], gy)) acc = fma(al * cw0, XN[wi(x - 1, y)], acc);
+                if (inside(gx, gy + s9::NBY[kS])) acc = fma(al * cs0, XN[wi(x, y - 1)], acc);
+                if (inside(gx + s9::NBX[kSW], gy + s9::NBY[kSW])) acc = fma(al * cd0, XN[wi(x - 1, y - 1)], acc);
                 XN[wi(x, y)] = acc;
             } else if (k == 2) {
                 // a pair across one coupled start face, in registers: members in ascending global
@@ -285,8 +295,11 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
             }
         }
-        if (x < T0 && y >= 0 && y < T1) fetch(y + 2, ring[y & 1]);   // two fronts ahead
-        asm volatile("bar.sync 1, %0;" ::"r"(s9::LT) : "memory");
+        if (t < s9::LT && x < T0 && y >= 0 && y < T1) {   // rotate: the next triple, fetch two fronts ahead
+            cw0 = cw1; cs0 = cs1; cd0 = cd1;
+            fetch(y + 2, cw1, cs1, cd1);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(s9::FT) : "memory");
         SW_JITTER_POINT();
     }
     if (fl) atomicOr(A.flag, 1);
