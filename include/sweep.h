@@ -201,7 +201,10 @@ sw_status sw_set_precond_steps(sw_grid *g, int m, double theta);
  * theta on P^-1 A from zero, P the decomposed SGS (SYMMETRIC pairing), i.e. theta times the m-step
  * operator of sw_set_precond_steps, before and after the coarse correction, which is added scaled by coarse_scale (the usual
  * over-correction of piecewise-constant interpolation; any value > 0 keeps the V-cycle symmetric
- * positive definite); on the coarsest level nu_coarse steps.  Single rank.  SW_EINVAL for levels
+ * positive definite); on the coarsest level nu_coarse steps.  With a communicator every level is
+ * decomposed over the same ranks (each level's tile rows must split evenly, else SW_EINVAL), the
+ * coarse faces of the neighbours' layers are exchanged once and the cycle exchanges ghost layers
+ * before every residual; without one, single rank.  SW_EINVAL for levels
  * outside [2, 16], nu outside [1, 64], nu_coarse outside [1, 1024], theta outside (0, 1],
  * coarse_scale outside (0, 4] or an odd count on a level to be coarsened.  `axes` (bit a = axis a)
  * selects the coarsened axes of every level, 0 = all: for anisotropic problems (config 5's
@@ -228,7 +231,8 @@ sw_status sw_mg_set_cycle(sw_grid *g, int gamma);
  * double-double partial, all-gathered on the device and summed in rank order, so all ranks take
  * identical steps; ghost layers are exchanged inside the iteration (r and the preconditioner's
  * intermediate layers, then z, from which each rank forms the neighbours' direction values
- * itself).  Iteration counts agree with the single-rank solve to +-1. */
+ * itself).  Iteration counts agree with the single-rank solve to +-1.  SW_PC_MG works over ranks
+ * too (sw_mg_setup with a communicator). */
 sw_status sw_pcg_solve(sw_grid *g, sw_precond precond, double omega, sw_pairing pairing, double rtol, int maxit,
                        int *iters_out, double *relres_out, sw_stream_t s);
 

@@ -1095,7 +1095,8 @@ static sw_status mg_build(sw_grid *g, int levels, int axes);
 extern "C" sw_status sw_mg_setup(sw_grid *g, int levels, int nu, double theta, int nu_coarse, double coarse_scale,
                                  int axes) {
     if (!g || !g->decomposed) return fail(SW_ESTATE, "grid not decomposed");
-    if (g->nranks > 1) return fail(SW_EINVAL, "multigrid is single-rank in this build");
+    if (g->nranks > 1 && !g->comm) return fail(SW_EINVAL, "multigrid over several ranks needs a communicator");
+    if (g->nine) return fail(SW_ESTATE, "nine-point grids support the SOR sweep only");
     if (levels < 2 || levels > 16 || nu < 1 || nu > 64 || nu_coarse < 1 || nu_coarse > 1024 ||
         !(theta > 0.0 && theta <= 1.0) || !(coarse_scale > 0.0 && coarse_scale <= 4.0))
         return fail(SW_EINVAL, "bad multigrid parameters");
@@ -1144,7 +1145,8 @@ static sw_status mg_build(sw_grid *g, int levels, int axes) {
         if ((st = sw_create_grid(g->dim, nc, SW_COEF_FACES, bc, g->dev, &c)) != SW_OK) return st;
         g->mg.push_back(c);
         c->fast2d = g->fast2d;
-        if ((st = sw_decompose(c, tc, 0, 1, nullptr)) != SW_OK) return st;
+        // every level is decomposed over the same ranks (slab offsets halve with the node count)
+        if ((st = sw_decompose(c, tc, g->rank, g->nranks, g->comm)) != SW_OK) return st;
         if ((st = ensure_work(c)) != SW_OK) return st;
         for (int a = 0; a < g->dim; ++a) {
             const double *ff = (fine == g) ? (src_faces ? src_faces[a] : nullptr) : fine->F[a];
@@ -1153,6 +1155,9 @@ static sw_status mg_build(sw_grid *g, int levels, int axes) {
             k_coarsen_faces<<<nb, 256>>>(fine->G, c->G, make_coarsen(axes, g->dim), a, ff, c->F[a]);
             CK(cudaGetLastError());
         }
+        CK(cudaDeviceSynchronize());
+        for (int a = 0; a < g->dim; ++a)        // the coarse faces of the neighbours' slab layers
+            if ((st = exch(c, c->F[a], 2, 0)) != SW_OK) return st;
         CK(cudaDeviceSynchronize());
         double **ptrs[] = {&c->MGR, &c->MGX, &c->MT1, &c->MT2, &c->MGW, &c->MGY};
         for (double **p : ptrs)
@@ -1194,6 +1199,8 @@ static sw_status mg_smooth(sw_grid *l, const double *r, double *x, int m, double
 }
 
 static sw_status mg_residual(sw_grid *l, const double *r, const double *x, double *out, cudaStream_t s) {
+    sw_status st0 = exch(l, const_cast<double *>(x), 1, s);     // (multi-rank: A x reads the neighbours' layer)
+    if (st0 != SW_OK) return st0;
     const Rows RW = make_rows(l->G);
     const int nr = (int)std::min<int64_t>(RW.items, red_blocks());
     const double *F0 = l->F[0], *F1 = l->F[1], *F2 = l->F[2];
@@ -1212,6 +1219,8 @@ static sw_status mg_residual(sw_grid *l, const double *r, const double *x, doubl
 
 // r_c = R (r - A x), one pass
 static sw_status mg_resid_restrict(sw_grid *l, sw_grid *c, int axes, const double *r, const double *x, cudaStream_t s) {
+    sw_status st0 = exch(l, const_cast<double *>(x), 1, s);
+    if (st0 != SW_OK) return st0;
     const int64_t nct = c->G.n[0] * c->G.n[1] * c->G.n[2];
     const int nb = (int)std::min<int64_t>((nct + 255) / 256, 8192);
     const double *F0 = l->F[0], *F1 = l->F[1], *F2 = l->F[2];
@@ -1523,7 +1532,7 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
 // the neighbour computes), so the fused direction update + SpMV needs no further exchange.
 static sw_status pcg_multi(sw_grid *g, sw_precond pc, double omega, sw_pairing pairing, double rtol, int maxit,
                            int *iters_out, double *relres_out, cudaStream_t cs) {
-    if (pc == SW_PC_MG) return fail(SW_EINVAL, "the multigrid preconditioner is single-rank");
+    if (pc == SW_PC_MG && g->mg.empty()) return fail(SW_ESTATE, "sw_mg_setup must precede SW_PC_MG");
     sw_status st = ensure_work(g);
     if (st != SW_OK) return st;
     CK(cudaSetDevice(g->dev));
@@ -1558,6 +1567,7 @@ static sw_status pcg_multi(sw_grid *g, sw_precond pc, double omega, sw_pairing p
     };
     auto apply_pc = [&]() -> sw_status {
         if (pc == SW_PC_NONE) return SW_OK;
+        if (pc == SW_PC_MG) return sw_mg_apply(g, g->R, g->Z, cs);
         return tri_apply(g, pc == SW_PC_ILU0, omega, g->R, g->Z, pairing, cs);
     };
     double *pcur = g->Pv, *pprev = g->Pv2;

@@ -212,6 +212,59 @@ def test_multirank_pcg_matches_oracle(n, tile, nranks, var, pc, pairing):
     assert O.relres(pb, x, b) < 2e-8
 
 
+MG_CASES = [((128, 128), (16, 16), 2, True, 3, 0), ((64, 128), (16, 16), 4, False, 3, 0),
+            ((32, 32, 32), (16, 8, 4), 2, True, 3, 0), ((64, 32, 16), (32, 8, 4), 2, True, 3, 3)]
+
+
+@pytest.mark.parametrize("n,tile,nranks,var,levels,axes", MG_CASES)
+def test_multirank_mg_vcycle_matches_oracle(n, tile, nranks, var, levels, axes):
+    """The multigrid V-cycle over slabs (every level decomposed over the same ranks, ghost exchanges
+    inside the library) against the oracle-side composition (tests/mg_compose.py), 1e-12."""
+    from tests.mg_compose import build_levels, vcycle
+    faces = rand_faces(n, 17) if var else None
+    mask = axes or (1 << len(n)) - 1
+    pbs = build_levels(n, tile, faces, 0.0, levels, mask)
+    r0 = gen.uniform_field(8, gen.STREAM_TEST, pbs[0].shape)
+
+    def rank_fn(r, comm):
+        s = torch.cuda.Stream().cuda_stream
+        g = make_slab(n, tile, r, nranks, faces, 0.0, comm).mg_setup(levels, 1, 0.5, 6, 1.3, axes)
+        g.set_vector(B.R, local_part(g, r0), stream=s)
+        g.mg_apply(g.ptr(B.R), g.ptr(B.Z), stream=s)
+        g.check(stream=s)
+        return g.get_vector(B.Z, stream=s)
+    got = np.concatenate(run_threads(nranks, rank_fn), axis=0)
+    want = vcycle(pbs, 0, r0, 1, 0.5, 6, 1.3, mask)
+    assert rel_maxdiff(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("n,tile,nranks,levels", [((256, 256), (32, 32), 2, 4), ((32, 32, 32), (16, 8, 4), 2, 3)])
+def test_multirank_mg_pcg_matches_single_grid(n, tile, nranks, levels):
+    """MG-preconditioned CG over slabs: iterations within 1 of the single-grid solve, solution's oracle
+    residual < 2e-8."""
+    ring = tuple(v + 2 for v in reversed(n))
+    faces = O.faces_from_k(n, gen.lognormal_k(0, ring, 1.0))
+    pb = O.tiled(n, tile, faces=faces)
+    b = gen.uniform_field(0, gen.STREAM_RHS, pb.shape) / float((n[0] + 1) ** 2)
+    one = B.Grid(len(n), n, B.COEF_FACES).decompose(tile)
+    one.set_faces_global(faces)
+    one.mg_setup(levels, 1, 0.5, 16)
+    one.set_vector(B.B, b)
+    it1, _, ok1 = one.pcg_solve(B.PC_MG, 1.0, B.PAIR_SYMMETRIC, 1e-8, 2000)
+
+    def rank_fn(r, comm):
+        s = torch.cuda.Stream().cuda_stream
+        g = make_slab(n, tile, r, nranks, faces, 0.0, comm).mg_setup(levels, 1, 0.5, 16)
+        g.set_vector(B.B, local_part(g, b), stream=s)
+        it, rel, ok = g.pcg_solve(B.PC_MG, 1.0, B.PAIR_SYMMETRIC, 1e-8, 2000, stream=s)
+        return it, ok, g.get_vector(B.X, stream=s)
+    res = run_threads(nranks, rank_fn)
+    its = {r[0] for r in res}
+    assert ok1 and len(its) == 1 and all(r[1] for r in res)
+    assert abs(its.pop() - it1) <= 1
+    assert O.relres(pb, np.concatenate([r[2] for r in res], axis=0), b) < 2e-8
+
+
 def test_multirank_validation():
     n, tile = (128, 128), (64, 64)
     g = make_slab(n, tile, 0, 2)                       # no communicator: staged use only
