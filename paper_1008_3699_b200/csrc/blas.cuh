@@ -256,11 +256,15 @@ __global__ void __launch_bounds__(RED_THREADS) k_pspmv_dot_r(Rows R, double beta
                                                              const double *__restrict__ F1,
                                                              const double *__restrict__ F2,
                                                              const double *__restrict__ z,
-                                                             const double *__restrict__ pold,
-                                                             double *__restrict__ pnew, double *__restrict__ q,
-                                                             DD *partial) {
+                                                             const double *pold_a, double *pnew_a,
+                                                             double *__restrict__ q, DD *partial,
+                                                             const int *par_dev = nullptr) {
     __shared__ DD sh[RED_THREADS / 32];
     const double be = *beta_dev;
+    // par_dev (a device-resident PCG loop): odd parity swaps the two direction buffers
+    const bool sw_ = par_dev && *par_dev;
+    const double *const pold = sw_ ? pnew_a : pold_a;
+    double *const pnew = sw_ ? const_cast<double *>(pold_a) : pnew_a;
     auto P = [&](int64_t j) { return fma(be, pold[j], z[j]); };
     DD acc = {0.0, 0.0};
     for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
@@ -316,12 +320,15 @@ template <bool FACES>
 __global__ void __launch_bounds__(256) k_pspmv3_zm(Rows R, double beta_a, const double *beta_dev,
                                                    const double *__restrict__ F0, const double *__restrict__ F1,
                                                    const double *__restrict__ F2, const double *__restrict__ z,
-                                                   const double *__restrict__ pold, double *__restrict__ pnew,
-                                                   double *__restrict__ q, DD *partial) {
+                                                   const double *pold_a, double *pnew_a,
+                                                   double *__restrict__ q, DD *partial, const int *par_dev = nullptr) {
     constexpr int TX = 32, TY = 8;
     __shared__ double tile[2][TY + 2][TX + 2];
     __shared__ DD sh[256 / 32];
     const double be = *beta_dev;
+    const bool sw_ = par_dev && *par_dev;
+    const double *const pold = sw_ ? pnew_a : pold_a;
+    double *const pnew = sw_ ? const_cast<double *>(pold_a) : pnew_a;
     auto P = [&](int64_t j) { return fma(be, pold[j], z[j]); };
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     constexpr int ZC = SW_ZC;                 // planes per work item (more items in flight)
@@ -436,10 +443,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_dot_diff_r(Rows R, const double
 
 // x = fma(alpha, p, x) ; r = fma(-alpha, q, r) ; partial = sum r.r
 __global__ void __launch_bounds__(RED_THREADS) k_axpy2_dot_r(Rows R, const double *alpha_dev, double *__restrict__ x,
-                                                             double *__restrict__ r, const double *__restrict__ p,
-                                                             const double *__restrict__ q, DD *partial) {
+                                                             double *__restrict__ r, const double *p_a,
+                                                             const double *__restrict__ q, DD *partial,
+                                                             const double *p_b = nullptr, const int *par_dev = nullptr) {
     __shared__ DD sh[RED_THREADS / 32];
     const double al = *alpha_dev;
+    const double *const p = (par_dev && *par_dev) ? p_b : p_a;   // (device-resident PCG: the current direction)
     DD acc = {0.0, 0.0};
     for (int64_t it = blockIdx.x; it < R.items; it += gridDim.x) {
         const int64_t row = it / R.segs, seg = it % R.segs;
@@ -538,7 +547,23 @@ __global__ void __launch_bounds__(RED_THREADS) k_axpby_r(Rows R, double a, const
 // PCG scalars kept on the device
 struct CgScalars {
     double rz, pq, alpha, beta, rr, bb, rz_new, zd;   // zd = z.(r_new - r_old) (flexible CG)
+    int it, par, stop, pad;                           // device-resident loop: iteration, buffer parity, stop code
 };
+
+// End of one iteration of the device-resident PCG loop (a conditional WHILE node): count it, flip the
+// direction-buffer parity, and keep looping while ||r|| / ||b|| >= rtol, r.r is a number and it < maxit
+// (stop: 1 converged, 2 NaN, 3 maxit) -- the host loop's decisions, taken on the device.
+__global__ void k_pcg_step(CgScalars *c, cudaGraphConditionalHandle h, double rtol, double bnorm, int maxit) {
+    c->it += 1;
+    c->par ^= 1;
+    const double rel = sqrt(c->rr) / bnorm;
+    int stop = 0;
+    if (rel < rtol) stop = 1;
+    else if (!(c->rr == c->rr)) stop = 2;
+    else if (c->it >= maxit) stop = 3;
+    c->stop = stop;
+    cudaGraphSetConditional(h, stop == 0 ? 1u : 0u);
+}
 
 // sum `nparts` partials (stride `stride`, offset `off`) in fixed order into *dst = hi + lo
 __global__ void k_finish_sum(const DD *partial, int nparts, int stride, int off, double *dst) {

@@ -1375,8 +1375,16 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
                       (g->pcg_flexible < 0 && pairing == SW_PAIR_PAPER && (pc == SW_PC_ILU0 || pc == SW_PC_SSOR));
     if (flex && (st = alloc_arr(g, &g->Rold)) != SW_OK) return st;
     double *pcur = g->Pv, *pprev = g->Pv2;     // current direction, and the buffer of the other one
+    // dyn: the iteration is being captured into the device-resident loop, where the direction buffers
+    // alternate by the parity the loop keeps on the device (cg->par: 0 = old Pv, new Pv2)
+    bool dyn = false;
+    const int *par_dev = &g->cg->par;
     // q = A p (first iteration) or, fused, p' = z + beta p, q = A p'
     auto spmv = [&](bool fused) {
+        if (dyn) {
+            pprev = g->Pv;
+            pcur = g->Pv2;
+        }
         const double *F0 = g->F[0], *F1 = g->F[1], *F2 = g->F[2];
         if (!fused) {
             if (g->dim == 1) fc ? k_spmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial)
@@ -1387,12 +1395,12 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
                     : k_spmv_dot_r<3, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, F0, F1, F2, pcur, g->Q, g->partial);
         } else {
             const double *bd = &g->cg->beta;
-            if (g->dim == 1) fc ? k_pspmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
-                                : k_pspmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
-            else if (g->dim == 2) fc ? k_pspmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
-                                     : k_pspmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
-            else fc ? k_pspmv3_zm<true><<<nr, 256, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial)
-                    : k_pspmv3_zm<false><<<nr, 256, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial);
+            if (g->dim == 1) fc ? k_pspmv_dot_r<1, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial, dyn ? par_dev : nullptr)
+                                : k_pspmv_dot_r<1, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial, dyn ? par_dev : nullptr);
+            else if (g->dim == 2) fc ? k_pspmv_dot_r<2, true><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial, dyn ? par_dev : nullptr)
+                                     : k_pspmv_dot_r<2, false><<<nr, RED_THREADS, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial, dyn ? par_dev : nullptr);
+            else fc ? k_pspmv3_zm<true><<<nr, 256, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial, dyn ? par_dev : nullptr)
+                    : k_pspmv3_zm<false><<<nr, 256, 0, ws>>>(RW, G.beta, bd, F0, F1, F2, z, pprev, pcur, g->Q, g->partial, dyn ? par_dev : nullptr);
         }
         g->launches++;
     };
@@ -1423,10 +1431,11 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
         k_cg_alpha<<<1, 1, 0, ws>>>(g->cg);
         g->launches++;
         if (flex) CK(cudaMemcpyAsync(g->Rold, g->R, sizeof(double) * (size_t)g->nelem, cudaMemcpyDeviceToDevice, ws));
-        k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, pcur, g->Q, g->partial);
+        if (dyn) k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, g->Pv2, g->Q, g->partial, g->Pv, par_dev);
+        else k_axpy2_dot_r<<<nr, RED_THREADS, 0, ws>>>(RW, &g->cg->alpha, x, g->R, pcur, g->Q, g->partial);
         g->launches++;
         if ((t = finish(g, nr, 1, 0, &g->cg->rr, ws)) != SW_OK) return t;
-        CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, ws));
+        if (!dyn) CK(cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, ws));
         return SW_OK;
     };
     // z = P^-1 r, r.z, beta (the direction update p = z + beta p is fused into the next SpMV)
@@ -1468,8 +1477,86 @@ extern "C" sw_status sw_pcg_solve(sw_grid *g, sw_precond pc, double omega, sw_pa
     int64_t graph_launches = 0;
     bool graph_ok = !no_graph;
     auto cleanup = [&]() { graphs.reset(); };
+    // Iterations 2..: ONE graph whose conditional WHILE node replays the iteration on the device until
+    // the stop test (k_pcg_step) ends it -- alpha, beta and the decision never leave the device, the
+    // host synchronises once.  SW_PCG_HOSTLOOP=1 (or a runtime without conditional
+    // nodes) keeps the per-iteration graph launch and readback below.
+    static const bool host_loop = getenv("SW_PCG_HOSTLOOP") != nullptr;
+    auto device_loop = [&](int *iters, double *rel, int *stop) -> bool {
+        if (no_graph || host_loop) return false;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t gexec = nullptr;
+        cudaGraphConditionalHandle hnd;
+        if (cudaGraphCreate(&graph, 0) != cudaSuccess) { cudaGetLastError(); return false; }
+        bool ok = cudaGraphConditionalHandleCreate(&hnd, graph, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        cudaGraphNodeParams cp = {};
+        cudaGraphNode_t node;
+        if (ok) {
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = hnd;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            ok = cudaGraphAddNode(&node, graph, nullptr, 0, &cp) == cudaSuccess;
+        }
+        if (ok && !g->cap_stream) ok = cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
+        const int64_t l0 = g->launches;
+        double *const keep_cur = pcur, *const keep_prev = pprev;   // (the capture rebinds them)
+        if (ok) {
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            ok = cudaStreamBeginCaptureToGraph(g->cap_stream, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                ws = g->cap_stream;
+                dyn = true;
+                sw_status t1 = tail();
+                sw_status t2 = t1 == SW_OK ? head(true) : t1;
+                k_pcg_step<<<1, 1, 0, ws>>>(g->cg, hnd, rtol, bnorm, maxit);
+                g->launches++;
+                dyn = false;
+                ws = cs;
+                cudaGraph_t b2 = body;
+                const cudaError_t ce = cudaStreamEndCapture(g->cap_stream, &b2);
+                ok = t1 == SW_OK && t2 == SW_OK && ce == cudaSuccess;
+            }
+        }
+        pcur = keep_cur;
+        pprev = keep_prev;
+        const int64_t per_iter = g->launches - l0;
+        g->launches = l0;
+        if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+        // the loop's state: one iteration done, the next reads its direction from Pv
+        int init[3] = {1, 0, 0};
+        if (ok) ok = cudaMemcpyAsync(&g->cg->it, init, sizeof(init), cudaMemcpyHostToDevice, cs) == cudaSuccess;
+        if (ok) ok = cudaGraphLaunch(gexec, cs) == cudaSuccess;
+        if (ok) ok = cudaMemcpyAsync(&h, g->cg, sizeof(h), cudaMemcpyDeviceToHost, cs) == cudaSuccess;
+        if (ok) ok = cudaStreamSynchronize(cs) == cudaSuccess;
+        if (gexec) cudaGraphExecDestroy(gexec);
+        cudaGraphDestroy(graph);
+        if (!ok) {
+            cudaGetLastError();
+            return false;
+        }
+        g->launches += per_iter * (h.it - 1);
+        *iters = h.it;
+        *rel = sqrt(h.rr) / bnorm;
+        *stop = h.stop;
+        return true;
+    };
     for (int it = 1; it <= maxit; ++it) {
         const int par = it & 1;
+        if (it == 2) {
+            int di = 0, dstop = 0;
+            double drel = 1.0;
+            if (device_loop(&di, &drel, &dstop)) {
+                *iters_out = di;
+                *relres_out = drel;
+                if (dstop == 1) return sw_check_status(g, s);
+                if (dstop == 2) return fail(SW_ENOCONV, "PCG produced NaN");
+                st = sw_check_status(g, s);
+                if (st != SW_OK) return st;
+                return fail(SW_ENOCONV, "PCG reached maxit");
+            }
+        }
         if (it == 1) {
             ws = cs;
             if ((st = head(false)) != SW_OK) return st;
