@@ -227,7 +227,8 @@ sw_status sw_mg_set_cycle(sw_grid *g, int gamma);
  * first.  SW_ENOCONV: iters/relres still valid.  beta = (r+.z+)/(r.z), or the flexible
  * (Polak-Ribiere) beta = z+.(r+ - r)/(r.z) that the nonsymmetric PAPER pairing needs
  * (SURVEY §8(c) C-PCG; sw_set_pcg_flexible).  alpha, beta and the stop test stay on the
- * device.  With a communicator (SW_PC_NONE / SSOR / ILU0): every reduction is each rank's
+ * device: one rank runs iterations 2.. as one CUDA graph with a conditional WHILE node and
+ * synchronises once per solve.  With a communicator (SW_PC_NONE / SSOR / ILU0): every reduction is each rank's
  * double-double partial, all-gathered on the device and summed in rank order, so all ranks take
  * identical steps; ghost layers are exchanged inside the iteration (r and the preconditioner's
  * intermediate layers, then z, from which each rank forms the neighbours' direction values
