@@ -19,6 +19,7 @@
 #include "sweep2v.cuh"
 #include "tri2t.cuh"
 #include "sweep3.cuh"
+#include "sweep3s.cuh"
 #include "tri3t.cuh"
 #include "mg.cuh"
 #include "comm.cuh"
@@ -123,6 +124,66 @@ static bool get_map(sw_grid *g, const double *ptr, int box, CUtensorMap *out, in
     g->mapcache.push_back(e);
     *out = e.map;
     return true;
+}
+
+// 3D TMA descriptor (box (4, b1, b2)) of a padded array whose slab extent is n2pad planes, cached
+// by pointer like get_map; copied out by value.
+static bool get_map3(sw_grid *g, const double *ptr, int b1, int b2, int64_t n2pad, CUtensorMap *out) {
+    const int key = 100000 + b1 * 1000 + b2 * 10;
+    for (auto &e : g->mapcache)
+        if (e.ptr == ptr && e.box == key && e.rows == n2pad) {
+            *out = e.map;
+            return true;
+        }
+    sw_grid::MapEntry e;
+    e.ptr = ptr;
+    e.box = key;
+    e.rows = n2pad;
+    if (!encode_3d(&e.map, ptr, g->pad[0], g->pad[1], n2pad, 4, b1, b2)) return false;
+    if (g->mapcache.size() >= 48) g->mapcache.pop_front();
+    g->mapcache.push_back(e);
+    *out = e.map;
+    return true;
+}
+
+// The streaming 3D engine (sweep3s.cuh) for boxes at least 64 long in x (k_sweep3 stages whole
+// boxes in shared memory and cannot take them; for 32 x 8 x 4 it is the faster of the two:
+// 23 against 20 GLUP/s at 512^3, profiles/r02_sweep3_experiments.txt); *ran = false leaves the
+// call to k_sweep3 / the generic kernel.  SW_SWEEP3=new / old forces either (A/B measurements).
+static sw_status run_sweep3s(sw_grid *g, const Geo &G, int base, const double *w8, const double *xin,
+                             const double *aux, const double *F0, const double *F1, const double *F2, double *out,
+                             int tri, int invd_mode, int rscale, double coef, int couple, cudaStream_t s, bool *ran) {
+    *ran = false;
+    static const int force = [] {
+        const char *e = getenv("SW_SWEEP3");
+        return !e ? 0 : (std::string(e) == "old" ? -1 : (std::string(e) == "new" ? 1 : 0));
+    }();
+    if (force < 0 || !g->fast2d || (force == 0 && G.T[0] < 64)) return SW_OK;
+    const bool faces = !G.poisson;
+    const bool has_aux = !tri || invd_mode;
+    Sweep3sArgs A{};
+    size_t smem = 0;
+    if (!sweep3s_layout(G, faces, has_aux, tri, A, smem)) return SW_OK;
+    A.G = G;
+    A.base = base;
+    for (int i = 0; i < 8; ++i) A.omega[i] = w8[i];
+    A.coef = coef;
+    A.flag = g->flag;
+    A.tri = tri;
+    A.invd_mode = invd_mode;
+    A.rscale = rscale;
+    A.couple = couple;
+    const int64_t n2pad = G.n[2] + 4;
+    CUtensorMap M[6];
+    const double *arr[5] = {xin, has_aux ? aux : xin, faces ? F0 : xin, faces ? F1 : xin, faces ? F2 : xin};
+    for (int a = 0; a < 5; ++a)
+        if (!get_map3(g, arr[a], A.R[a], A.Q[a], n2pad, &M[a])) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+    if (!get_map3(g, out, G.T[1], G.T[2], n2pad, &M[5])) return fail(SW_ECUDA, "cuTensorMapEncodeTiled (3D) failed");
+    cudaError_t e = launch_sweep3s(A, M, smem, faces, s);
+    g->launches++;
+    if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep3s launch: ") + cudaGetErrorString(e));
+    *ran = true;
+    return SW_OK;
 }
 
 extern "C" const char *sw_last_error(void) { return g_err.c_str(); }
@@ -657,6 +718,12 @@ static sw_status sweep_rows(sw_grid *g, int r0, int cnt, int base, const double 
         if (e != cudaSuccess) return fail(SW_ECUDA, std::string("sweep2 launch: ") + cudaGetErrorString(e));
         return SW_OK;
     }
+    if (g->dim == 3 && g->fast2d) {
+        bool ran = false;
+        sw_status st3 = run_sweep3s(g, G, base, w8, xo, bb, G.poisson ? nullptr : F0, G.poisson ? nullptr : F1,
+                                    G.poisson ? nullptr : F2, xn, 0, 0, 0, 1.0, 1, cs, &ran);
+        if (st3 != SW_OK || ran) return st3;
+    }
     if (g->dim == 3 && g->fast2d && sweep3_supported(G)) {
         Sweep3Args A3{};
         A3.G = G;
@@ -969,6 +1036,17 @@ static sw_status tri_stage(sw_grid *g, bool ilu, double omega, const double *r, 
     P.alpha_mode = ilu ? A_INVD : A_OMEGA_AP;
     P.invD = g->invD;
     for (int i = 0; i < 8; ++i) P.omega[i] = omega;
+    if (stage <= 1 && g->dim == 3 && g->fast2d) {
+        const double *src = stage == 0 ? r : g->Y;
+        const Geo &G3 = g->G;
+        bool ran = false;
+        sw_status st3 = stage == 0
+            ? run_sweep3s(g, G3, base, P.omega, src, invd, G3.poisson ? nullptr : g->F[0], G3.poisson ? nullptr : g->F[1],
+                          G3.poisson ? nullptr : g->F[2], g->Y, 1, ilu, 1, 1.0, 1, s, &ran)
+            : run_sweep3s(g, G3, rev, P.omega, src, invd, G3.poisson ? nullptr : g->F[0], G3.poisson ? nullptr : g->F[1],
+                          G3.poisson ? nullptr : g->F[2], z, 1, ilu, 0, coef, pairing == SW_PAIR_PAPER, s, &ran);
+        if (st3 != SW_OK || ran) return st3;
+    }
     if (stage <= 1 && g->dim == 3 && g->fast2d && sweep3_supported(g->G)) {
         // 3D engine for the two forward-type solves
         const double *src = stage == 0 ? r : g->Y;

@@ -3,7 +3,8 @@ the race-exposure build libsweep_jitter.so (-DSW_JITTER, csrc/common.cuh), in wh
 sleeps a pseudo-random 0-1023 ns after every barrier, mbarrier wait and flag acquire and at kernel
 start, under three seeds.  Warps, and the lanes of a warp, then reach the shared-memory hand-offs
 of the wavefronts (k_sweep2p / k_sweep2v in-place predicated updates, k_sweep3's release/acquire
-x-edge hand-off and named barrier, the k_tri2t / k_tri3t lane groups, k_generic's levels) in
+x-edge hand-off and named barrier, k_sweep3s's producer/consumer batches behind a named barrier
+and its TMA chunk ring, the k_tri2t / k_tri3t lane groups, k_generic's levels) in
 orders the normal build never produces; a missing barrier shows up as a result that is no longer
 bitwise equal to the oracle.  (SURVEY.md §5 race detection.)"""
 import os
@@ -16,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITES = ["tests/test_gpu_parity.py", "tests/test_gpu_degenerate.py", "tests/test_gpu_msteps.py", "tests/test_gpu_eikonal.py",
-          "tests/test_gpu_ninepoint.py"]
+          "tests/test_gpu_ninepoint.py", "tests/test_gpu_sweep3s.py"]
 
 
 @pytest.mark.parametrize("seed", [1, 7, 12345])
