@@ -121,16 +121,17 @@ constexpr int NR = 3;          // raw chunk slots
 }
 __host__ __device__ inline int lay_round(int n, int a) { return (n + a - 1) / a * a; }
 // entries of the ring of x-line (j, k) at skew j + k: the producer writes batch m (columns up to
-// 4m) once the consumer has passed barrier B_{m-1} at the start of step 4m - 8, whose end still
-// prefetches column 4m - 7 - skew for step 4m - 7
-__host__ __device__ inline int ring_depth(int j, int k) { return (j > 0 ? j : 0) + (k > 0 ? k : 0) + 9; }
+// 4m) once the consumer has reached barrier B_{m-1} before step 4m - 12, so the consumer may still
+// read column 4m - 12 - skew (and prefetch the next one) while it does
+constexpr int RING_EXTRA = 13;
+__host__ __device__ inline int ring_depth(int j, int k) { return (j > 0 ? j : 0) + (k > 0 ? k : 0) + RING_EXTRA; }
 // first entry of line (j, k) (lines ordered by k, then j, both from -1)
 __host__ __device__ inline int ring_first(int T1, int j, int k) {
     const int kk = k + 1, jj = j + 1;                        // rows / lines before
-    const int rowsum0 = (T1 * (T1 - 1)) / 2 + 9 * (T1 + 1);  // a row with max(k, 0) = 0
+    const int rowsum0 = (T1 * (T1 - 1)) / 2 + RING_EXTRA * (T1 + 1);  // a row with max(k, 0) = 0
     const int km = kk >= 2 ? ((kk - 2) * (kk - 1)) / 2 : 0;  // sum of max(k', 0) over k' < k
     const int before_rows = kk * rowsum0 + (T1 + 1) * km;
-    const int K5 = (k > 0 ? k : 0) + 9;
+    const int K5 = (k > 0 ? k : 0) + RING_EXTRA;
     const int jm = jj >= 2 ? ((jj - 2) * (jj - 1)) / 2 : 0;  // sum of max(j', 0) over j' < j
     return before_rows + jj * K5 + jm;
 }
@@ -160,10 +161,12 @@ __host__ __device__ inline Lay3 lay3(int T1, int T2, bool faces, bool has_aux) {
     L.nres = (T1 + T2 + 2) / 4 + 1 <= 4 ? 4 : 8;
     L.ressz = lay_round(4 * T1 * T2, 16);
     L.res = L.ring + lay_round(L.rings, 16);
-    L.xf = L.res + L.nres * L.ressz;
-    L.mx = L.xf + 3 * 96;                                    // x-edge factors of three batches
+    // the start column's compact arrays (MX) share the result ring: they are read right after B_0,
+    // the first result is written after B_2
     const int WSm = 2 * (T1 + 1) * (T2 + 1);
-    L.mbar = 8 * lay_round(L.mx + 4 * WSm + 80, 2);
+    L.mx = L.res;
+    L.xf = lay_round(L.res + (L.nres * L.ressz > 4 * WSm + 80 ? L.nres * L.ressz : 4 * WSm + 80), 16);
+    L.mbar = 8 * lay_round(L.xf + 16 * 4, 2);                // after the x-edge results of 16 columns
     L.smem = L.mbar + 8 * NR;
     return L;
 }
@@ -204,7 +207,7 @@ __device__ __forceinline__ void sts2(double *p, double a, double b) {
 }
 
 template <bool FACES, bool TRI, int SHAPE>
-__global__ void __launch_bounds__(64, 4)
+__global__ void __launch_bounds__(96, 4)
     k_sweep3s(const __grid_constant__ Sweep3sArgs A, const __grid_constant__ CUtensorMap mXO,
               const __grid_constant__ CUtensorMap mBB, const __grid_constant__ CUtensorMap mF0,
               const __grid_constant__ CUtensorMap mF1, const __grid_constant__ CUtensorMap mF2,
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(64, 4)
     double *const ring = sm;
     double *const rng = sm + Y.ring;                          // the x-lines' compact rings
     double *const res = sm + Y.res;
-    double *const XF = sm + Y.xf;
+    double *const XE = sm + Y.xf;                             // x-edge results: (u, across z, across y) per column
     double *const MX = sm + Y.mx;
     uint64_t *const bar = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(sm) + Y.mbar);
 
@@ -240,6 +243,10 @@ __global__ void __launch_bounds__(64, 4)
     const int sx = sb & 1, sy = (sb >> 1) & 1, sz = (sb >> 2) & 1;
     const int X0 = tx * T0, Y0 = ty * T1, Z0 = tz * T2;      // padded coordinates of (box min - 2)
     const int NCH = T0 / 4 + 1;                              // raw chunks = production batches
+    // barriers B_1 .. B_MLAST after B_0: the producer forms batch m before B_m, the x-edge warp
+    // solves the sets of batch m between B_m and B_{m+1}, the wavefront runs steps [4m - 8, 4m - 4)
+    // between B_m and B_{m+1}
+    const int MLAST = (T0 + T1 + T2 - 3) / 4 + 2;
     const int RSm = 2, PSm = 2 * (T1 + 1), WSm = PSm * (T2 + 1);
     auto wofm = [&](int l0, int l1, int l2) { return (l0 + 1) + RSm * (l1 + 1) + PSm * (l2 + 1); };
     const int nl = T1 * T2;
@@ -509,54 +516,11 @@ __global__ void __launch_bounds__(64, 4)
                 }
             }
         };
-        // x-edge sets of batch m (columns cs + t, t < 4): members from the rings, factored in rank
-        // order (as factor4<6>); XF[m % 3][t] = l 6, U 6, inv 4, r0 4, cx 4 (the consumer reads
-        // batch m until step 4m, after it let the producer start batch m + 2)
-        const int mm = (sy ? 0 : 1) | (sz ? 0 : 2);
-        auto xedge_factor = [&](int m) {
-            const int c = 4 * m - 3 + lane;
-            if (lane < 4 && c >= 1 && c < T0) {
-                double M[4][4];
-                double *o = XF + 96 * (m % 3) + 24 * lane;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int S = r ^ mm, j = -(S & 1), k = -(S >> 1);
-                    const int D = ring_depth(j, k);
-                    const int pos = c - D * (int)(((float)c + 0.5f) * __frcp_rn((float)D));
-                    const double *e = rng + 4 * (ring_first(T1, j, k) + pos);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
-                    M[r][r ^ 1] = -e[2];                    // toward the partner across y
-                    M[r][r ^ 2] = -e[3];                    // across z
-                    o[16 + r] = e[0];
-                    o[20 + r] = e[1];
-                }
-                int li = 0;
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const double piv = M[p][p];
-                    fl |= !(fabs(piv) >= 1e-14);
-                    o[12 + p] = div_rn(1.0, piv);
-#pragma unroll
-                    for (int q = p + 1; q < 4; ++q) {
-                        const double l = M[q][p] * o[12 + p];
-                        o[li++] = l;
-#pragma unroll
-                        for (int jj = p + 1; jj < 4; ++jj) M[q][jj] = fma(-l, M[p][jj], M[q][jj]);
-                    }
-                }
-                int ui = 6;
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-#pragma unroll
-                    for (int jj = p + 1; jj < 4; ++jj) o[ui++] = M[p][jj];
-            }
-        };
         S3T(t_xs);
         S3ADD(3, t_xs - t_sets, 32);
         produce0();
         __syncwarp();
-        named_bar(1, 64);                                    // B_0: start column and batch 0
+        named_bar(1, 96);                                    // B_0: start column and batch 0
         S3T(t_b0);
         S3ADD(4, t_b0 - t_xs, 32);
 #ifdef SW_TRACE
@@ -568,7 +532,6 @@ __global__ void __launch_bounds__(64, 4)
             S3ACC(wch, t_w);
             produce(m);
             __syncwarp();
-            if ((cb & 6) == 6) xedge_factor(m);
             if (lane == 0 && m + 2 < NCH) {                  // chunk m - 1 is dead: its slot takes m + 2
                 fence_proxy_async_smem();
                 issue(m + 2);
@@ -576,14 +539,91 @@ __global__ void __launch_bounds__(64, 4)
             }
             __syncwarp();
             S3T(t_bb);
-            named_bar(1, 64);                                // B_m
+            named_bar(1, 96);                                // B_m
             S3ACC(wbar, t_bb);
         }
+        for (int m = NCH; m <= MLAST; ++m) named_bar(1, 96);
 #ifdef SW_TRACE
         S3ADD(6, wch, 32);
         S3ADD(7, wbar, 32);
         S3ADD(8, sw_clock() - t_start, 32);
 #endif
+    } else if (warp == 2) {
+        // ============================================================ x-edge chain (warp X)
+        // The sets of the y- and z-start faces' common edge along x (members: own line (0, 0),
+        // across y (-1, 0), across z (0, -1), both (-1, -1)), one per column c >= 1, each reading
+        // the previous column's solution: a serial chain that needs nothing the wavefront computes,
+        // so lane 0 runs it one batch ahead of the wavefront.  Members in rank order S = r ^ mm
+        // (bit 0 across y, bit 1 across z), factored and substituted exactly as ge_solve_k<4> (the
+        // oracle's elimination order, DESIGN R-8).  XE[c % 16] = (u(c,0,0), u(c,0,-1), u(c,-1,0)).
+        const bool xe_box = (cb & 6) == 6;
+        const int mm = (sy ? 0 : 1) | (sz ? 0 : 2);
+        named_bar(1, 96);                                    // B_0
+        double er[4] = {0.0, 0.0, 0.0, 0.0};                 // previous set, rank order
+        if (xe_box) {
+            const double u0 = MX[wofm(0, 0, 0)], py = MX[wofm(0, -1, 0)], pz = MX[wofm(0, 0, -1)];
+            const double pyz = MX[wofm(0, -1, -1)];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int S = r ^ mm;
+                er[r] = S == 0 ? u0 : (S == 1 ? py : (S == 2 ? pz : pyz));
+            }
+        }
+        for (int m = 1; m <= MLAST; ++m) {
+            const int bt = m - 1;                            // the batch of this interval
+            if (xe_box && lane == 0 && bt >= 1 && bt < NCH) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int c = 4 * bt - 3 + t;
+                    if (c >= 1 && c < T0) {
+                        double M[4][4], r0v[4], cxv[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int S = r ^ mm, jj = -(S & 1), kk = -(S >> 1);
+                            const double *e = rng + 4 * (ring_first(T1, jj, kk) + c % ring_depth(jj, kk));
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
+                            M[r][r ^ 1] = -e[2];                 // toward the partner across y
+                            M[r][r ^ 2] = -e[3];                 // across z
+                            r0v[r] = e[0];
+                            cxv[r] = e[1];
+                        }
+                        double rhs[4], uu[4], inv[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) rhs[r] = fma(cxv[r], er[r], r0v[r]);
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) {
+                            const double piv = M[p][p];
+                            fl |= !(fabs(piv) >= 1e-14);
+                            inv[p] = div_rn(1.0, piv);
+#pragma unroll
+                            for (int q = p + 1; q < 4; ++q) {
+                                const double l = M[q][p] * inv[p];
+#pragma unroll
+                                for (int jj = p + 1; jj < 4; ++jj) M[q][jj] = fma(-l, M[p][jj], M[q][jj]);
+                                rhs[q] = fma(-l, rhs[p], rhs[q]);
+                            }
+                        }
+#pragma unroll
+                        for (int p = 3; p >= 0; --p) {
+                            double sacc = rhs[p];
+#pragma unroll
+                            for (int q = p + 1; q < 4; ++q) sacc = fma(-M[p][q], uu[q], sacc);
+                            uu[p] = sacc * inv[p];
+                        }
+                        auto pick = [&](int r) { return r == 0 ? uu[0] : (r == 1 ? uu[1] : (r == 2 ? uu[2] : uu[3])); };
+                        double *o = XE + 4 * (c & 15);
+                        o[0] = pick(mm);
+                        o[1] = pick(2 ^ mm);
+                        o[2] = pick(1 ^ mm);
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) er[r] = uu[r];
+                    }
+                }
+            }
+            __syncwarp();
+            named_bar(1, 96);                                // B_m
+        }
     } else {
         // ============================================================ consumer
         const bool onl = lane < nl;
@@ -597,12 +637,11 @@ __global__ void __launch_bounds__(64, 4)
         const int pax = (m1 == 2) ? 1 : (m1 == 4 ? 2 : -1); // pair axis at c >= 1
         const int pj = pax == 1 ? -1 : j, pk = pax == 2 ? -1 : k;
         const int qf = pax < 0 ? 1 : (((sb >> pax) & 1) == 0);
-        const int mm = (sy ? 0 : 1) | (sz ? 0 : 2);
         const int Do = ring_depth(j, k), Dp = ring_depth(pj, pk);
         const double *const ro = rng + 4 * ring_first(T1, j, k);
         const double *const rp_ = rng + 4 * ring_first(T1, pj, pk);
         const int rrow = ((sz ? T2 - 1 - k : k) * T1 + (sy ? T1 - 1 - j : j)) * 4;
-        named_bar(1, 64);                                    // B_0
+        named_bar(1, 96);                                    // B_0
         S3T(t_cb0);
         S3ADD(9, t_cb0 - t_start, 0);
         S3ADD(5, 1, 0);
@@ -610,7 +649,6 @@ __global__ void __launch_bounds__(64, 4)
         long long cbar = 0;
 #endif
         double u0 = 0.0, sS0 = 0.0, sB0 = 0.0, wq0 = 0.0;
-        double er[4] = {0.0, 0.0, 0.0, 0.0};                 // x-edge chain: previous set, rank order
         if (pre0) {
             u0 = MX[wofm(0, j, k)];
             const double px = (m0 & 1) ? MX[wofm(-1, j, k)] : 0.0;
@@ -620,12 +658,6 @@ __global__ void __launch_bounds__(64, 4)
                 if (!(cb & 1)) {
                     sS0 = pz;
                     sB0 = py;
-                }
-                const double pyz = (cb & 6) == 6 ? MX[wofm(0, -1, -1)] : 0.0;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {                // member S = r ^ mm: bit 0 across y, bit 1 across z
-                    const int S = r ^ mm;
-                    er[r] = S == 0 ? u0 : (S == 1 ? py : (S == 2 ? pz : pyz));
                 }
             }
             if (m1 == 2) wq0 = MX[wofm(0, -1, k)];
@@ -639,11 +671,16 @@ __global__ void __launch_bounds__(64, 4)
         lds2(ro + 2, c1, c2);
         lds2(rp_, q0, d0);
         lds2(rp_ + 2, d1, d2);
+        int passed = 0;                                      // barriers passed after B_0
+        double xu = 0.0, xs = 0.0, xb = 0.0;                 // x-edge results of lane 0's column
 #pragma unroll 1
         for (int s = 0; s < NS; ++s, ++c) {
-            if ((s & 3) == 0 && (s >> 2) + 1 < NCH) {        // B_m, m = s / 4 + 1: batch m is in the rings
+            if ((s & 3) == 0) {                              // steps [4m - 8, 4m - 4) run after B_m
                 S3T(t_cb);
-                named_bar(1, 64);
+                while (passed < s / 4 + 2) {
+                    named_bar(1, 96);
+                    ++passed;
+                }
                 S3ACC(cbar, t_cb);
             }
             if ((s & 3) == 0 && s / 4 >= Y.nres) {           // result slot of chunk s / 4 is free
@@ -670,38 +707,14 @@ __global__ void __launch_bounds__(64, 4)
             const double ua = fma(mab, ub, ra);
             double un = qf ? ub : ua, pv = qf ? ua : ub;
             double nS = pv, nB = pv, nWq = pv;
-            if (xe_box) {                                    // the x-edge set of lane 0's column (all lanes, no divergence)
-                const int cx = s;                            // lane 0's column
-                const double *o = XF + 96 * (((cx + 3) >> 2) % 3) + 24 * ((cx + 3) & 3);
-                double rhs[4], uu[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) rhs[r] = fma(o[20 + r], er[r], o[16 + r]);
-                int li = 0;
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-#pragma unroll
-                    for (int q = p + 1; q < 4; ++q) {
-                        rhs[q] = fma(-o[li], rhs[p], rhs[q]);
-                        ++li;
-                    }
-                constexpr int UI[4] = {0, 3, 5, 6};
-#pragma unroll
-                for (int p = 3; p >= 0; --p) {
-                    double sacc = rhs[p];
-#pragma unroll
-                    for (int q = p + 1; q < 4; ++q) sacc = fma(-o[6 + UI[p] + (q - p - 1)], uu[q], sacc);
-                    uu[p] = sacc * o[12 + p];
-                }
-                auto member = [&](int Sm) {                  // value of member Sm (rank Sm ^ mm)
-                    const int r = Sm ^ mm;
-                    return r == 0 ? uu[0] : (r == 1 ? uu[1] : (r == 2 ? uu[2] : uu[3]));
-                };
-                const bool use = xedge && cx >= 1 && cx < T0;
-                un = use ? member(0) : un;
-                nS = use ? member(2) : nS;
-                nB = use ? member(1) : nB;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) er[r] = use ? uu[r] : er[r];
+            if (xe_box) {                                    // the x-edge set of lane 0's column (warp X)
+                const double *o = XE + 4 * (s & 15);
+                lds2(o, xu, xs);
+                xb = o[2];
+                const bool use = xedge && s >= 1 && s < T0;
+                un = use ? xu : un;
+                nS = use ? xs : nS;
+                nB = use ? xb : nB;
             }
             if (pre0 && c == 0) {
                 un = u0;
@@ -737,6 +750,10 @@ __global__ void __launch_bounds__(64, 4)
                     bulk_commit();
                 }
             }
+        }
+        while (passed < MLAST) {
+            named_bar(1, 96);
+            ++passed;
         }
         if (lane == 0) bulk_wait_all();
 #ifdef SW_TRACE
@@ -786,7 +803,7 @@ inline cudaError_t launch_sweep3s_t(const Sweep3sArgs &A, const CUtensorMap *M, 
                                     cudaStream_t s) {
     auto kern = k_sweep3s<FACES, TRI, SHAPE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<tiles, 64, smem, s>>>(A, M[0], M[1], M[2], M[3], M[4], M[5]);
+    kern<<<tiles, 96, smem, s>>>(A, M[0], M[1], M[2], M[3], M[4], M[5]);
     return cudaGetLastError();
 }
 

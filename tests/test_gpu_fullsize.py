@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (64 x 64 boxes
-for configs 3 and 4, 32 x 8 x 4 for config 5), on sampled outputs the oracle computes one by one.
+for configs 3 and 4, 512 x 8 x 4 for config 5, plus the 32 x 8 x 4 comparison line), on sampled
+outputs the oracle computes one by one.
 
 A box's part of a decomposed sweep depends only on the old values, b and faces within two layers
 of the box (tile locality, SURVEY §8(c) C-SOR 2).  So the oracle sweeps a sub-grid of a few boxes
@@ -92,8 +93,9 @@ def test_config3_full_size_sampled_boxes_and_pcg():
     assert O.relres(pb, g.get_vector(B.X), b) < 2e-8
 
 
-def test_config5_full_size_sampled_boxes():
-    n, tile = (512, 512, 512), (32, 8, 4)
+@pytest.mark.parametrize("tile", [(512, 8, 4), (32, 8, 4)])
+def test_config5_full_size_sampled_boxes(tile):
+    n = (512, 512, 512)
     shape = tuple(reversed(n))
     k = gen.lognormal_k(0, tuple(v + 2 for v in shape), 0.5)
     x0 = gen.uniform_field(13, gen.STREAM_X0, shape)
@@ -105,3 +107,21 @@ def test_config5_full_size_sampled_boxes():
     g.sor_sweep([1.0], 1, 5)
     torch.cuda.synchronize()
     check_boxes(n, tile, x0, b, g.get_vector(B.X), [1.0], 5, k, (1.0, 0.1, 0.01), nsample=4)
+
+
+def test_config5_full_size_pcg():
+    """ILU(0)-PCG on config 5's grid with bench.py's boxes: the oracle's residual of the GPU solution."""
+    n, tile = (512, 512, 512), (512, 8, 4)
+    shape = tuple(reversed(n))
+    k = gen.lognormal_k(0, tuple(v + 2 for v in shape), 0.5)
+    kp = np.pad(k, [(1, 1), (0, 0), (0, 0)], constant_values=1.0)
+    b = gen.uniform_field(0, gen.STREAM_RHS, shape) / float((n[0] + 1) ** 2)
+    g = B.Grid(3, n, B.COEF_FACES).decompose(tile)
+    g.set_coefficients_k(kp, (1.0, 0.1, 0.01))
+    g.set_vector(B.B, b)
+    it, rel, ok = g.pcg_solve(B.PC_ILU0, 1.0, B.PAIR_SYMMETRIC, 1e-8, 5000)
+    assert ok and rel < 1e-8
+    x = g.get_vector(B.X)
+    del g
+    pb = O.tiled(n, tile, faces=O.faces_from_k(n, k, (1.0, 0.1, 0.01)))
+    assert O.relres(pb, x, b) < 2e-8
