@@ -202,12 +202,24 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 __device__ __forceinline__ void lds2(const double *p, double &a, double &b) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(smem_u32(p)));
 }
+__device__ __forceinline__ void lds2u(uint32_t a, double &x, double &y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ double lds1u(uint32_t a) {
+    double x;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
+    return x;
+}
+__device__ __forceinline__ void sts1u_if(uint32_t a, double v, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.f64 [%0], %1;\n}\n" ::"r"(a), "d"(v), "r"((int)pred)
+                 : "memory");
+}
 __device__ __forceinline__ void sts2(double *p, double a, double b) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(p)), "d"(a), "d"(b) : "memory");
 }
 
 template <bool FACES, bool TRI, int SHAPE>
-__global__ void __launch_bounds__(96, 4)
+__global__ void __launch_bounds__(128, 4)
     k_sweep3s(const __grid_constant__ Sweep3sArgs A, const __grid_constant__ CUtensorMap mXO,
               const __grid_constant__ CUtensorMap mBB, const __grid_constant__ CUtensorMap mF0,
               const __grid_constant__ CUtensorMap mF1, const __grid_constant__ CUtensorMap mF2,
@@ -253,8 +265,11 @@ __global__ void __launch_bounds__(96, 4)
     int fl = 0;                                              // singular-pivot flag of this lane
 
     S3T(t_start);
-    if (warp == 1) {
-        // ============================================================ producer
+    if (warp == 1 || warp == 3) {
+        // ============================================================ producers
+        // warp 1 (pw = 0) also stages the raw chunks (TMA) and solves the start column; the two
+        // producer warps form the even / odd rounds of every batch
+        const int pw = warp == 3;
         auto org = [&](int arr, int axis) -> int {           // padded global origin of a window axis
             const int lmn = axis == 1 ? Y.lmin[arr] : Y.pmin[arr];
             const int n = axis == 1 ? Y.R[arr] : Y.Q[arr];
@@ -294,7 +309,7 @@ __global__ void __launch_bounds__(96, 4)
             }
         };
         auto wait_chunk = [&](int m) { mbar_wait(&bar[m % NR], (m / NR) & 1); };
-        if (lane == 0) {
+        if (pw == 0 && lane == 0) {
             for (int q = 0; q < NR; ++q) mbar_init(&bar[q], 1);
             fence_mbar_init();
             for (int m = 0; m < min(NCH, NR); ++m) issue(m);
@@ -342,6 +357,7 @@ __global__ void __launch_bounds__(96, 4)
             node_compact<TRI>(A, v, L, lz, sb, cb, r0, cc);
         };
 
+        if (pw == 0) {
         // ---- 1. the start column: compact arrays over local columns {-1, 0}, rows [-1, T1),
         //      planes [-1, T2) (X: r0, then the solved values; C0..C2), solved in place
         wait_chunk(0);
@@ -417,12 +433,13 @@ __global__ void __launch_bounds__(96, 4)
             }
         }
 
+        }
         // ---- 2. production batches: batch 0 = column 0, batch m >= 1 = columns [4m-3, 4m+1);
         //      lanes: column cs + (lane & 3) of x-line 8 r + (lane >> 2), round r.  Everything but
         //      the column is the same in every batch: per-round word offsets, ring line, depth.
         const int NLn = Y.nl;
-        constexpr int MAXR = 8;                               // rounds (x-lines / 8), <= 8
-        const int nr = (NLn + 7) / 8;
+        constexpr int MAXR = 4;                               // rounds per producer warp (x-lines / 16)
+        const int nr = (NLn + 7) / 8;                         // rounds of both warps (r = 2 i + pw)
         struct PRound {
             int kx, kxy, kxz, kb, k0, k1i, k1e, k2i, k2e, rb, D, pos, L;
             bool on, cuty, cutz;
@@ -431,12 +448,13 @@ __global__ void __launch_bounds__(96, 4)
         {
             const int dy = sy ? -4 : 4;
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) {
+            for (int i = 0; i < MAXR; ++i) {
+                const int r = 2 * i + pw;
                 if (r < nr) {
                     const int li = 8 * r + (lane >> 2);
                     const int j = li % (T1 + 1) - 1, k = li / (T1 + 1) - 1;
                     const int L = (j < 0 ? 2 : 0) | (k < 0 ? 4 : 0);
-                    PRound &q = pr[r];
+                    PRound &q = pr[i];
                     q.L = L;
                     q.on = li < NLn && (L & cb) == L;
                     q.kx = rowk(XO, j, k);
@@ -479,9 +497,9 @@ __global__ void __launch_bounds__(96, 4)
             const int wc = colw(c), wp = colw(c + 1), wm = colw(c - 1);
             const int f0i = sx ? wm : wc, f0e = sx ? wc : wp;
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) {
-                if (r < nr) {
-                    PRound &q = pr[r];
+            for (int i = 0; i < MAXR; ++i) {
+                if (2 * i + pw < nr) {
+                    PRound &q = pr[i];
                     const double xo = ring[wc + q.kx];
                     const double b = A.has_aux ? ring[wc + q.kb] : 0.0;
                     double fi0 = 1.0, fe0 = 1.0, fi1 = 1.0, fe1 = 1.0, fi2 = 1.0, fe2 = 1.0;
@@ -518,9 +536,9 @@ __global__ void __launch_bounds__(96, 4)
         };
         S3T(t_xs);
         S3ADD(3, t_xs - t_sets, 32);
-        produce0();
+        if (pw == 0) produce0();
         __syncwarp();
-        named_bar(1, 96);                                    // B_0: start column and batch 0
+        named_bar(1, 128);                                    // B_0: start column and batch 0
         S3T(t_b0);
         S3ADD(4, t_b0 - t_xs, 32);
 #ifdef SW_TRACE
@@ -532,17 +550,18 @@ __global__ void __launch_bounds__(96, 4)
             S3ACC(wch, t_w);
             produce(m);
             __syncwarp();
-            if (lane == 0 && m + 2 < NCH) {                  // chunk m - 1 is dead: its slot takes m + 2
+            named_bar(2, 64);                                // both producers are done with chunk m - 1
+            if (pw == 0 && lane == 0 && m + 2 < NCH) {       // chunk m - 1 is dead: its slot takes m + 2
                 fence_proxy_async_smem();
                 issue(m + 2);
                 if (m + 4 < NCH) prefetch(m + 4);
             }
             __syncwarp();
             S3T(t_bb);
-            named_bar(1, 96);                                // B_m
+            named_bar(1, 128);                                // B_m
             S3ACC(wbar, t_bb);
         }
-        for (int m = NCH; m <= MLAST; ++m) named_bar(1, 96);
+        for (int m = NCH; m <= MLAST; ++m) named_bar(1, 128);
 #ifdef SW_TRACE
         S3ADD(6, wch, 32);
         S3ADD(7, wbar, 32);
@@ -558,7 +577,7 @@ __global__ void __launch_bounds__(96, 4)
         // oracle's elimination order, DESIGN R-8).  XE[c % 16] = (u(c,0,0), u(c,0,-1), u(c,-1,0)).
         const bool xe_box = (cb & 6) == 6;
         const int mm = (sy ? 0 : 1) | (sz ? 0 : 2);
-        named_bar(1, 96);                                    // B_0
+        named_bar(1, 128);                                    // B_0
         double er[4] = {0.0, 0.0, 0.0, 0.0};                 // previous set, rank order
         if (xe_box) {
             const double u0 = MX[wofm(0, 0, 0)], py = MX[wofm(0, -1, 0)], pz = MX[wofm(0, 0, -1)];
@@ -622,7 +641,7 @@ __global__ void __launch_bounds__(96, 4)
                 }
             }
             __syncwarp();
-            named_bar(1, 96);                                // B_m
+            named_bar(1, 128);                                // B_m
         }
     } else {
         // ============================================================ consumer
@@ -641,7 +660,7 @@ __global__ void __launch_bounds__(96, 4)
         const double *const ro = rng + 4 * ring_first(T1, j, k);
         const double *const rp_ = rng + 4 * ring_first(T1, pj, pk);
         const int rrow = ((sz ? T2 - 1 - k : k) * T1 + (sy ? T1 - 1 - j : j)) * 4;
-        named_bar(1, 96);                                    // B_0
+        named_bar(1, 128);                                    // B_0
         S3T(t_cb0);
         S3ADD(9, t_cb0 - t_start, 0);
         S3ADD(5, 1, 0);
@@ -666,19 +685,41 @@ __global__ void __launch_bounds__(96, 4)
         const int NS = T0 + T1 + T2 - 2, lag = T1 + T2 - 2, NQ = T0 / 4;
         int c = -j - k, po = 0, pp = 0;                      // column; ring positions of column c
         double W = 0.0, Wq = 0.0, u = 0.0, sS = 0.0, sB = 0.0;
-        double r0, c0, c1, c2, q0, d0, d1, d2;               // ring entries of column c (loaded a step ahead)
-        lds2(ro, r0, c0);                                    // (entries of column c < 0: never used)
-        lds2(ro + 2, c1, c2);
-        lds2(rp_, q0, d0);
-        lds2(rp_ + 2, d1, d2);
+        // 32-bit shared addresses (no generic-to-shared conversion in the loop)
+        const uint32_t ro_a = smem_u32(ro), rp_a = smem_u32(rp_), xe_a = smem_u32(XE);
+        const uint32_t res_a = smem_u32(res) + 8 * (rrow);
+        // coefficients of the step's column, prepared a step ahead (off the wavefront's dependence
+        // chain): the couplings without the pair axis, the pair couplings and 1 / (1 - m m')
+        struct Co {
+            double r0, c0, e1, e2, q0, d0, f1, f2, mab, mba, inv;
+            bool sing;
+        };
+        auto prep = [&](Co &o) {
+            double c1, c2, d1, d2;
+            lds2u(ro_a + 32 * po, o.r0, o.c0);
+            lds2u(ro_a + 32 * po + 16, c1, c2);
+            lds2u(rp_a + 32 * pp, o.q0, o.d0);
+            lds2u(rp_a + 32 * pp + 16, d1, d2);
+            const double cpp = pax == 1 ? c1 : c2, cqp = pax == 1 ? d1 : d2;
+            o.e1 = pax == 1 ? 0.0 : c1;
+            o.e2 = pax == 2 ? 0.0 : c2;
+            o.f1 = pax == 1 ? 0.0 : d1;
+            o.f2 = pax == 2 ? 0.0 : d2;
+            o.mab = pax < 0 ? 0.0 : (qf ? cqp : cpp);
+            o.mba = pax < 0 ? 0.0 : (qf ? cpp : cqp);
+            const double m11 = fma(o.mba, -o.mab, 1.0);
+            o.sing = pax >= 0 && !(fabs(m11) >= 1e-14);
+            o.inv = div_rn(1.0, m11);
+        };
+        Co co;
+        prep(co);                                            // (entries of column c < 0: never used)
         int passed = 0;                                      // barriers passed after B_0
-        double xu = 0.0, xs = 0.0, xb = 0.0;                 // x-edge results of lane 0's column
 #pragma unroll 1
         for (int s = 0; s < NS; ++s, ++c) {
             if ((s & 3) == 0) {                              // steps [4m - 8, 4m - 4) run after B_m
                 S3T(t_cb);
                 while (passed < s / 4 + 2) {
-                    named_bar(1, 96);
+                    named_bar(1, 128);
                     ++passed;
                 }
                 S3ACC(cbar, t_cb);
@@ -688,29 +729,24 @@ __global__ void __launch_bounds__(96, 4)
                 __syncwarp();
             }
             const bool act = onl && c >= 0 && c < T0;
-            // ---- own node and partner: r0 and couplings from the rings
-
+            double xu = 0.0, xs = 0.0, xb = 0.0;             // x-edge results of lane 0's column (warp X)
+            if (xe_box) {
+                lds2u(xe_a + 32 * (s & 15), xu, xs);
+                xb = lds1u(xe_a + 32 * (s & 15) + 16);
+            }
             // ---- the neighbours' new values (previous step)
             const double S = shfl_up_w(u, 1), B = shfl_up_w(u, T1);
             const double Sq = shfl_up_w(sS, 1), Bq = shfl_up_w(sB, T1);
             // ---- rows in axis order x, y, z without the pair axis; the 2 x 2 pair (ge_solve_k<2>)
-            const double cpp = pax == 1 ? c1 : c2, cqp = pax == 1 ? d1 : d2;
-            const double e1 = pax == 1 ? 0.0 : c1, e2 = pax == 2 ? 0.0 : c2;
-            const double f1 = pax == 1 ? 0.0 : d1, f2 = pax == 2 ? 0.0 : d2;
-            const double rp = fma(e2, B, fma(e1, S, fma(c0, W, r0)));
-            const double rq = fma(f2, Bq, fma(f1, Sq, fma(d0, Wq, q0)));
+            const double rp = fma(co.e2, B, fma(co.e1, S, fma(co.c0, W, co.r0)));
+            const double rq = fma(co.f2, Bq, fma(co.f1, Sq, fma(co.d0, Wq, co.q0)));
             const double ra = qf ? rq : rp, rb = qf ? rp : rq;
-            const double mab = pax < 0 ? 0.0 : (qf ? cqp : cpp), mba = pax < 0 ? 0.0 : (qf ? cpp : cqp);
-            const double m11 = fma(mba, -mab, 1.0);
-            fl |= act && pax >= 0 && !(pre0 && c == 0) && !(fabs(m11) >= 1e-14);
-            const double ub = fma(mba, ra, rb) * div_rn(1.0, m11);
-            const double ua = fma(mab, ub, ra);
+            fl |= act && !(pre0 && c == 0) && co.sing;
+            const double ub = fma(co.mba, ra, rb) * co.inv;
+            const double ua = fma(co.mab, ub, ra);
             double un = qf ? ub : ua, pv = qf ? ua : ub;
             double nS = pv, nB = pv, nWq = pv;
-            if (xe_box) {                                    // the x-edge set of lane 0's column (warp X)
-                const double *o = XE + 4 * (s & 15);
-                lds2(o, xu, xs);
-                xb = o[2];
+            {
                 const bool use = xedge && s >= 1 && s < T0;
                 un = use ? xu : un;
                 nS = use ? xs : nS;
@@ -723,7 +759,7 @@ __global__ void __launch_bounds__(96, 4)
                 nWq = wq0;
             }
             // ---- results, state for the next step (idle lanes forward zeros: finite values only)
-            if (act) res[((c >> 2) & (Y.nres - 1)) * Y.ressz + rrow + (sx ? 3 - (c & 3) : (c & 3))] = un;
+            sts1u_if(res_a + 8 * (((c >> 2) & (Y.nres - 1)) * Y.ressz + (sx ? 3 - (c & 3) : (c & 3))), un, act);
             W = act ? un : W;
             Wq = act ? nWq : Wq;
             u = act ? un : 0.0;
@@ -734,10 +770,7 @@ __global__ void __launch_bounds__(96, 4)
                 pp = pp + 1 == Dp ? 0 : pp + 1;
             }
             // next step's entries (idle lanes read stale ones: never stored or forwarded)
-            lds2(ro + 4 * po, r0, c0);
-            lds2(ro + 4 * po + 2, c1, c2);
-            lds2(rp_ + 4 * pp, q0, d0);
-            lds2(rp_ + 4 * pp + 2, d1, d2);
+            prep(co);
             // ---- result chunk q complete: all lanes passed its last column
             const int qd = s - lag - 3;
             if (qd >= 0 && (qd & 3) == 0 && qd / 4 < NQ) {
@@ -752,7 +785,7 @@ __global__ void __launch_bounds__(96, 4)
             }
         }
         while (passed < MLAST) {
-            named_bar(1, 96);
+            named_bar(1, 128);
             ++passed;
         }
         if (lane == 0) bulk_wait_all();
@@ -803,7 +836,7 @@ inline cudaError_t launch_sweep3s_t(const Sweep3sArgs &A, const CUtensorMap *M, 
                                     cudaStream_t s) {
     auto kern = k_sweep3s<FACES, TRI, SHAPE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<tiles, 96, smem, s>>>(A, M[0], M[1], M[2], M[3], M[4], M[5]);
+    kern<<<tiles, 128, smem, s>>>(A, M[0], M[1], M[2], M[3], M[4], M[5]);
     return cudaGetLastError();
 }
 
