@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(128, 4)
             node_compact<TRI>(A, v, L, lz, sb, cb, r0, cc);
         };
 
+#ifdef SW_TRACE
+        long long t_sets_out = 0;
+#endif
         if (pw == 0) {
         // ---- 1. the start column: compact arrays over local columns {-1, 0}, rows [-1, T1),
         //      planes [-1, T2) (X: r0, then the solved values; C0..C2), solved in place
@@ -408,6 +411,9 @@ __global__ void __launch_bounds__(128, 4)
         }
         S3T(t_sets);
         S3ADD(2, t_sets - t_mx, 32);
+#ifdef SW_TRACE
+        t_sets_out = t_sets;
+#endif
         // the x-start face pairs (0, j, k) / (-1, j, k), a 2D recurrence over d = j + k
         if (cb & 1) {
             const bool on = lane < nl;
@@ -535,14 +541,14 @@ __global__ void __launch_bounds__(128, 4)
             }
         };
         S3T(t_xs);
-        S3ADD(3, t_xs - t_sets, 32);
+        S3ADD(3, t_xs - t_sets_out, 32);
         if (pw == 0) produce0();
         __syncwarp();
         named_bar(1, 128);                                    // B_0: start column and batch 0
         S3T(t_b0);
         S3ADD(4, t_b0 - t_xs, 32);
 #ifdef SW_TRACE
-        long long wch = 0, wbar = 0;
+        long long wch = 0, wbar = 0, p1b2 = 0, p2b2 = 0;
 #endif
         for (int m = 1; m < NCH; ++m) {
             S3T(t_w);
@@ -550,7 +556,11 @@ __global__ void __launch_bounds__(128, 4)
             S3ACC(wch, t_w);
             produce(m);
             __syncwarp();
+            S3T(t_b2);
             named_bar(2, 64);                                // both producers are done with chunk m - 1
+#ifdef SW_TRACE
+            if (pw) p2b2 += sw_clock() - t_b2; else p1b2 += sw_clock() - t_b2;
+#endif
             if (pw == 0 && lane == 0 && m + 2 < NCH) {       // chunk m - 1 is dead: its slot takes m + 2
                 fence_proxy_async_smem();
                 issue(m + 2);
@@ -564,6 +574,8 @@ __global__ void __launch_bounds__(128, 4)
         for (int m = NCH; m <= MLAST; ++m) named_bar(1, 128);
 #ifdef SW_TRACE
         S3ADD(6, wch, 32);
+        S3ADD(14, p1b2, 32);
+        S3ADD(15, p2b2, 96);
         S3ADD(7, wbar, 32);
         S3ADD(8, sw_clock() - t_start, 32);
 #endif
@@ -588,61 +600,96 @@ __global__ void __launch_bounds__(128, 4)
                 er[r] = S == 0 ? u0 : (S == 1 ? py : (S == 2 ? pz : pyz));
             }
         }
+#ifdef SW_TRACE
+        long long xbusy = 0;
+#endif
         for (int m = 1; m <= MLAST; ++m) {
+            S3T(t_xb);
             const int bt = m - 1;                            // the batch of this interval
-            if (xe_box && lane == 0 && bt >= 1 && bt < NCH) {
+            if (xe_box && bt >= 1 && bt < NCH) {
+                // lane t < 4 factors the set of the batch's column 4 bt - 3 + t (independent of the
+                // chain): multipliers l, eliminated upper triangle U, reciprocal pivots, the rows' r0
+                // and x couplings, in registers; then the chain passes from lane to lane: in round t
+                // lane t substitutes its set with the previous set's solution, broadcast by shuffles
+                const int c = 4 * bt - 3 + lane;
+                const bool mine = lane < 4 && c >= 1 && c < T0;
+                double fL[6], fU[6], fI[4], fR[4], fX[4];
+                {
+                    const int pos = (mine ? c : 1) % RING_EXTRA;  // members have skew 0
+                    double M[4][4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int S = r ^ mm, jj = -(S & 1), kk = -(S >> 1);
+                        const double *e = rng + 4 * (ring_first(T1, jj, kk) + pos);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
+                        M[r][r ^ 1] = -e[2];                     // toward the partner across y
+                        M[r][r ^ 2] = -e[3];                     // across z
+                        fR[r] = e[0];
+                        fX[r] = e[1];
+                    }
+                    int li = 0;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        const double piv = M[p][p];
+                        fl |= mine && !(fabs(piv) >= 1e-14);
+                        fI[p] = div_rn(1.0, piv);
+#pragma unroll
+                        for (int q = p + 1; q < 4; ++q) {
+                            const double l = M[q][p] * fI[p];
+                            fL[li++] = l;
+#pragma unroll
+                            for (int jj = p + 1; jj < 4; ++jj) M[q][jj] = fma(-l, M[p][jj], M[q][jj]);
+                        }
+                    }
+                    int ui = 0;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int jj = p + 1; jj < 4; ++jj) fU[ui++] = M[p][jj];
+                }
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const int c = 4 * bt - 3 + t;
-                    if (c >= 1 && c < T0) {
-                        double M[4][4], r0v[4], cxv[4];
+                    // the same operations and order as ge_solve_k<4> (every lane runs them on its own
+                    // factors; lane t's result is the chain's)
+                    double rhs[4], uu[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int S = r ^ mm, jj = -(S & 1), kk = -(S >> 1);
-                            const double *e = rng + 4 * (ring_first(T1, jj, kk) + c % ring_depth(jj, kk));
+                    for (int r = 0; r < 4; ++r) rhs[r] = fma(fX[r], er[r], fR[r]);
+                    int li = 0;
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
-                            M[r][r ^ 1] = -e[2];                 // toward the partner across y
-                            M[r][r ^ 2] = -e[3];                 // across z
-                            r0v[r] = e[0];
-                            cxv[r] = e[1];
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int q = p + 1; q < 4; ++q) {
+                            rhs[q] = fma(-fL[li], rhs[p], rhs[q]);
+                            ++li;
                         }
-                        double rhs[4], uu[4], inv[4];
+                    constexpr int UI[4] = {0, 3, 5, 6};
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) rhs[r] = fma(cxv[r], er[r], r0v[r]);
+                    for (int p = 3; p >= 0; --p) {
+                        double sacc = rhs[p];
 #pragma unroll
-                        for (int p = 0; p < 4; ++p) {
-                            const double piv = M[p][p];
-                            fl |= !(fabs(piv) >= 1e-14);
-                            inv[p] = div_rn(1.0, piv);
+                        for (int q = p + 1; q < 4; ++q) sacc = fma(-fU[UI[p] + (q - p - 1)], uu[q], sacc);
+                        uu[p] = sacc * fI[p];
+                    }
+                    const int cc = 4 * bt - 3 + t;
+                    if (cc >= 1 && cc < T0) {
 #pragma unroll
-                            for (int q = p + 1; q < 4; ++q) {
-                                const double l = M[q][p] * inv[p];
-#pragma unroll
-                                for (int jj = p + 1; jj < 4; ++jj) M[q][jj] = fma(-l, M[p][jj], M[q][jj]);
-                                rhs[q] = fma(-l, rhs[p], rhs[q]);
-                            }
+                        for (int r = 0; r < 4; ++r) er[r] = __shfl_sync(0xffffffffu, uu[r], t);
+                        if (lane == 0) {
+                            auto pick = [&](int r) { return r == 0 ? er[0] : (r == 1 ? er[1] : (r == 2 ? er[2] : er[3])); };
+                            double *w = XE + 4 * (cc & 15);
+                            w[0] = pick(mm);
+                            w[1] = pick(2 ^ mm);
+                            w[2] = pick(1 ^ mm);
                         }
-#pragma unroll
-                        for (int p = 3; p >= 0; --p) {
-                            double sacc = rhs[p];
-#pragma unroll
-                            for (int q = p + 1; q < 4; ++q) sacc = fma(-M[p][q], uu[q], sacc);
-                            uu[p] = sacc * inv[p];
-                        }
-                        auto pick = [&](int r) { return r == 0 ? uu[0] : (r == 1 ? uu[1] : (r == 2 ? uu[2] : uu[3])); };
-                        double *o = XE + 4 * (c & 15);
-                        o[0] = pick(mm);
-                        o[1] = pick(2 ^ mm);
-                        o[2] = pick(1 ^ mm);
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) er[r] = uu[r];
                     }
                 }
             }
             __syncwarp();
+            S3ACC(xbusy, t_xb);
             named_bar(1, 128);                                // B_m
         }
+        S3ADD(13, xbusy, 64);
     } else {
         // ============================================================ consumer
         const bool onl = lane < nl;

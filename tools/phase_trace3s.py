@@ -11,7 +11,7 @@ from paper_1008_3699_b200 import binding, gen  # noqa: E402
 
 NAMES = {0: "P: chunk 0 arrives", 1: "P: start-column compact", 2: "P: corner + edge chains", 3: "P: x-start sheet",
          4: "P: batch 0 + B_0 wait", 6: "P: chunk waits (batches)", 7: "P: barrier waits (batches)", 8: "P: total",
-         9: "C: wait for B_0", 10: "C: barrier waits (loop)", 11: "C: loop", 12: "C: total"}
+         9: "C: wait for B_0", 10: "C: barrier waits (loop)", 11: "C: loop", 12: "C: total", 13: "X: busy (batches)", 14: "P1: pair-barrier waits", 15: "P2: pair-barrier waits"}
 
 
 def main():
