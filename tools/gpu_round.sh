@@ -19,3 +19,8 @@ echo "ncu launches exit $?"
 timeout 300 $CMD > $OUT/plain_prof.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep2p -s 4 -c 1 -o $OUT/sweep2p $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu full exit $?"
+# config 5's engine: one k_sweep3s launch at 512^3 with 512x8x4 boxes
+ARGS5="--dim 3 --n 512 --tile 512 8 4 --faces --sweeps 4"
+timeout 120 python tools/profile_case.py $ARGS5 > $OUT/plain_c5.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep3s -s 2 -c 1 -o $OUT/sweep3s $(echo python tools/profile_case.py $ARGS5) > $OUT/ncu_c5.log 2>&1
+echo "ncu c5 exit $?"
