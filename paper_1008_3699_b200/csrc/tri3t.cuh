@@ -67,7 +67,7 @@ __device__ __forceinline__ void tri3t_solve(const Tri3tArgs &A, const int64_t gl
             al = A.invd[i];
         } else {
             const double ap = (((fm[0] + fp[0]) + (fm[1] + fp[1])) + (fm[2] + fp[2])) + G.beta;
-            al = A.omega / ap;
+            al = div_rn(A.omega, ap);               // = A.omega / ap (IEEE), no slow-path branch
         }
         double acc = A.coef * A.src[i];
 #pragma unroll
@@ -104,7 +104,7 @@ __device__ __forceinline__ void tri3t_solve(const Tri3tArgs &A, const int64_t gl
     for (int p = 0; p < k; ++p) {
         const double piv = M[p][p];
         if (!(fabs(piv) >= 1e-14)) atomicOr(A.flag, 1);
-        inv[p] = 1.0 / piv;
+        inv[p] = div_rn(1.0, piv);
 #pragma unroll
         for (int q = p + 1; q < k; ++q) {
             const double l = M[q][p] * inv[p];
@@ -151,7 +151,7 @@ __device__ __forceinline__ void tri3t_row(const Tri3tArgs &A, const int64_t gl[3
         al = A.invd[i];
     } else {
         const double ap = (((fm[0] + fp[0]) + (fm[1] + fp[1])) + (fm[2] + fp[2])) + G.beta;
-        al = A.omega / ap;
+        al = div_rn(A.omega, ap);               // = A.omega / ap (IEEE), no slow-path branch
     }
     double acc = A.coef * A.src[i];
 #pragma unroll
@@ -191,7 +191,7 @@ __device__ __forceinline__ void tri3t_ge(double (&M)[K][K], double (&rhs)[K], do
     for (int p = 0; p < K; ++p) {
         const double piv = M[p][p];
         if (report && !(fabs(piv) >= 1e-14)) atomicOr(flag, 1);
-        inv[p] = 1.0 / piv;
+        inv[p] = div_rn(1.0, piv);
 #pragma unroll
         for (int q = p + 1; q < K; ++q) {
             const double l = M[q][p] * inv[p];
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(32) k_tri3t(Tri3tArgs A) {
                     al = cur.invd;
                 } else {
                     const double ap = (((cur.fm[0] + cur.fp[0]) + (cur.fm[1] + cur.fp[1])) + (cur.fm[2] + cur.fp[2])) + G.beta;
-                    al = A.omega / ap;
+                    al = div_rn(A.omega, ap);               // = A.omega / ap (IEEE), no slow-path branch
                 }
                 double acc = A.coef * cur.src;
                 int t = 0;
