@@ -8,11 +8,12 @@
 // One CTA of 256 threads per box (T0, T1 <= 64).  All threads stage in the old values of the box and
 // its 2-node halo in LOCAL coordinates (local +a points away from the box's start corner; a node
 // outside the domain reads +inf) and the slowness of the active nodes (own and partner layers).
-// Level d = x + y of the own nodes: thread t < 64 takes own node (t, d - t) -- directly from the
-// window when it is in no coupled set, else with its partner layer by ordered fixing; results go
-// in place (the window then holds new values on every node's start side and old values on its end
-// side, exactly the split the method prescribes); a named barrier of the 64 level threads per
-// level; write-back of the box by all threads.
+// Thread 0 solves the corner set, then threads 0 and 1 run the two start-face chains (row 0 with
+// its partner row, column 0 with its partner column: pairs by ordered fixing, or plain updates
+// along an uncoupled face); then level d = x + y of the other own nodes: thread t < 64 takes node
+// (t, d - t) directly from the window; results go in place (the window then holds new values on
+// every node's start side and old values on its end side, exactly the split the method
+// prescribes); a named barrier of the 64 level threads per level; write-back by all threads.
 #pragma once
 #include "common.cuh"
 
@@ -71,20 +72,40 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
     auto gyo = [&](int ly) { return Y0 + (sy ? T1 - 1 - ly : ly); };
     auto uw = [&](int lx, int ly) -> double & { return U[(ly + 2) * WX + (lx + 2)]; };
     auto fw = [&](int lx, int ly) -> double { return F[(ly + 1) * FX + (lx + 1)]; };
-    // ---- stage in (old values, +inf outside the domain; slowness of the active region)
-#pragma unroll 4
-    for (int e = threadIdx.x; e < WX * (T1 + 4); e += ek::NT) {
-        const int lx = e % WX - 2, ly = e / WX - 2;
-        const int64_t gx = gxo(lx), gy = gyo(ly);
-        const bool in = gx >= 0 && gx < G.ng[0] && gy >= 0 && gy < G.ng[1];
-        const bool act = lx >= -1 && lx < T0 && ly >= -1 && ly < T1;
-        const int64_t gi = in ? gidx(G, gx, gy, 0) : 0;
-        const double uv = in ? __ldg(A.uo + gi) : eik_inf();
-        const double sv = (in && act) ? __ldg(A.S + gi) : 1.0;
-        U[e] = uv;
-        if (act) F[(ly + 1) * FX + (lx + 1)] = sv;
+    SW_TMARK(t_start);
+    // ---- stage in (old values, +inf outside the domain; slowness of the active region): warp w
+    //      takes local rows w, w + 8, ..., lanes along x (consecutive addresses in either direction)
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int nrow = T1 + 4;
+#pragma unroll 2
+        for (int r = warp; r < nrow; r += ek::NT / 32) {
+            const int ly = r - 2;
+            const int64_t gy = gyo(ly);
+            const bool yin = gy >= 0 && gy < G.ng[1];
+            const bool yact = ly >= -1 && ly < T1;
+            const int64_t rowi = yin ? gidx(G, 0, gy, 0) : 0;
+            double uv[3], sv[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {                  // lx = lane + 32 c - 2 < T0 + 2 <= 68 < 96
+                const int lx = lane + 32 * c - 2;
+                const int64_t gx = gxo(lx);
+                const bool in = yin && lx < T0 + 2 && gx >= 0 && gx < G.ng[0];
+                const bool act = yact && lx >= -1 && lx < T0;
+                uv[c] = in ? __ldg(A.uo + rowi + gx) : eik_inf();
+                sv[c] = (in && act) ? __ldg(A.S + rowi + gx) : 1.0;
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int lx = lane + 32 * c - 2;
+                if (lx < T0 + 2) U[r * WX + (lx + 2)] = uv[c];
+                if (yact && lx >= -1 && lx < T0) F[(ly + 1) * FX + (lx + 1)] = sv[c];
+            }
+        }
     }
     __syncthreads();
+    SW_TMARK(t_staged);
+    SW_TADD(0, t_start, t_staged);
     if (threadIdx.x >= ek::LT) {           // the other warps rejoin for the write-back
         __syncthreads();
         for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
@@ -93,61 +114,49 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
         }
         return;
     }
-    // ---- levels
     const int t = threadIdx.x;
-    for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
-        const int x = t, y = d - t;
-        const bool single = !((x == 0 && cx) || (y == 0 && cy));
-        if (x < T0 && y >= 0 && y < T1 && single) {
-            // a node outside every coupled set: its window neighbours are new on its start side,
-            // old elsewhere (in place, level order), exactly the oracle's values
-            const double a = fmin(uw(x - 1, y), uw(x + 1, y)), b = fmin(uw(x, y - 1), uw(x, y + 1));
-            const double ub = eik_godunov_d(a, b, __dmul_rn(fw(x, y), A.h));
-            const double uo = uw(x, y);
-            uw(x, y) = uo < ub ? uo : ub;
-        } else if (x < T0 && y >= 0 && y < T1 && !(x == 0 && y == 0 && cx && cy)) {
-            // a pair across one coupled start face, ordered fixing written out (R-E3): both
-            // candidates with the other member at +inf, the smaller (ties: lower global index) is
-            // fixed, the other recomputed with it
-            const bool xf = x == 0 && cx;
-            const int qx = xf ? -1 : x, qy = xf ? y : -1;
-            auto cand = [&](int px, int py, int ox, int oy, double ov) {
-                const double w0 = (px - 1 == ox && py == oy) ? ov : uw(px - 1, py);
-                const double w1 = (px + 1 == ox && py == oy) ? ov : uw(px + 1, py);
-                const double v0 = (px == ox && py - 1 == oy) ? ov : uw(px, py - 1);
-                const double v1 = (px == ox && py + 1 == oy) ? ov : uw(px, py + 1);
-                const double ub = eik_godunov_d(fmin(w0, w1), fmin(v0, v1), __dmul_rn(fw(px, py), A.h));
-                const double uo = uw(px, py);
-                return uo < ub ? uo : ub;
-            };
-            const double cp = cand(x, y, qx, qy, eik_inf()), cq = cand(qx, qy, x, y, eik_inf());
-            const int64_t gp = gyo(y) * G.ng[0] + gxo(x), gq = gyo(qy) * G.ng[0] + gxo(qx);
-            const bool pfirst = gp < gq ? !(cq < cp) : (cp < cq);
-            double up, uq;
-            if (pfirst) {
-                up = cp;
-                uq = cand(qx, qy, x, y, up);
-            } else {
-                uq = cq;
-                up = cand(x, y, qx, qy, uq);
-            }
-            uw(x, y) = up;
-            uw(qx, qy) = uq;
-        } else if (x < T0 && y >= 0 && y < T1) {
+    // a node outside every coupled set: its window neighbours are new on its start side, old
+    // elsewhere (in place, in a causal order), exactly the oracle's values
+    auto single_upd = [&](int x, int y) {
+        const double a = fmin(uw(x - 1, y), uw(x + 1, y)), b = fmin(uw(x, y - 1), uw(x, y + 1));
+        const double ub = eik_godunov_d(a, b, __dmul_rn(fw(x, y), A.h));
+        const double uo = uw(x, y);
+        uw(x, y) = uo < ub ? uo : ub;
+    };
+    // candidate of member (px, py) with member (ox, oy) at value ov (+inf: unfixed)
+    auto cand = [&](int px, int py, int ox, int oy, double ov) {
+        const double w0 = (px - 1 == ox && py == oy) ? ov : uw(px - 1, py);
+        const double w1 = (px + 1 == ox && py == oy) ? ov : uw(px + 1, py);
+        const double v0 = (px == ox && py - 1 == oy) ? ov : uw(px, py - 1);
+        const double v1 = (px == ox && py + 1 == oy) ? ov : uw(px, py + 1);
+        const double ub = eik_godunov_d(fmin(w0, w1), fmin(v0, v1), __dmul_rn(fw(px, py), A.h));
+        const double uo = uw(px, py);
+        return uo < ub ? uo : ub;
+    };
+    // a pair across one coupled start face, ordered fixing written out (R-E3): both candidates
+    // with the other member at +inf, the smaller (ties: lower global index) is fixed, the other
+    // recomputed with it
+    auto pairfix = [&](int x, int y, bool xf) {
+        const int qx = xf ? -1 : x, qy = xf ? y : -1;
+        const double cp = cand(x, y, qx, qy, eik_inf()), cq = cand(qx, qy, x, y, eik_inf());
+        const int64_t gp = gyo(y) * G.ng[0] + gxo(x), gq = gyo(qy) * G.ng[0] + gxo(qx);
+        const bool pfirst = gp < gq ? !(cq < cp) : (cp < cq);
+        // the other member recomputed with the fixed one (one call with selected arguments, so
+        // that the two chain lanes stay converged)
+        const double fv = pfirst ? cp : cq;
+        const double ov = pfirst ? cand(qx, qy, x, y, fv) : cand(x, y, qx, qy, fv);
+        uw(x, y) = pfirst ? fv : ov;
+        uw(qx, qy) = pfirst ? ov : fv;
+    };
+    // ---- the corner set, then the two start-face chains (row 0 with its partner row, column 0
+    //      with its partner column), then the rest of the box level by level.  Any causal order
+    //      gives the oracle's values (every node reads new values only on its start side); the
+    //      chains first leave uniform single-node levels (no divergent set solves inside them).
+    if (t == 0) {
+        if (cx && cy) {
             // the corner set (4 members) in local coordinates, generic ordered fixing
-            int mx[4], my[4], k = 1;
-            mx[0] = x;
-            my[0] = y;
-            if (x == 0 && y == 0 && cx && cy) {
-                mx[1] = -1; my[1] = 0; mx[2] = 0; my[2] = -1; mx[3] = -1; my[3] = -1;
-                k = 4;
-            } else if (x == 0 && cx) {
-                mx[1] = -1; my[1] = y;
-                k = 2;
-            } else if (y == 0 && cy) {
-                mx[1] = x; my[1] = -1;
-                k = 2;
-            }
+            int mx[4] = {0, -1, 0, -1}, my[4] = {0, 0, -1, -1};
+            constexpr int k = 4;
             // ascending global index (the oracle's member order; ties in the selection go to it)
             int64_t gi[4];
             for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
@@ -187,10 +196,81 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
                 val[best] = cbest;
             }
             for (int m = 0; m < k; ++m) uw(mx[m], my[m]) = val[m];
+        } else if (cx || cy) {
+            pairfix(0, 0, cx);
+        } else {
+            single_upd(0, 0);
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(ek::LT) : "memory");   // the level threads only
+    }
+    __syncwarp();
+    if (t < 2) {
+        // lane 0: row 0 with the partner row (k, -1); lane 1: column 0 with the partner column
+        // (-1, k); in step, with the pair geometry written out: along the chain the member's and the
+        // partner's previous values stay in registers (their west / south new neighbour), the old
+        // neighbours come from the window, the pair is solved by ordered fixing as pairfix does
+        // (its member order is fixed per chain: the partner is first iff the box starts at the low
+        // end of the coupled axis)
+        const bool row = t == 0;
+        const bool cpl = row ? cy : cx;
+        const int len = row ? T0 : T1;
+        const bool pfix = row ? (sy == 0) : (sx == 0);           // partner before own in global order
+        // window accessors in chain coordinates: node k of the chain, offset o across the face
+        // (o = 0 own line, -1 partner line, +1 the line after own, -2 the line beyond the partner)
+        auto cw = [&](int k, int o) -> double { return row ? uw(k, o) : uw(o, k); };
+        auto cf = [&](int k, int o) -> double { return row ? fw(k, o) : fw(o, k); };
+        double po = cw(0, 0), pq = cw(0, -1);                       // the corner's results
+        const double inf = eik_inf();
+        for (int k = 1; k < (T0 > T1 ? T0 : T1); ++k) {
+            if (k < len) {
+                const double uo_o = cw(k, 0), e_o = cw(k + 1, 0), n_o = cw(k, 1);
+                const double fh_o = __dmul_rn(cf(k, 0), A.h);
+                double res_o, res_q;
+                if (cpl) {
+                    const double uo_q = cw(k, -1), e_q = cw(k + 1, -1), s_q = cw(k, -2);
+                    const double fh_q = __dmul_rn(cf(k, -1), A.h);
+                    // chain-along pairs (the oracle's sides in global order are order independent: min)
+                    auto cand_o = [&](double vq) {       // own: W new (po), E old, across the face vq, N old
+                        const double ub = eik_godunov_d(fmin(po, e_o), fmin(vq, n_o), fh_o);
+                        return uo_o < ub ? uo_o : ub;
+                    };
+                    auto cand_q = [&](double vo) {       // partner: W new (pq), E old, S old, across vo
+                        const double ub = eik_godunov_d(fmin(pq, e_q), fmin(s_q, vo), fh_q);
+                        return uo_q < ub ? uo_q : ub;
+                    };
+                    // (for the column chain "W/E" are the partner's and own's south / north sides and
+                    //  "across" the west / east side: a = min over x, b = min over y either way,
+                    //  and fmin is symmetric, so the same two mins result)
+                    const double co = cand_o(inf), cq = cand_q(inf);
+                    const bool ofirst = pfix ? (co < cq) : !(cq < co);   // ties: the lower global index
+                    const double fv = ofirst ? co : cq;
+                    const double ov = ofirst ? cand_q(fv) : cand_o(fv);
+                    res_o = ofirst ? fv : ov;
+                    res_q = ofirst ? ov : fv;
+                    (row ? uw(k, -1) : uw(-1, k)) = res_q;
+                } else {
+                    const double ub = eik_godunov_d(fmin(po, e_o), fmin(cw(k, -1), n_o), fh_o);
+                    res_o = uo_o < ub ? uo_o : ub;
+                    res_q = pq;
+                }
+                (row ? uw(k, 0) : uw(0, k)) = res_o;
+                po = res_o;
+                pq = res_q;
+            }
+        }
+    }
+    SW_TMARK(t_chains);
+    asm volatile("bar.sync 1, %0;" ::"r"(ek::LT) : "memory");   // the level threads only
+    SW_JITTER_POINT();
+    SW_TADD(1, t_staged, t_chains);
+    for (int d = 2; d <= (T0 - 1) + (T1 - 1); ++d) {
+        const int x = t, y = d - t;
+        if (x >= 1 && x < T0 && y >= 1 && y < T1) single_upd(x, y);
+        asm volatile("bar.sync 1, %0;" ::"r"(ek::LT) : "memory");
         SW_JITTER_POINT();
     }
+    SW_TMARK(t_levels);
+    SW_TADD(2, t_chains, t_levels);
+    SW_TADD(5, 0, 1);
     __syncthreads();                          // with the waiting warps
     // ---- write-back of the box
     for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
