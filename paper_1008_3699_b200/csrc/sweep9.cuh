@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         qy = py + (sy ? -s9::NBY[kk] : s9::NBY[kk]);
         (void)p;
     };
+    SW_TMARK(t_start);
     // ---- stage in the old window (0 outside the domain: Dirichlet data are folded into b)
 #pragma unroll 4
     for (int e = threadIdx.x; e < WX * (T1 + 4); e += s9::NT) {
@@ -108,6 +109,8 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         XO[e] = inside(gx, gy) ? __ldg(A.xo + gidx(G, gx, gy, 0)) : 0.0;
     }
     __syncthreads();
+    SW_TMARK(t_staged);
+    SW_TADD(0, t_start, t_staged);
     // ---- explicit parts of every node of local [-1, T)^2 inside the domain (own nodes and the
     // partner layers): alpha = w / a_P, r0 = fma(alpha, b + sum_explicit c u_old, (1 - w) u_old)
     for (int e = threadIdx.x; e < AX * (T1 + 1); e += s9::NT) {
@@ -135,6 +138,8 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         AW[ai(px, py)] = al;
     }
     __syncthreads();
+    SW_TMARK(t_r0);
+    SW_TADD(1, t_staged, t_r0);
     // ---- the 8 coefficients of every node that can be in a coupled set (local x in {-1, 0} or
     // local y in {-1, 0}), into the x_old window's space (dead from here on)
     const int nslot = 2 * (T1 + 1) + 2 * (T0 - 1);
@@ -157,6 +162,8 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         CS[e] = inside(gx, gy) ? coef(kk, gx, gy) : 0.0;
     }
     __syncthreads();
+    SW_TMARK(t_cs);
+    SW_TADD(2, t_r0, t_cs);
     if (threadIdx.x >= s9::FT) {            // the other warps rejoin for the write-back
         __syncthreads();
         for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
@@ -303,6 +310,9 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         SW_JITTER_POINT();
     }
     if (fl) atomicOr(A.flag, 1);
+    SW_TMARK(t_fronts);
+    SW_TADD(3, t_cs, t_fronts);
+    SW_TADD(5, 0, 1);
     __syncthreads();                          // with the waiting warps
     for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
         const int lx = e % T0, ly = e / T0;
