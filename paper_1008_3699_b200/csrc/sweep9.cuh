@@ -238,8 +238,35 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                     }
                     return acc;
                 };
-                double m01, m10;
-                const double r0a = row(ax, ay, bx, by, m01), r0b = row(bx, by, ax, ay, m10);
+                double m01, m10, r0a, r0b;
+                if (d >= 1) {
+                    // a chain pair (d >= 1), its rows written out: besides the member across the face,
+                    // the own node's implicit neighbours are the previous chain node (along the face)
+                    // and the previous partner (diagonal), the partner's are the previous partner and
+                    // the previous chain node (diagonal); in the oracle's global neighbour order the
+                    // axis neighbour comes before the diagonal, so acc = fma(diag, ., fma(axis, ., r0))
+                    const int ox = x, oy = y;                              // own node
+                    const int dxl = xpair ? 0 : -1, dyl = xpair ? -1 : 0;  // local step back along the chain
+                    const int kax = xpair ? (sy ? 3 : 2) : (sx ? 1 : 0);   // the axis step back (S / W)
+                    const int kd_o = 4 + sx + 2 * sy;                      // own: local SW
+                    // partner: local SW seen from the other side (x-face: SE; y-face: NW)
+                    const int kd_p = xpair ? 4 + (sx ^ 1) + 2 * sy : 4 + sx + 2 * (sy ^ 1);
+                    const int kc_o = xpair ? (sx ? 1 : 0) : (sy ? 3 : 2);  // own -> partner (local W / S)
+                    const int kc_p = xpair ? (sx ? 0 : 1) : (sy ? 2 : 3);  // partner -> own (local E / N)
+                    const double al_o = AW[ai(ox, oy)], al_p = AW[ai(px2, py2)];
+                    const double *cs_o = CS + 8 * slot(ox, oy), *cs_p = CS + 8 * slot(px2, py2);
+                    const double u_op = XN[wi(ox + dxl, oy + dyl)], u_pp = XN[wi(px2 + dxl, py2 + dyl)];
+                    const double acc_o = fma(al_o * cs_o[kd_o], u_pp, fma(al_o * cs_o[kax], u_op, XN[wi(ox, oy)]));
+                    const double acc_p = fma(al_p * cs_p[kd_p], u_op, fma(al_p * cs_p[kax], u_pp, XN[wi(px2, py2)]));
+                    const double mo = -(al_o * cs_o[kc_o]), mp = -(al_p * cs_p[kc_p]);
+                    r0a = sw01 ? acc_p : acc_o;
+                    r0b = sw01 ? acc_o : acc_p;
+                    m01 = sw01 ? mp : mo;
+                    m10 = sw01 ? mo : mp;
+                } else {
+                    r0a = row(ax, ay, bx, by, m01);
+                    r0b = row(bx, by, ax, ay, m10);
+                }
                 const double inv0 = div_rn(1.0, 1.0);
                 const double l = m10 * inv0;
                 const double m11 = fma(-l, m01, 1.0);
