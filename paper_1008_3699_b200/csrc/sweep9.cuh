@@ -44,10 +44,10 @@ struct Sweep9Args {
 };
 
 // region 0: the x_old window over local [-2, T + 2), later the coupled-set coefficients (8 per node
-// of the start-face layers, 16 (T0 + T1) doubles); then (r0, later the new values) over local
+// of the start-face layers, 16 (T0 + T1) doubles) and the fronts' coefficient ring; then (r0, later the new values) over local
 // [-2, T + 2) and alpha over local [-1, T)
 __host__ __device__ inline int sweep9_r0(int T0, int T1) {
-    const int w = (T0 + 4) * (T1 + 4), c = 16 * (T0 + T1);
+    const int w = (T0 + 4) * (T1 + 4), c = 16 * (T0 + T1) + 8 * 64 * 3;   // + the coefficient ring
     return w > c ? w : c;
 }
 inline size_t sweep9_smem(const Geo &G) {
@@ -175,20 +175,36 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     const int t = threadIdx.x;
     int fl = 0;
     // implicit neighbours of an own node outside the sets: local W, S, SW, always in this order in
-    // the oracle's global neighbour order; their coefficients come two fronts ahead (a register ring)
+    // the oracle's global neighbour order.  Their coefficients arrive PD fronts ahead by cp.async
+    // into a per-thread ring in region 0 (after the set coefficients): one commit group per front
     const int kW = sx ? 1 : 0, kS = sy ? 3 : 2, kSW = 4 + sx + 2 * sy;
-    // (two named register triples, rotated: a dynamically indexed ring would live in local memory)
-    double cw0 = 0.0, cs0 = 0.0, cd0 = 0.0, cw1 = 0.0, cs1 = 0.0, cd1 = 0.0;
-    auto fetch = [&](int yy, double &a, double &b, double &c) {
+    constexpr int PD = 8;
+    double *const RING = XO + 16 * (T0 + T1);                 // [PD][LT][3]
+    auto cptr = [&](int k, int64_t gx, int64_t gy) -> const double * {   // address of coef(k, gx, gy)
+        const int dx = s9::NBX[k], dy = s9::NBY[k];
+        const int64_t cxg = gx + (dx > 0), cyg = gy + (dy > 0);
+        if (dy == 0) return A.f0 ? A.f0 + gidx(G, cxg, gy, 0) : nullptr;
+        if (dx == 0) return A.f1 ? A.f1 + gidx(G, gx, cyg, 0) : nullptr;
+        return (dx == dy ? A.dd : A.da) + gidx(G, cxg, cyg, 0);
+    };
+    auto fetch = [&](int yy) {                                 // node (t, yy) into slot yy % PD, then commit
         if (t < T0 && yy < T1) {
             const int64_t gx = gxo(t), gy = gyo(yy);
-            a = coef(kW, gx, gy);
-            b = coef(kS, gx, gy);
-            c = coef(kSW, gx, gy);
+            double *dst = RING + ((yy % PD) * s9::LT + t) * 3;
+            const int kk[3] = {kW, kS, kSW};
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double *src = cptr(kk[q], gx, gy);
+                if (src)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + q)), "l"(src) : "memory");
+                else
+                    dst[q] = 1.0;
+            }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    fetch(0, cw0, cs0, cd0);
-    fetch(1, cw1, cs1, cd1);
+    if (t < s9::LT)
+        for (int yy = 0; yy < PD; ++yy) fetch(yy);
     for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
         // fronts: threads < LT the nodes outside the coupled sets (one branch-free path); one more
         // warp the sets of the front, so the two kinds never diverge inside a warp
@@ -206,6 +222,9 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
             const int k = corner ? 4 : ((xpair || ypair) ? 2 : 1);
             if (k == 1) {
                 // (a neighbour outside the domain holds 0 and is skipped, as in the oracle)
+                asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");   // node (t, y)'s group
+                const double *cr = RING + ((y % PD) * s9::LT + t) * 3;
+                const double cw0 = cr[0], cs0 = cr[1], cd0 = cr[2];
                 const int64_t gx = gxo(x), gy = gyo(y);
                 const double al = AW[ai(x, y)];
                 double acc = XN[wi(x, y)];
@@ -329,9 +348,9 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
             }
         }
-        if (t < s9::LT && x < T0 && y >= 0 && y < T1) {   // rotate: the next triple, fetch two fronts ahead
-            cw0 = cw1; cs0 = cs1; cd0 = cd1;
-            fetch(y + 2, cw1, cs1, cd1);
+        if (t < s9::LT && x < T0 && y >= 0 && y < T1) {   // this slot is read: refill it PD rows ahead
+            if (!valid) asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");   // (keep the count)
+            fetch(y + PD);
         }
         asm volatile("bar.sync 1, %0;" ::"r"(s9::FT) : "memory");
         SW_JITTER_POINT();
