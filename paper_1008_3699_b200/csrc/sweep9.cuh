@@ -11,13 +11,19 @@
 // elimination (no pivoting, ascending global index) in neighbour order W, E, S, N, SW, SE, NW, NE:
 // bitwise equal results.
 //
-// One CTA of 256 threads per box (T0, T1 <= 64): the old values of the box and its 2-node halo in
-// shared memory in LOCAL coordinates (local +a points away from the box's start corner); all threads
-// then compute alpha and the explicit part r0 of every node of local [-1, T)^2 (own nodes and partner
-// layers) into a second window and an alpha window; front d = x + y of the own nodes: thread t < 64
-// takes node (t, d - t) unless it is on a coupled start face (its implicit neighbours are local W,
-// S, SW); a third warp solves the front's coupled sets (the x- and y-face pairs, the corner); a named
-// barrier of those 96 threads per front; write-back by all threads.  Implicit couplings are read from global memory (L1 / L2).
+// One CTA of 256 threads per box (T0, T1 <= 64), two CTAs per SM:
+//  1. the old values of the box and its 2-node halo into shared memory in LOCAL coordinates (local +a
+//     points away from the box's start corner);
+//  2. all threads: alpha and the explicit part r0 of every node of local [-1, T)^2 (own nodes and the
+//     partner layers), three nodes per thread and pass with all their global loads in flight;
+//  3. threads 0..127: per step of the two start-face chains the pair data (implicit couplings of both
+//     members, the 2 x 2 matrix in the oracle's member order and its pivot reciprocal); thread 0: the
+//     start corner (the dense 4 x 4, or a pair);
+//  4. warp 0, lanes 0 / 1: the chains of 2 x 2 systems along local row 0 / column 0 (or the plain
+//     recurrence along a physical boundary), then the whole warp: the wavefront over [1, T)^2 as in
+//     k_sweep2p -- lane l owns rows 2l+1, 2l+2, S by shfl.up, W and SW from registers, the nodes'
+//     three implicit coefficients fetched 16 steps ahead by cp.async into a per-lane ring;
+//  5. write-back by all threads.
 #pragma once
 #include "common.cuh"
 #include "sweep2p.cuh"
@@ -25,12 +31,13 @@
 namespace sw {
 
 namespace s9 {
-constexpr int NT = 256;   // threads per CTA: the prologue and write-back by all, the fronts by the first LT
-constexpr int LT = 64;    // one thread per box column (T0 <= 64): the nodes outside the coupled sets
-constexpr int FT = 96;    // threads on the fronts: LT + one warp for the coupled sets (lanes 0 / 1: the
-                          // x- / y-face pair of the front, lane 2: the corner set)
-__constant__ int NBX[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+constexpr int NT = 256;   // threads per CTA
+constexpr int PD = 16;    // wavefront coefficient ring depth (steps ahead)
+constexpr int CDW = 8;    // doubles of chain data per chain step
+__constant__ int NBX[8] = {-1, 1, 0, 0, -1, 1, -1, 1};   // global neighbour order W, E, S, N, SW, SE, NW, NE
 __constant__ int NBY[8] = {0, 0, -1, 1, -1, -1, 1, 1};
+__host__ __device__ constexpr int nbx(int k) { return k == 0 ? -1 : (k == 1 ? 1 : (k < 4 ? 0 : ((k & 1) ? 1 : -1))); }
+__host__ __device__ constexpr int nby(int k) { return k < 2 ? 0 : (k == 2 ? -1 : (k == 3 ? 1 : (k < 6 ? -1 : 1))); }
 }  // namespace s9
 
 struct Sweep9Args {
@@ -43,11 +50,11 @@ struct Sweep9Args {
     int *flag;
 };
 
-// region 0: the x_old window over local [-2, T + 2), later the coupled-set coefficients (8 per node
-// of the start-face layers, 16 (T0 + T1) doubles) and the fronts' coefficient ring; then (r0, later the new values) over local
-// [-2, T + 2) and alpha over local [-1, T)
+// region 0: the x_old window over local [-2, T + 2), after the explicit parts the chain data
+// [2][64][CDW] and the wavefront's coefficient ring [PD][32][6]; then (r0, later the new values) over
+// local [-2, T + 2) and alpha over local [-1, T)
 __host__ __device__ inline int sweep9_r0(int T0, int T1) {
-    const int w = (T0 + 4) * (T1 + 4), c = 16 * (T0 + T1) + 8 * 64 * 3;   // + the coefficient ring
+    const int w = (T0 + 4) * (T1 + 4), c = 2 * 64 * s9::CDW + s9::PD * 32 * 6;
     return w > c ? w : c;
 }
 inline size_t sweep9_smem(const Geo &G) {
@@ -56,7 +63,7 @@ inline size_t sweep9_smem(const Geo &G) {
 }
 
 inline bool sweep9_supported(const Geo &G) {
-    return G.dim == 2 && G.T[0] <= s9::LT && G.T[1] <= s9::LT && sweep9_smem(G) <= 227 * 1024;
+    return G.dim == 2 && G.T[0] <= 64 && G.T[1] <= 64 && sweep9_smem(G) <= 227 * 1024;
 }
 
 __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
@@ -112,254 +119,304 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     SW_TMARK(t_staged);
     SW_TADD(0, t_start, t_staged);
     // ---- explicit parts of every node of local [-1, T)^2 inside the domain (own nodes and the
-    // partner layers): alpha = w / a_P, r0 = fma(alpha, b + sum_explicit c u_old, (1 - w) u_old)
-    for (int e = threadIdx.x; e < AX * (T1 + 1); e += s9::NT) {
-        const int px = e % AX - 1, py = e / AX - 1;
-        const int64_t gx = gxo(px), gy = gyo(py);
-        if (!inside(gx, gy)) continue;
-        double c8[8];
+    // partner layers): alpha = w / a_P, r0 = fma(alpha, b + sum_explicit c u_old, (1 - w) u_old).
+    // Three nodes per thread and pass, all 27 of their global loads issued before any use.
+    {
+        const int NA = AX * (T1 + 1);
+        const int64_t ng0 = G.ng[0], ng1 = G.ng[1], P0 = G.P0;
+        for (int e0 = threadIdx.x; e0 < NA; e0 += 3 * s9::NT) {
+            double c8[3][8], bv[3];
+            int px[3], py[3];
+            int64_t gx[3], gy[3];
+            bool ok[3];
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) c8[kk] = coef(kk, gx, gy);
-        const double bv = __ldg(A.b + gidx(G, gx, gy, 0));
-        const double ap = ((c8[0] + c8[1]) + (c8[2] + c8[3])) + ((c8[4] + c8[7]) + (c8[5] + c8[6])) + G.beta;
-        const int bits = (sx ^ (px < 0 ? 1 : 0)) | ((sy ^ (py < 0 ? 1 : 0)) << 1);
-        const double w = A.omega[bits];
-        const double al = div_rn(w, ap);
-        double ev = bv;
+            for (int u = 0; u < 3; ++u) {
+                const int e = e0 + u * s9::NT;
+                px[u] = e % AX - 1;
+                py[u] = e / AX - 1;
+                gx[u] = gxo(px[u]);
+                gy[u] = gyo(py[u]);
+                ok[u] = e < NA && inside(gx[u], gy[u]);
+                // coefficient of global neighbour k (coef(), R-N3): faces at the node (W, S) or
+                // one step up (E, N), diagonals at the cell corners
+                const int64_t i = ok[u] ? gidx(G, gx[u], gy[u], 0) : G.origin;
+                c8[u][0] = A.f0 ? __ldg(A.f0 + i) : 1.0;
+                c8[u][1] = A.f0 ? __ldg(A.f0 + i + 1) : 1.0;
+                c8[u][2] = A.f1 ? __ldg(A.f1 + i) : 1.0;
+                c8[u][3] = A.f1 ? __ldg(A.f1 + i + P0) : 1.0;
+                c8[u][4] = __ldg(A.dd + i);
+                c8[u][5] = __ldg(A.da + i + 1);
+                c8[u][6] = __ldg(A.da + i + P0);
+                c8[u][7] = __ldg(A.dd + i + 1 + P0);
+                bv[u] = __ldg(A.b + i);
+            }
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
-            int qx, qy;
-            lnb(0, kk, qx, qy, px, py);
-            if (implicit(px, py, qx, qy)) continue;
-            ev = fma(c8[kk], XO[wi(qx, qy)], ev);
+            for (int u = 0; u < 3; ++u) {
+                if (!ok[u]) continue;
+                const double *c = c8[u];
+                const double ap = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[7]) + (c[5] + c[6])) + G.beta;
+                const int bx = px[u] < 0, by = py[u] < 0;   // partner layers: the neighbour box starts toward ours
+                const double w = A.omega[(sx ^ bx) | ((sy ^ by) << 1)];
+                const double al = div_rn(w, ap);
+                const bool xm = gx[u] > 0, xp = gx[u] + 1 < ng0, ym = gy[u] > 0, yp = gy[u] + 1 < ng1;
+                const int sdx = bx ? 1 : -1, sdy = by ? 1 : -1;   // local start side of the node's box
+                double ev = bv[u];
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int dx = s9::nbx(kk), dy = s9::nby(kk);
+                    const bool in = (dx < 0 ? xm : (dx > 0 ? xp : true)) && (dy < 0 ? ym : (dy > 0 ? yp : true));
+                    const int ldx = sx ? -dx : dx, ldy = sy ? -dy : dy;
+                    const bool imp = (dx == 0 || ldx == sdx) && (dy == 0 || ldy == sdy);
+                    if (in && !imp) ev = fma(c[kk], XO[wi(px[u] + ldx, py[u] + ldy)], ev);
+                }
+                XN[wi(px[u], py[u])] = fma(al, ev, (1.0 - w) * XO[wi(px[u], py[u])]);
+                AW[ai(px[u], py[u])] = al;
+            }
         }
-        XN[wi(px, py)] = fma(al, ev, (1.0 - w) * XO[wi(px, py)]);
-        AW[ai(px, py)] = al;
     }
     __syncthreads();
     SW_TMARK(t_r0);
     SW_TADD(1, t_staged, t_r0);
-    // ---- the 8 coefficients of every node that can be in a coupled set (local x in {-1, 0} or
-    // local y in {-1, 0}), into the x_old window's space (dead from here on)
-    const int nslot = 2 * (T1 + 1) + 2 * (T0 - 1);
-    double *const CS = XO;
-    auto slot = [&](int lx, int ly) {
-        return lx <= 0 ? (lx + 1) * (T1 + 1) + (ly + 1) : 2 * (T1 + 1) + (ly + 1) * (T0 - 1) + (lx - 1);
-    };
-    for (int e = threadIdx.x; e < nslot * 8; e += s9::NT) {
-        const int sl = e >> 3, kk = e & 7;
-        int lx, ly;
-        if (sl < 2 * (T1 + 1)) {
-            lx = sl / (T1 + 1) - 1;
-            ly = sl % (T1 + 1) - 1;
-        } else {
-            const int r = sl - 2 * (T1 + 1);
-            lx = r % (T0 - 1) + 1;
-            ly = r / (T0 - 1) - 1;
-        }
-        const int64_t gx = gxo(lx), gy = gyo(ly);
-        CS[e] = inside(gx, gy) ? coef(kk, gx, gy) : 0.0;
-    }
-    __syncthreads();
-    SW_TMARK(t_cs);
-    SW_TADD(2, t_r0, t_cs);
-    if (threadIdx.x >= s9::FT) {            // the other warps rejoin for the write-back
-        __syncthreads();
-        for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
-            const int lx = e % T0, ly = e / T0;
-            A.xn[gidx(G, gxo(lx), gyo(ly), 0)] = XN[wi(lx, ly)];
-        }
-        return;
-    }
-    const int t = threadIdx.x;
-    int fl = 0;
-    // implicit neighbours of an own node outside the sets: local W, S, SW, always in this order in
-    // the oracle's global neighbour order.  Their coefficients arrive PD fronts ahead by cp.async
-    // into a per-thread ring in region 0 (after the set coefficients): one commit group per front
-    const int kW = sx ? 1 : 0, kS = sy ? 3 : 2, kSW = 4 + sx + 2 * sy;
-    constexpr int PD = 8;
-    double *const RING = XO + 16 * (T0 + T1);                 // [PD][LT][3]
-    auto cptr = [&](int k, int64_t gx, int64_t gy) -> const double * {   // address of coef(k, gx, gy)
-        const int dx = s9::NBX[k], dy = s9::NBY[k];
-        const int64_t cxg = gx + (dx > 0), cyg = gy + (dy > 0);
-        if (dy == 0) return A.f0 ? A.f0 + gidx(G, cxg, gy, 0) : nullptr;
-        if (dx == 0) return A.f1 ? A.f1 + gidx(G, gx, cyg, 0) : nullptr;
-        return (dx == dy ? A.dd : A.da) + gidx(G, cxg, cyg, 0);
-    };
-    auto fetch = [&](int yy) {                                 // node (t, yy) into slot yy % PD, then commit
-        if (t < T0 && yy < T1) {
-            const int64_t gx = gxo(t), gy = gyo(yy);
-            double *dst = RING + ((yy % PD) * s9::LT + t) * 3;
-            const int kk[3] = {kW, kS, kSW};
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const double *src = cptr(kk[q], gx, gy);
-                if (src)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + q)), "l"(src) : "memory");
-                else
-                    dst[q] = 1.0;
+    // ---- region 0 is dead from here on: the chain data and the wavefront's coefficient ring
+    double *const CD = XO;                                     // [2][64][CDW]
+    double *const RING = XO + 2 * 64 * s9::CDW;                // [PD][32][6]
+    const int lane = threadIdx.x & 31;
+    // wavefront geometry (warp 0): lane l owns rows A = 2l + 1 and B = 2l + 2 (local y) and at step
+    // s updates column x = s - l + 1 of both; rows >= T1 do not exist
+    const int rA = 2 * lane + 1, rB = rA + 1;
+    const bool onA = rA < T1, onB = rB < T1;
+    const int rAl = onA ? rA : T1 - 1, rBl = onB ? rB : (T1 > 1 ? T1 - 1 : 0);
+    // the implicit couplings of a wavefront node are local W, S, SW (global kW, kS, kSW: in the
+    // oracle's neighbour order always in this order); their coefficients arrive PD steps ahead by
+    // cp.async into a per-lane ring, one commit group per step
+    const int64_t P0 = G.P0;
+    const int sgx = sx ? -1 : 1;
+    const int64_t iA = gidx(G, gxo(0), gyo(rAl), 0), iB = gidx(G, gxo(0), gyo(rBl), 0);
+    const double *const fdg = (sx == sy) ? A.dd : A.da;
+    auto fetch = [&](int s) {
+        const int x = s - lane + 1;
+        if (threadIdx.x < 32 && onA && x >= 1 && x < T0) {
+            double *dst = RING + ((s % s9::PD) * 32 + lane) * 6;
+            const int64_t ia = iA + sgx * x, ib = iB + sgx * x;
+            auto cpa = [&](double *d, const double *src) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(src) : "memory");
+            };
+            if (A.f0) cpa(dst + 0, A.f0 + ia + sx); else dst[0] = 1.0;
+            if (A.f1) cpa(dst + 1, A.f1 + ia + sy * P0); else dst[1] = 1.0;
+            cpa(dst + 2, fdg + ia + sx + sy * P0);
+            if (onB) {
+                if (A.f0) cpa(dst + 3, A.f0 + ib + sx); else dst[3] = 1.0;
+                if (A.f1) cpa(dst + 4, A.f1 + ib + sy * P0); else dst[4] = 1.0;
+                cpa(dst + 5, fdg + ib + sx + sy * P0);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (t < s9::LT)
-        for (int yy = 0; yy < PD; ++yy) fetch(yy);
-    for (int d = 0; d <= (T0 - 1) + (T1 - 1); ++d) {
-        // fronts: threads < LT the nodes outside the coupled sets (one branch-free path); one more
-        // warp the sets of the front, so the two kinds never diverge inside a warp
-        const int x = t < s9::LT ? t : ((t - s9::LT) == 1 ? d : 0);
-        const int y = t < s9::LT ? d - t : ((t - s9::LT) == 1 ? 0 : d);
-        const bool member = (x == 0 && cx) || (y == 0 && cy);
-        const int lane = t - s9::LT;
-        const bool valid = x < T0 && y >= 0 && y < T1 &&
-                           (t < s9::LT ? !member
-                                       : (lane == 0 ? (cx && !(d == 0 && cy))
-                                                    : (lane == 1 ? (cy && !(d == 0 && cx)) : (lane == 2 && d == 0 && cx && cy))));
-        if (valid) {
-            const bool corner = x == 0 && y == 0 && cx && cy;
-            const bool xpair = !corner && x == 0 && cx, ypair = !corner && !xpair && y == 0 && cy;
-            const int k = corner ? 4 : ((xpair || ypair) ? 2 : 1);
-            if (k == 1) {
-                // (a neighbour outside the domain holds 0 and is skipped, as in the oracle)
-                asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");   // node (t, y)'s group
-                const double *cr = RING + ((y % PD) * s9::LT + t) * 3;
-                const double cw0 = cr[0], cs0 = cr[1], cd0 = cr[2];
-                const int64_t gx = gxo(x), gy = gyo(y);
-                const double al = AW[ai(x, y)];
-                double acc = XN[wi(x, y)];
-                if (inside(gx + s9::NBX[kW], gy)) acc = fma(al * cw0, XN[wi(x - 1, y)], acc);
-                if (inside(gx, gy + s9::NBY[kS])) acc = fma(al * cs0, XN[wi(x, y - 1)], acc);
-                if (inside(gx + s9::NBX[kSW], gy + s9::NBY[kSW])) acc = fma(al * cd0, XN[wi(x - 1, y - 1)], acc);
-                XN[wi(x, y)] = acc;
-            } else if (k == 2) {
-                // a pair across one coupled start face, in registers: members in ascending global
-                // index, rows (1, -m01; -m10, 1), the oracle's ge_solve for K = 2 written out
-                const int px2 = xpair ? -1 : x, py2 = xpair ? y : -1;
-                const bool sw01 = gyo(py2) * G.ng[0] + gxo(px2) < gyo(y) * G.ng[0] + gxo(x);
-                const int ax = sw01 ? px2 : x, ay = sw01 ? py2 : y;
-                const int bx = sw01 ? x : px2, by = sw01 ? y : py2;
-                auto row = [&](int px, int py, int ox, int oy, double &moff) {
-                    const int64_t gx = gxo(px), gy = gyo(py);
-                    const double al = AW[ai(px, py)];
-                    const double *cs = CS + 8 * slot(px, py);
-                    double acc = XN[wi(px, py)];
-                    moff = 0.0;
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
-                        int qx, qy;
-                        lnb(0, kk, qx, qy, px, py);
-                        if (!implicit(px, py, qx, qy)) continue;
-                        const double m = al * cs[kk];
-                        if (qx == ox && qy == oy) moff = -m;
-                        else acc = fma(m, XN[wi(qx, qy)], acc);
-                    }
-                    return acc;
-                };
-                double m01, m10, r0a, r0b;
-                if (d >= 1) {
-                    // a chain pair (d >= 1), its rows written out: besides the member across the face,
-                    // the own node's implicit neighbours are the previous chain node (along the face)
-                    // and the previous partner (diagonal), the partner's are the previous partner and
-                    // the previous chain node (diagonal); in the oracle's global neighbour order the
-                    // axis neighbour comes before the diagonal, so acc = fma(diag, ., fma(axis, ., r0))
-                    const int ox = x, oy = y;                              // own node
-                    const int dxl = xpair ? 0 : -1, dyl = xpair ? -1 : 0;  // local step back along the chain
-                    const int kax = xpair ? (sy ? 3 : 2) : (sx ? 1 : 0);   // the axis step back (S / W)
-                    const int kd_o = 4 + sx + 2 * sy;                      // own: local SW
-                    // partner: local SW seen from the other side (x-face: SE; y-face: NW)
-                    const int kd_p = xpair ? 4 + (sx ^ 1) + 2 * sy : 4 + sx + 2 * (sy ^ 1);
-                    const int kc_o = xpair ? (sx ? 1 : 0) : (sy ? 3 : 2);  // own -> partner (local W / S)
-                    const int kc_p = xpair ? (sx ? 0 : 1) : (sy ? 2 : 3);  // partner -> own (local E / N)
-                    const double al_o = AW[ai(ox, oy)], al_p = AW[ai(px2, py2)];
-                    const double *cs_o = CS + 8 * slot(ox, oy), *cs_p = CS + 8 * slot(px2, py2);
-                    const double u_op = XN[wi(ox + dxl, oy + dyl)], u_pp = XN[wi(px2 + dxl, py2 + dyl)];
-                    const double acc_o = fma(al_o * cs_o[kd_o], u_pp, fma(al_o * cs_o[kax], u_op, XN[wi(ox, oy)]));
-                    const double acc_p = fma(al_p * cs_p[kd_p], u_op, fma(al_p * cs_p[kax], u_pp, XN[wi(px2, py2)]));
-                    const double mo = -(al_o * cs_o[kc_o]), mp = -(al_p * cs_p[kc_p]);
-                    r0a = sw01 ? acc_p : acc_o;
-                    r0b = sw01 ? acc_o : acc_p;
-                    m01 = sw01 ? mp : mo;
-                    m10 = sw01 ? mo : mp;
-                } else {
-                    r0a = row(ax, ay, bx, by, m01);
-                    r0b = row(bx, by, ax, ay, m10);
-                }
-                const double inv0 = div_rn(1.0, 1.0);
-                const double l = m10 * inv0;
-                const double m11 = fma(-l, m01, 1.0);
-                const double rb = fma(-l, r0a, r0b);
+    if (threadIdx.x < 32)
+        for (int s = 0; s < s9::PD; ++s) fetch(s);
+    int fl = 0;
+    // ---- the chain data (threads 0..127, item (chain, k)): chain 0 = local row 0 (node (k, 0),
+    // partner (k, -1) across the y start face), chain 1 = local column 0 (node (0, k), partner
+    // (-1, k)).  Besides the member across the face, the own node's implicit neighbours are the
+    // previous chain node (axis) and the previous partner (diagonal), the partner's the previous
+    // partner (axis) and the previous chain node (diagonal); in the oracle's neighbour order the
+    // axis term comes first.  Stored: m_ax, m_d of both, the pair matrix (1, -m01; -m10, 1) in
+    // ascending global index and its second pivot's reciprocal (the oracle's ge_solve for K = 2:
+    // the first pivot is 1).  An uncoupled face (physical boundary) leaves the plain recurrence
+    // along the chain (the other implicit neighbours lie outside the domain).
+    if (threadIdx.x < 128) {
+        const int ch = threadIdx.x >> 6, k = threadIdx.x & 63;
+        const bool cpl = ch == 0 ? cy : cx;
+        const int len = ch == 0 ? T0 : T1;
+        if (k >= 1 && k < len) {
+            const int ox = ch == 0 ? k : 0, oy = ch == 0 ? 0 : k;
+            const int kax = ch == 0 ? (sx ? 1 : 0) : (sy ? 3 : 2);        // local W / S
+            const int64_t gox = gxo(ox), goy = gyo(oy);
+            const double al_o = AW[ai(ox, oy)];
+            double *cd = CD + (ch * 64 + k) * s9::CDW;
+            cd[0] = al_o * coef(kax, gox, goy);
+            if (cpl) {
+                const int qx = ch == 0 ? k : -1, qy = ch == 0 ? -1 : k;
+                const int kd_o = 4 + sx + 2 * sy;                             // own: local SW
+                // partner: local SW seen from the other side (row chain: NW; column chain: SE)
+                const int kd_p = ch == 1 ? 4 + (sx ^ 1) + 2 * sy : 4 + sx + 2 * (sy ^ 1);
+                const int kc_o = ch == 1 ? (sx ? 1 : 0) : (sy ? 3 : 2);      // own -> partner (local W / S)
+                const int kc_p = ch == 1 ? (sx ? 0 : 1) : (sy ? 2 : 3);      // partner -> own (local E / N)
+                const int64_t gqx = gxo(qx), gqy = gyo(qy);
+                const double al_p = AW[ai(qx, qy)];
+                cd[1] = al_o * coef(kd_o, gox, goy);
+                cd[2] = al_p * coef(kax, gqx, gqy);
+                cd[3] = al_p * coef(kd_p, gqx, gqy);
+                const double mo = -(al_o * coef(kc_o, gox, goy)), mp = -(al_p * coef(kc_p, gqx, gqy));
+                const bool pfirst = ch == 0 ? (sy == 0) : (sx == 0);          // partner before own
+                const double m01 = pfirst ? mp : mo, m10 = pfirst ? mo : mp;
+                const double m11 = fma(-m10, m01, 1.0);                       // l = m10 / 1
                 fl |= !(fabs(m11) >= 1e-14);
-                const double inv1 = div_rn(1.0, m11);
-                const double ub = rb * inv1;
-                const double ua = fma(-m01, ub, r0a) * inv0;
-                XN[wi(ax, ay)] = ua;
-                XN[wi(bx, by)] = ub;
+                cd[4] = m01;
+                cd[5] = m10;
+                cd[6] = div_rn(1.0, m11);
             } else {
-                // the corner set: the four start-corner nodes, a dense 4 x 4 (once per box)
-                int mx[4] = {0, -1, 0, -1}, my[4] = {0, 0, -1, -1};
-                int64_t gi[4];
-                for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
-                for (int a1 = 1; a1 < k; ++a1)
-                    for (int b1 = a1; b1 > 0 && gi[b1 - 1] > gi[b1]; --b1) {
-                        int64_t tg = gi[b1]; gi[b1] = gi[b1 - 1]; gi[b1 - 1] = tg;
-                        int tt = mx[b1]; mx[b1] = mx[b1 - 1]; mx[b1 - 1] = tt;
-                        tt = my[b1]; my[b1] = my[b1 - 1]; my[b1 - 1] = tt;
-                    }
-                double M[4][4], rhs[4], u[4];
-                for (int p = 0; p < k; ++p) {
-                    const int px = mx[p], py = my[p];
-                    const int64_t gx = gxo(px), gy = gyo(py);
-                    const double al = AW[ai(px, py)];
-                    double acc = XN[wi(px, py)];
-                    for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
-                    const double *cs = CS + 8 * slot(px, py);
-                    for (int kk = 0; kk < 8; ++kk) {
-                        if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
-                        int qx, qy;
-                        lnb(0, kk, qx, qy, px, py);
-                        if (!implicit(px, py, qx, qy)) continue;
-                        const double m = al * cs[kk];
-                        int in = -1;
-                        for (int q = 0; q < k; ++q)
-                            if (mx[q] == qx && my[q] == qy) in = q;
-                        if (in >= 0) M[p][in] = -m;
-                        else acc = fma(m, XN[wi(qx, qy)], acc);
-                    }
-                    rhs[p] = acc;
-                }
-                double inv[4];                             // the oracle's ge_solve (R-8)
-                for (int p = 0; p < k; ++p) {
-                    const double piv = M[p][p];
-                    fl |= !(fabs(piv) >= 1e-14);
-                    inv[p] = div_rn(1.0, piv);
-                    for (int q = p + 1; q < k; ++q) {
-                        const double l = M[q][p] * inv[p];
-                        for (int j = p + 1; j < k; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
-                        rhs[q] = fma(-l, rhs[p], rhs[q]);
-                    }
-                }
-                for (int p = k - 1; p >= 0; --p) {
-                    double sacc = rhs[p];
-                    for (int j = p + 1; j < k; ++j) sacc = fma(-M[p][j], u[j], sacc);
-                    u[p] = sacc * inv[p];
-                }
-                for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
+                cd[1] = cd[2] = cd[3] = cd[4] = cd[5] = 0.0;
+                cd[6] = 1.0;
             }
         }
-        if (t < s9::LT && x < T0 && y >= 0 && y < T1) {   // this slot is read: refill it PD rows ahead
-            if (!valid) asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");   // (keep the count)
-            fetch(y + PD);
+    }
+    // ---- the start corner (thread 0): the dense 4 x 4 set, a pair across the one coupled face,
+    // or a single node without implicit neighbours in the domain (u = r0, nothing to do)
+    if (threadIdx.x == 0 && (cx || cy)) {
+        if (cx && cy) {
+            constexpr int k = 4;
+            int mx[4] = {0, -1, 0, -1}, my[4] = {0, 0, -1, -1};
+            int64_t gi[4];
+            for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
+            for (int a1 = 1; a1 < k; ++a1)
+                for (int b1 = a1; b1 > 0 && gi[b1 - 1] > gi[b1]; --b1) {
+                    int64_t tg = gi[b1]; gi[b1] = gi[b1 - 1]; gi[b1 - 1] = tg;
+                    int tt = mx[b1]; mx[b1] = mx[b1 - 1]; mx[b1 - 1] = tt;
+                    tt = my[b1]; my[b1] = my[b1 - 1]; my[b1 - 1] = tt;
+                }
+            double M[4][4], rhs[4], u[4];
+            for (int p = 0; p < k; ++p) {
+                const int px = mx[p], py = my[p];
+                const int64_t gx = gxo(px), gy = gyo(py);
+                const double al = AW[ai(px, py)];
+                double acc = XN[wi(px, py)];
+                for (int q = 0; q < k; ++q) M[p][q] = (p == q) ? 1.0 : 0.0;
+                for (int kk = 0; kk < 8; ++kk) {
+                    if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
+                    int qx, qy;
+                    lnb(0, kk, qx, qy, px, py);
+                    if (!implicit(px, py, qx, qy)) continue;
+                    const double m = al * coef(kk, gx, gy);
+                    int in = -1;
+                    for (int q = 0; q < k; ++q)
+                        if (mx[q] == qx && my[q] == qy) in = q;
+                    if (in >= 0) M[p][in] = -m;
+                    else acc = fma(m, XN[wi(qx, qy)], acc);
+                }
+                rhs[p] = acc;
+            }
+            double inv[4];                             // the oracle's ge_solve (R-8)
+            for (int p = 0; p < k; ++p) {
+                const double piv = M[p][p];
+                fl |= !(fabs(piv) >= 1e-14);
+                inv[p] = div_rn(1.0, piv);
+                for (int q = p + 1; q < k; ++q) {
+                    const double l = M[q][p] * inv[p];
+                    for (int j = p + 1; j < k; ++j) M[q][j] = fma(-l, M[p][j], M[q][j]);
+                    rhs[q] = fma(-l, rhs[p], rhs[q]);
+                }
+            }
+            for (int p = k - 1; p >= 0; --p) {
+                double sacc = rhs[p];
+                for (int j = p + 1; j < k; ++j) sacc = fma(-M[p][j], u[j], sacc);
+                u[p] = sacc * inv[p];
+            }
+            for (int m = 0; m < k; ++m) XN[wi(mx[m], my[m])] = u[m];
+        } else {
+            // a pair across one coupled start face: members in ascending global index, rows
+            // (1, -m01; -m10, 1), the oracle's ge_solve for K = 2 written out
+            const int px2 = cx ? -1 : 0, py2 = cx ? 0 : -1;
+            const bool sw01 = gyo(py2) * G.ng[0] + gxo(px2) < gyo(0) * G.ng[0] + gxo(0);
+            const int ax = sw01 ? px2 : 0, ay = sw01 ? py2 : 0;
+            const int bx = sw01 ? 0 : px2, by = sw01 ? 0 : py2;
+            auto row = [&](int px, int py, int ox, int oy, double &moff) {
+                const int64_t gx = gxo(px), gy = gyo(py);
+                const double al = AW[ai(px, py)];
+                double acc = XN[wi(px, py)];
+                moff = 0.0;
+                for (int kk = 0; kk < 8; ++kk) {
+                    if (!inside(gx + s9::NBX[kk], gy + s9::NBY[kk])) continue;
+                    int qx, qy;
+                    lnb(0, kk, qx, qy, px, py);
+                    if (!implicit(px, py, qx, qy)) continue;
+                    const double m = al * coef(kk, gx, gy);
+                    if (qx == ox && qy == oy) moff = -m;
+                    else acc = fma(m, XN[wi(qx, qy)], acc);
+                }
+                return acc;
+            };
+            double m01, m10;
+            const double r0a = row(ax, ay, bx, by, m01);
+            const double r0b = row(bx, by, ax, ay, m10);
+            const double m11 = fma(-m10, m01, 1.0);
+            fl |= !(fabs(m11) >= 1e-14);
+            const double ub = fma(-m10, r0a, r0b) * div_rn(1.0, m11);
+            XN[wi(ax, ay)] = fma(-m01, ub, r0a);
+            XN[wi(bx, by)] = ub;
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(s9::FT) : "memory");
+    }
+    __syncthreads();
+    SW_TMARK(t_cs);
+    SW_TADD(2, t_r0, t_cs);
+    if (threadIdx.x < 32) {
+        // ---- the two start-face chains (lane 0: row 0, lane 1: column 0), then the wavefront
+        if (lane < 2) {
+            const int ch = lane;
+            const bool cpl = ch == 0 ? cy : cx;
+            const int len = ch == 0 ? T0 : T1;
+            const bool pfirst = ch == 0 ? (sy == 0) : (sx == 0);
+            const int so = ch == 0 ? 1 : WX, sp = ch == 0 ? -WX : -1;   // window strides along / across
+            double *const xc = XN + wi(0, 0);
+            double u_op = xc[0], u_pp = cpl ? xc[sp] : 0.0;             // the corner's results
+            const double *cd = CD + ch * 64 * s9::CDW;
+            for (int k = 1; k < len; ++k) {
+                cd += s9::CDW;
+                const double r0o = xc[k * so], r0p = cpl ? xc[k * so + sp] : 0.0;
+                const double in_o = fma(cd[0], u_op, r0o);
+                const double acc_o = fma(cd[1], u_pp, in_o);
+                const double acc_p = fma(cd[3], u_op, fma(cd[2], u_pp, r0p));
+                const double r0a = pfirst ? acc_p : acc_o, r0b = pfirst ? acc_o : acc_p;
+                const double ub = fma(-cd[5], r0a, r0b) * cd[6];
+                const double ua = fma(-cd[4], ub, r0a);
+                const double uo = cpl ? (pfirst ? ub : ua) : in_o;
+                u_pp = pfirst ? ua : ub;
+                u_op = uo;
+                xc[k * so] = uo;
+            }
+        }
+        __syncwarp();
         SW_JITTER_POINT();
+        // ---- the wavefront over local [1, T0) x [1, T1):
+        //   u_A = fma(m_SW, SW_A, fma(m_S, S, fma(m_W, W_A, r0_A))),
+        //   u_B = fma(m_SW, W_A, fma(m_S, u_A, fma(m_W, W_B, r0_B)))
+        // W from the lane's registers, S = u_B of lane l - 1 by shfl.up (lane 0: row 0), SW = the
+        // previous step's S (A) or W_A (B); in place, branch-free (idle lanes of the ramps only
+        // predicate their stores and keep their column-0 values)
+        if (T0 > 1 && T1 > 1) {
+            const int nl = T1 / 2;                                     // lanes with a row
+            const int NSTEP = (T0 - 1) + (nl - 1);
+            double WA = XN[wi(0, rAl)], WB = XN[wi(0, rBl)], SWA = XN[wi(0, rAl - 1)];
+            double uBp = 0.0;
+            for (int s = 0; s < NSTEP; ++s) {
+                const int x = s - lane + 1;
+                const bool act = onA && x >= 1 && x < T0;
+                const int xl = x < 1 ? 1 : (x >= T0 ? T0 - 1 : x);
+                asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 1) : "memory");
+                const double *cr = RING + ((s % s9::PD) * 32 + lane) * 6;
+                const double aA = AW[ai(xl, rAl)], aB = AW[ai(xl, rBl)];
+                const double mWA = aA * cr[0], mSA = aA * cr[1], mDA = aA * cr[2];
+                const double mWB = aB * cr[3], mSB = aB * cr[4], mDB = aB * cr[5];
+                const double r0A = XN[wi(xl, rAl)], r0B = XN[wi(xl, rBl)], row0 = XN[wi(xl, 0)];
+                const double S = sel_f64(lane == 0, row0, shfl_up1_f64(uBp));
+                const double uA = fma(mDA, SWA, fma(mSA, S, fma(mWA, WA, r0A)));
+                const double uB = fma(mDB, WA, fma(mSB, uA, fma(mWB, WB, r0B)));
+                st_shared_if(XN + wi(xl, rAl), uA, act);
+                st_shared_if(XN + wi(xl, rBl), uB, act && onB);
+                SWA = sel_f64(act, S, SWA);
+                WA = sel_f64(act, uA, WA);
+                WB = sel_f64(act, uB, WB);
+                uBp = uB;
+                fetch(s + s9::PD);                                     // this lane's slot is consumed
+            }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     if (fl) atomicOr(A.flag, 1);
     SW_TMARK(t_fronts);
     SW_TADD(3, t_cs, t_fronts);
     SW_TADD(5, 0, 1);
-    __syncthreads();                          // with the waiting warps
+    __syncthreads();
     for (int e = threadIdx.x; e < T0 * T1; e += s9::NT) {
         const int lx = e % T0, ly = e / T0;
         A.xn[gidx(G, gxo(lx), gyo(ly), 0)] = XN[wi(lx, ly)];
