@@ -499,10 +499,21 @@ def run_secondary(args):
     t0 = time.perf_counter()
     while ge.eikonal_changes() > 0 and ph < 4000:
         ph = ge.eikonal_sweep(8, ph)
+    t_fix = time.perf_counter() - t0
+    # the same passes once every box has been reached (the full per-node work: no box is skipped as
+    # all +inf)
+    torch.cuda.synchronize()
+    e0.record()
+    ge.eikonal_sweep(8, ph)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_all = e0.elapsed_time(e1) / 8
     out["n4_eikonal"] = {"n": [n, n], "tile": [64, 64], "ms_per_pass": round(ms, 4),
                          "glups": round(n * n / (ms * 1e-3) / 1e9, 2), "algorithmic_B_per_lup": 24,
                          "frac_of_measured_hbm": round(24 * n * n / (ms * 1e-3) / 1e9 / peaks()[0], 3),
-                         "passes_to_fixed_point": ph, "seconds_to_fixed_point": round(time.perf_counter() - t0, 3)}
+                         "ms_per_pass_all_reached": round(ms_all, 4),
+                         "glups_all_reached": round(n * n / (ms_all * 1e-3) / 1e9, 2),
+                         "passes_to_fixed_point": ph, "seconds_to_fixed_point": round(t_fix, 3)}
     del ge, u0
     # ---- config 1: 1D Poisson n = 1024, 4 boxes, SOR at omega_opt until relres < 1e-8
     n1 = 1024

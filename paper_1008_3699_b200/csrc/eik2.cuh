@@ -8,20 +8,23 @@
 // One CTA of 256 threads per box (T0, T1 <= 64).  All threads stage in the old values of the box and
 // its 2-node halo in LOCAL coordinates (local +a points away from the box's start corner; a node
 // outside the domain reads +inf) and the slowness of the active nodes (own and partner layers).
-// Thread 0 solves the corner set, then threads 0 and 1 run the two start-face chains (row 0 with
-// its partner row, column 0 with its partner column: pairs by ordered fixing, or plain updates
-// along an uncoupled face); then level d = x + y of the other own nodes: thread t < 64 takes node
-// (t, d - t) directly from the window; results go in place (the window then holds new values on
-// every node's start side and old values on its end side, exactly the split the method
-// prescribes); a named barrier of the 64 level threads per level; write-back by all threads.
+// Warp 0 then: thread 0 solves the corner set; lanes 0 and 1 run the two start-face chains (row 0
+// with its partner row, column 0 with its partner column: pairs by ordered fixing, or plain updates
+// along an uncoupled face), branch-free with their window operands loaded a step ahead; then the
+// other own nodes as a register wavefront (lane l owns rows 2l+1 and 2l+2, the second one column
+// behind the first so that the two are independent; S by shfl.up, W from registers, E and N old
+// from the window).  Results go in place (the window then holds new values on every node's start
+// side and old values on its end side, exactly the split the method prescribes); write-back by all
+// threads.
 #pragma once
 #include "common.cuh"
+#include "sweep2p.cuh"
 
 namespace sw {
 
 namespace ek {
 constexpr int NT = 256;   // threads per CTA: stage-in / write-back by all, the levels by the first LT
-constexpr int LT = 64;    // one thread per box column (T0 <= 64)
+constexpr int LT = 64;    // the levels: one thread per box column (T0 <= 64)
 }
 
 struct Eik2Args {
@@ -50,7 +53,7 @@ inline size_t eik2_smem(const Geo &G) {
 }
 
 inline bool eik2_supported(const Geo &G) {
-    return G.dim == 2 && G.T[0] <= ek::LT && G.T[1] <= ek::LT && eik2_smem(G) <= 227 * 1024;
+    return G.dim == 2 && G.T[0] <= 64 && G.T[1] <= 64 && eik2_smem(G) <= 227 * 1024;
 }
 
 __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
     SW_TMARK(t_start);
     // ---- stage in (old values, +inf outside the domain; slowness of the active region): warp w
     //      takes local rows w, w + 8, ..., lanes along x (consecutive addresses in either direction)
+    int finite = 0;   // some old value of the window is finite
     {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const int nrow = T1 + 4;
@@ -99,13 +103,25 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
             for (int c = 0; c < 3; ++c) {
                 const int lx = lane + 32 * c - 2;
                 if (lx < T0 + 2) U[r * WX + (lx + 2)] = uv[c];
+                finite |= uv[c] != eik_inf();
                 if (yact && lx >= -1 && lx < T0) F[(ly + 1) * FX + (lx + 1)] = sv[c];
             }
         }
     }
-    __syncthreads();
+    // a box whose whole window is +inf (not reached by the front yet) stays +inf: every Godunov
+    // update of it sees +inf neighbours only (R-E1: u = +inf if min(a, b) = +inf), so it is copied
+    // through unchanged -- exactly the oracle's result
+    const bool reached = __syncthreads_or(finite);
     SW_TMARK(t_staged);
     SW_TADD(0, t_start, t_staged);
+    if (!reached) {
+        for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
+            const int lx = e % T0, ly = e / T0;
+            A.un[gidx(G, gxo(lx), gyo(ly), 0)] = eik_inf();
+        }
+        SW_TADD(5, 0, 1);
+        return;
+    }
     if (threadIdx.x >= ek::LT) {           // the other warps rejoin for the write-back
         __syncthreads();
         for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
@@ -152,112 +168,110 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
     //      with its partner column), then the rest of the box level by level.  Any causal order
     //      gives the oracle's values (every node reads new values only on its start side); the
     //      chains first leave uniform single-node levels (no divergent set solves inside them).
-    if (t == 0) {
-        if (cx && cy) {
-            // the corner set (4 members) in local coordinates, generic ordered fixing
-            int mx[4] = {0, -1, 0, -1}, my[4] = {0, 0, -1, -1};
-            constexpr int k = 4;
-            // ascending global index (the oracle's member order; ties in the selection go to it)
-            int64_t gi[4];
-            for (int m = 0; m < k; ++m) gi[m] = gyo(my[m]) * G.ng[0] + gxo(mx[m]);
-            for (int a1 = 1; a1 < k; ++a1)
-                for (int b1 = a1; b1 > 0 && gi[b1 - 1] > gi[b1]; --b1) {
-                    int64_t tg = gi[b1]; gi[b1] = gi[b1 - 1]; gi[b1 - 1] = tg;
-                    int tt = mx[b1]; mx[b1] = mx[b1 - 1]; mx[b1 - 1] = tt;
-                    tt = my[b1]; my[b1] = my[b1 - 1]; my[b1 - 1] = tt;
-                }
-            bool fixed[4] = {false, false, false, false};
-            double val[4];
-            for (int round = 0; round < k; ++round) {
-                int best = -1;
-                double cbest = 0.0;
-                for (int m = 0; m < k; ++m) {
-                    if (fixed[m]) continue;
-                    // a neighbour that is a member: its fixed value or +inf; else the window
-                    auto nb = [&](int lx, int ly) -> double {
-                        for (int q = 0; q < k; ++q)
-                            if (mx[q] == lx && my[q] == ly) return fixed[q] ? val[q] : eik_inf();
-                        return uw(lx, ly);
-                    };
-                    const int px = mx[m], py = my[m];
-                    const double w0 = nb(px - 1, py), w1 = nb(px + 1, py);
-                    const double v0 = nb(px, py - 1), v1 = nb(px, py + 1);
-                    // (the oracle visits the sides in global order -, +; min is order independent)
-                    const double a = w0 < w1 ? w0 : w1, b = v0 < v1 ? v0 : v1;
-                    const double ub = eik_godunov_d(a, b, __dmul_rn(fw(px, py), A.h));
-                    const double uo = uw(px, py);
-                    const double c = uo < ub ? uo : ub;
-                    if (best < 0 || c < cbest) {
-                        best = m;
-                        cbest = c;
-                    }
-                }
-                fixed[best] = true;
-                val[best] = cbest;
+    if (cx && cy && t < 32) {
+        // the corner set (4 members), ordered fixing by lanes 0..3 of the warp: lane m owns member
+        // (-(m & 1), -(m >> 1)) in local coordinates, whose member neighbours are lanes m ^ 1 (along
+        // x) and m ^ 2 (along y), the other two neighbours come from the window.  Per round every
+        // unfixed member's candidate (members at their fixed value or +inf), then the smallest
+        // candidate by shuffles, ties to the lowest global index (the oracle scans the members in
+        // ascending global order and keeps the first minimum); it is fixed.  (The other lane
+        // groups of the warp compute the same and store nothing.)
+        const int m = t & 3;
+        const int mlx = -(m & 1), mly = -(m >> 1);
+        const double xw = uw(mlx ? -2 : 1, mly), yw = uw(mlx, mly ? -2 : 1);
+        const double uo = uw(mlx, mly), fh = __dmul_rn(fw(mlx, mly), A.h);
+        const long long gi = (long long)(gyo(mly) * G.ng[0] + gxo(mlx));
+        bool fixed = false;
+        double val = eik_inf();
+        for (int round = 0; round < 4; ++round) {
+            const double mine = fixed ? val : eik_inf();
+            const double xv = __shfl_xor_sync(0xffffffffu, mine, 1), yv = __shfl_xor_sync(0xffffffffu, mine, 2);
+            const double ub = eik_godunov_d(xv < xw ? xv : xw, yv < yw ? yv : yw, fh);
+            const double c = uo < ub ? uo : ub;
+            double kc = fixed ? eik_inf() : c;
+            long long kg = fixed ? 0x7fffffffffffffffLL : gi;
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                const double oc = __shfl_xor_sync(0xffffffffu, kc, o);
+                const long long og = __shfl_xor_sync(0xffffffffu, kg, o);
+                const bool take = oc < kc || (oc == kc && og < kg);
+                kc = take ? oc : kc;
+                kg = take ? og : kg;
             }
-            for (int m = 0; m < k; ++m) uw(mx[m], my[m]) = val[m];
-        } else if (cx || cy) {
+            if (!fixed && kg == gi) {
+                fixed = true;
+                val = c;
+            }
+        }
+        if (t < 4) uw(mlx, mly) = val;
+    } else if (t == 0 && !(cx && cy)) {
+        if (cx || cy) {
             pairfix(0, 0, cx);
         } else {
             single_upd(0, 0);
         }
     }
     __syncwarp();
+    SW_JITTER_POINT();
     if (t < 2) {
         // lane 0: row 0 with the partner row (k, -1); lane 1: column 0 with the partner column
-        // (-1, k); in step, with the pair geometry written out: along the chain the member's and the
-        // partner's previous values stay in registers (their west / south new neighbour), the old
-        // neighbours come from the window, the pair is solved by ordered fixing as pairfix does
-        // (its member order is fixed per chain: the partner is first iff the box starts at the low
-        // end of the coupled axis)
+        // (-1, k); in step and branch-free: along the chain the member's and the partner's previous
+        // values stay in registers (their west / south new neighbour), the old neighbours come from
+        // the window (loaded a step ahead), the pair is solved by ordered fixing as pairfix does --
+        // both candidates with the other member at +inf, the smaller fixed (its member order is
+        // fixed per chain: the partner is first iff the box starts at the low end of the coupled
+        // axis), the other recomputed by one Godunov update with selected operands.  Along an
+        // uncoupled face the partner line lies outside the domain (+inf in the window), and the
+        // plain update is the own candidate with the partner at +inf.
         const bool row = t == 0;
         const bool cpl = row ? cy : cx;
         const int len = row ? T0 : T1;
         const bool pfix = row ? (sy == 0) : (sx == 0);           // partner before own in global order
-        // window accessors in chain coordinates: node k of the chain, offset o across the face
-        // (o = 0 own line, -1 partner line, +1 the line after own, -2 the line beyond the partner)
-        auto cw = [&](int k, int o) -> double { return row ? uw(k, o) : uw(o, k); };
-        auto cf = [&](int k, int o) -> double { return row ? fw(k, o) : fw(o, k); };
-        double po = cw(0, 0), pq = cw(0, -1);                       // the corner's results
+        // node k of the chain, offset o across the face (o = 0 own line, -1 partner line, +1 the
+        // line after own, -2 the line beyond the partner)
+        const int sk = row ? 1 : WX, so = row ? WX : 1;
+        const double *const u0 = U + 2 * WX + 2;                 // local (0, 0)
+        const double *const f0 = F + FX + 1;
+        const int fk = row ? 1 : FX, fo = row ? FX : 1;
+        double po = u0[0], pq = u0[-so];                          // the corner's results
+        auto ld = [&](int k, double &uo_o, double &e_o, double &n_o, double &fh_o, double &uo_q, double &e_q,
+                      double &s_q, double &fh_q) {
+            const int kk = k < len ? k : len - 1;
+            uo_o = u0[kk * sk]; e_o = u0[(kk + 1) * sk]; n_o = u0[kk * sk + so];
+            uo_q = u0[kk * sk - so]; e_q = u0[(kk + 1) * sk - so]; s_q = u0[kk * sk - 2 * so];
+            fh_o = __dmul_rn(f0[kk * fk], A.h);
+            fh_q = __dmul_rn(f0[kk * fk - fo], A.h);   // (outside the domain: slowness 1, never used)
+        };
+        double uo_o, e_o, n_o, fh_o, uo_q, e_q, s_q, fh_q;
+        ld(1, uo_o, e_o, n_o, fh_o, uo_q, e_q, s_q, fh_q);
         const double inf = eik_inf();
-        for (int k = 1; k < (T0 > T1 ? T0 : T1); ++k) {
-            if (k < len) {
-                const double uo_o = cw(k, 0), e_o = cw(k + 1, 0), n_o = cw(k, 1);
-                const double fh_o = __dmul_rn(cf(k, 0), A.h);
-                double res_o, res_q;
-                if (cpl) {
-                    const double uo_q = cw(k, -1), e_q = cw(k + 1, -1), s_q = cw(k, -2);
-                    const double fh_q = __dmul_rn(cf(k, -1), A.h);
-                    // chain-along pairs (the oracle's sides in global order are order independent: min)
-                    auto cand_o = [&](double vq) {       // own: W new (po), E old, across the face vq, N old
-                        const double ub = eik_godunov_d(fmin(po, e_o), fmin(vq, n_o), fh_o);
-                        return uo_o < ub ? uo_o : ub;
-                    };
-                    auto cand_q = [&](double vo) {       // partner: W new (pq), E old, S old, across vo
-                        const double ub = eik_godunov_d(fmin(pq, e_q), fmin(s_q, vo), fh_q);
-                        return uo_q < ub ? uo_q : ub;
-                    };
-                    // (for the column chain "W/E" are the partner's and own's south / north sides and
-                    //  "across" the west / east side: a = min over x, b = min over y either way,
-                    //  and fmin is symmetric, so the same two mins result)
-                    const double co = cand_o(inf), cq = cand_q(inf);
-                    const bool ofirst = pfix ? (co < cq) : !(cq < co);   // ties: the lower global index
-                    const double fv = ofirst ? co : cq;
-                    const double ov = ofirst ? cand_q(fv) : cand_o(fv);
-                    res_o = ofirst ? fv : ov;
-                    res_q = ofirst ? ov : fv;
-                    (row ? uw(k, -1) : uw(-1, k)) = res_q;
-                } else {
-                    const double ub = eik_godunov_d(fmin(po, e_o), fmin(cw(k, -1), n_o), fh_o);
-                    res_o = uo_o < ub ? uo_o : ub;
-                    res_q = pq;
-                }
-                (row ? uw(k, 0) : uw(0, k)) = res_o;
-                po = res_o;
-                pq = res_q;
-            }
+        for (int k = 1; k < len; ++k) {
+            const double c_uo_o = uo_o, c_e_o = e_o, c_n_o = n_o, c_fh_o = fh_o;
+            const double c_uo_q = uo_q, c_e_q = e_q, c_s_q = s_q, c_fh_q = fh_q;
+            ld(k + 1, uo_o, e_o, n_o, fh_o, uo_q, e_q, s_q, fh_q);
+            // own: W new (po), E old, across the face (vq), N old; partner: W new (pq), E old, S old,
+            // across the face (vo)  (for the column chain the sides are swapped, and fmin is symmetric)
+            const double a_o = fmin(po, c_e_o), a_q = fmin(pq, c_e_q);
+            const double bo = eik_godunov_d(a_o, fmin(inf, c_n_o), c_fh_o);
+            const double bq = eik_godunov_d(a_q, fmin(c_s_q, inf), c_fh_q);
+            const double co = c_uo_o < bo ? c_uo_o : bo, cq = c_uo_q < bq ? c_uo_q : bq;
+            const bool ofirst = pfix ? (co < cq) : !(cq < co);   // ties: the lower global index
+            const double fv = ofirst ? co : cq;
+            // the other member with the fixed one: cand_q(fv) if own is fixed, else cand_o(fv)
+            const double ra = ofirst ? a_q : a_o;
+            const double rb = ofirst ? fmin(c_s_q, fv) : fmin(fv, c_n_o);
+            const double rfh = ofirst ? c_fh_q : c_fh_o, ruo = ofirst ? c_uo_q : c_uo_o;
+            const double ub = eik_godunov_d(ra, rb, rfh);
+            const double ov = ruo < ub ? ruo : ub;
+            const double res_o = cpl ? (ofirst ? fv : ov) : co;
+            const double res_q = ofirst ? ov : fv;
+            (row ? uw(k, 0) : uw(0, k)) = res_o;
+            if (cpl) (row ? uw(k, -1) : uw(-1, k)) = res_q;
+            po = res_o;
+            pq = res_q;
         }
     }
+    __syncwarp();
     SW_TMARK(t_chains);
     asm volatile("bar.sync 1, %0;" ::"r"(ek::LT) : "memory");   // the level threads only
     SW_JITTER_POINT();

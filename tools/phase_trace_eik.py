@@ -19,11 +19,14 @@ def main():
     u0 = np.full((n, n), np.inf)
     u0[n // 3, n // 2] = 0.0
     ge.set_vector(binding.X, u0)
-    ge.eikonal_sweep(2, 0)
+    ph = ge.eikonal_sweep(2, 0)
+    if len(sys.argv) > 1 and sys.argv[1] == "reached":      # every box reached: the full per-node work
+        while ge.eikonal_changes() > 0 and ph < 4000:
+            ph = ge.eikonal_sweep(8, ph)
     torch.cuda.synchronize()
     out = (ctypes.c_ulonglong * 16)()
     L.sw_debug_phase_times(out)
-    ge.eikonal_sweep(4, 2)
+    ge.eikonal_sweep(4, ph)
     torch.cuda.synchronize()
     L.sw_debug_phase_times(out)
     c = max(out[5], 1)

@@ -38,6 +38,19 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 8
     print(f"eikonal 4096^2: {ms:.3f} ms/pass, {n * n / ms / 1e6:.2f} GLUP/s, {24 * n * n / ms / 1e6 / 6536.4:.3f} of HBM")
+    import time
+    t0 = time.perf_counter()
+    ph = 10
+    while ge.eikonal_changes() > 0 and ph < 4000:
+        ph = ge.eikonal_sweep(8, ph)
+    print(f"eikonal fixed point: {ph} passes, {time.perf_counter() - t0:.3f} s")
+    torch.cuda.synchronize()
+    e0.record()
+    ge.eikonal_sweep(8, ph)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 8
+    print(f"eikonal all reached: {ms:.3f} ms/pass, {n * n / ms / 1e6:.2f} GLUP/s, {24 * n * n / ms / 1e6 / 6536.4:.3f} of HBM")
 
 
 if __name__ == "__main__":
