@@ -48,6 +48,22 @@ __device__ __forceinline__ double eik_godunov_d(double a, double b, double fh) {
     return __dmul_rn(0.5, __dadd_rn(__dadd_rn(a, b), __dsqrt_rn(disc)));
 }
 
+// The same value without branches (the start-face chains, where the two candidates of a pair are
+// independent and should overlap): every operand the oracle's eik_godunov would use is computed
+// and the result selected.  The square root's argument is clamped to >= fh^2 / 4 so that it is
+// always a positive normal number (no slow path); wherever its value is selected, |a - b| < fh and
+// disc = 2 fh^2 - (a - b)^2 > fh^2, so the clamp never changes it.
+__device__ __forceinline__ double eik_godunov_bf(double a, double b, double fh) {
+    const double m = a < b ? a : b;
+    const double d = __dsub_rn(a, b);
+    const double fhfh = __dmul_rn(fh, fh);
+    const double disc = fma(-d, d, __dmul_rn(2.0, fhfh));
+    const double sq = __dsqrt_rn(fmax(disc, __dmul_rn(0.25, fhfh)));
+    const double t2 = __dmul_rn(0.5, __dadd_rn(__dadd_rn(a, b), sq));
+    const double r = fabs(d) >= fh ? __dadd_rn(m, fh) : t2;
+    return m == eik_inf() ? m : r;
+}
+
 inline size_t eik2_smem(const Geo &G) {
     return sizeof(double) * ((size_t)(G.T[0] + 4) * (G.T[1] + 4) + (size_t)(G.T[0] + 1) * (G.T[1] + 1));
 }
@@ -252,8 +268,8 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
             // own: W new (po), E old, across the face (vq), N old; partner: W new (pq), E old, S old,
             // across the face (vo)  (for the column chain the sides are swapped, and fmin is symmetric)
             const double a_o = fmin(po, c_e_o), a_q = fmin(pq, c_e_q);
-            const double bo = eik_godunov_d(a_o, fmin(inf, c_n_o), c_fh_o);
-            const double bq = eik_godunov_d(a_q, fmin(c_s_q, inf), c_fh_q);
+            const double bo = eik_godunov_bf(a_o, fmin(inf, c_n_o), c_fh_o);
+            const double bq = eik_godunov_bf(a_q, fmin(c_s_q, inf), c_fh_q);
             const double co = c_uo_o < bo ? c_uo_o : bo, cq = c_uo_q < bq ? c_uo_q : bq;
             const bool ofirst = pfix ? (co < cq) : !(cq < co);   // ties: the lower global index
             const double fv = ofirst ? co : cq;
@@ -261,7 +277,7 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
             const double ra = ofirst ? a_q : a_o;
             const double rb = ofirst ? fmin(c_s_q, fv) : fmin(fv, c_n_o);
             const double rfh = ofirst ? c_fh_q : c_fh_o, ruo = ofirst ? c_uo_q : c_uo_o;
-            const double ub = eik_godunov_d(ra, rb, rfh);
+            const double ub = eik_godunov_bf(ra, rb, rfh);
             const double ov = ruo < ub ? ruo : ub;
             const double res_o = cpl ? (ofirst ? fv : ov) : co;
             const double res_q = ofirst ? ov : fv;

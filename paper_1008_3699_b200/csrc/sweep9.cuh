@@ -25,6 +25,8 @@
 //     three implicit coefficients fetched 16 steps ahead by cp.async into a per-lane ring;
 //  5. write-back by all threads.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "sweep2p.cuh"
 
@@ -51,10 +53,10 @@ struct Sweep9Args {
 };
 
 // region 0: the x_old window over local [-2, T + 2), after the explicit parts the chain data
-// [2][64][CDW] and the wavefront's coefficient ring [PD][32][6]; then (r0, later the new values) over
+// [2][64][CDW], the wavefront's coefficient ring [PD][32][6] and the corner's 4 x 8 coefficients; then (r0, later the new values) over
 // local [-2, T + 2) and alpha over local [-1, T)
 __host__ __device__ inline int sweep9_r0(int T0, int T1) {
-    const int w = (T0 + 4) * (T1 + 4), c = 2 * 64 * s9::CDW + s9::PD * 32 * 6;
+    const int w = (T0 + 4) * (T1 + 4), c = 2 * 64 * s9::CDW + s9::PD * 32 * 6 + 32;
     return w > c ? w : c;
 }
 inline size_t sweep9_smem(const Geo &G) {
@@ -120,10 +122,17 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     SW_TADD(0, t_start, t_staged);
     // ---- explicit parts of every node of local [-1, T)^2 inside the domain (own nodes and the
     // partner layers): alpha = w / a_P, r0 = fma(alpha, b + sum_explicit c u_old, (1 - w) u_old).
-    // Three nodes per thread and pass, all 27 of their global loads issued before any use.
-    {
+    // Three nodes per thread and pass, all 27 of their global loads issued before any use; the
+    // box's directions are compile-time constants of one of four instantiations (the implicit /
+    // explicit split and the window offsets of the neighbours fold away).
+    auto explicit_parts = [&](auto SXc, auto SYc) {
+        constexpr int SX = decltype(SXc)::value, SY = decltype(SYc)::value;
         const int NA = AX * (T1 + 1);
         const int64_t ng0 = G.ng[0], ng1 = G.ng[1], P0 = G.P0;
+        const int64_t gx0 = SX ? X0 + T0 - 1 : X0, gy0 = SY ? Y0 + T1 - 1 : Y0;   // global of local (0, 0)
+        constexpr int SGX = SX ? -1 : 1, SGY = SY ? -1 : 1;
+        const int dq = 3 * s9::NT / AX, dr = 3 * s9::NT % AX;                     // pass stride in (row, column)
+        int qx = threadIdx.x % AX, qy = threadIdx.x / AX;                         // first node of this thread
         for (int e0 = threadIdx.x; e0 < NA; e0 += 3 * s9::NT) {
             double c8[3][8], bv[3];
             int px[3], py[3];
@@ -132,11 +141,12 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
                 const int e = e0 + u * s9::NT;
-                px[u] = e % AX - 1;
-                py[u] = e / AX - 1;
-                gx[u] = gxo(px[u]);
-                gy[u] = gyo(py[u]);
-                ok[u] = e < NA && inside(gx[u], gy[u]);
+                const int ex = qx + (u * s9::NT) % AX, ey = qy + (u * s9::NT) / AX;   // (one carry at most)
+                px[u] = (ex >= AX ? ex - AX : ex) - 1;
+                py[u] = (ex >= AX ? ey + 1 : ey) - 1;
+                gx[u] = gx0 + SGX * px[u];
+                gy[u] = gy0 + SGY * py[u];
+                ok[u] = e < NA && gx[u] >= 0 && gx[u] < ng0 && gy[u] >= 0 && gy[u] < ng1;
                 // coefficient of global neighbour k (coef(), R-N3): faces at the node (W, S) or
                 // one step up (E, N), diagonals at the cell corners
                 const int64_t i = ok[u] ? gidx(G, gx[u], gy[u], 0) : G.origin;
@@ -150,29 +160,44 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 c8[u][7] = __ldg(A.dd + i + 1 + P0);
                 bv[u] = __ldg(A.b + i);
             }
+            qx += dr;
+            qy += dq;
+            if (qx >= AX) {
+                qx -= AX;
+                ++qy;
+            }
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
                 if (!ok[u]) continue;
                 const double *c = c8[u];
                 const double ap = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[7]) + (c[5] + c[6])) + G.beta;
                 const int bx = px[u] < 0, by = py[u] < 0;   // partner layers: the neighbour box starts toward ours
-                const double w = A.omega[(sx ^ bx) | ((sy ^ by) << 1)];
+                const double w = A.omega[(SX ^ bx) | ((SY ^ by) << 1)];
                 const double al = div_rn(w, ap);
                 const bool xm = gx[u] > 0, xp = gx[u] + 1 < ng0, ym = gy[u] > 0, yp = gy[u] + 1 < ng1;
-                const int sdx = bx ? 1 : -1, sdy = by ? 1 : -1;   // local start side of the node's box
+                const double *xo = XO + wi(px[u], py[u]);
                 double ev = bv[u];
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const int dx = s9::nbx(kk), dy = s9::nby(kk);
                     const bool in = (dx < 0 ? xm : (dx > 0 ? xp : true)) && (dy < 0 ? ym : (dy > 0 ? yp : true));
-                    const int ldx = sx ? -dx : dx, ldy = sy ? -dy : dy;
-                    const bool imp = (dx == 0 || ldx == sdx) && (dy == 0 || ldy == sdy);
-                    if (in && !imp) ev = fma(c[kk], XO[wi(px[u] + ldx, py[u] + ldy)], ev);
+                    const int ldx = SX ? -dx : dx, ldy = SY ? -dy : dy;
+                    // implicit iff on the start side of the node's box along every axis where they
+                    // differ (own box: local -; a partner layer's box: local +)
+                    const bool impx = dx == 0 || (ldx < 0 ? !bx : bx);
+                    const bool impy = dy == 0 || (ldy < 0 ? !by : by);
+                    if (in && !(impx && impy)) ev = fma(c[kk], xo[ldx + ldy * WX], ev);
                 }
-                XN[wi(px[u], py[u])] = fma(al, ev, (1.0 - w) * XO[wi(px[u], py[u])]);
+                XN[wi(px[u], py[u])] = fma(al, ev, (1.0 - w) * xo[0]);
                 AW[ai(px[u], py[u])] = al;
             }
         }
+    };
+    switch (sx | (sy << 1)) {
+    case 0: explicit_parts(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{}); break;
+    case 1: explicit_parts(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{}); break;
+    case 2: explicit_parts(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{}); break;
+    default: explicit_parts(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}); break;
     }
     __syncthreads();
     SW_TMARK(t_r0);
@@ -180,6 +205,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     // ---- region 0 is dead from here on: the chain data and the wavefront's coefficient ring
     double *const CD = XO;                                     // [2][64][CDW]
     double *const RING = XO + 2 * 64 * s9::CDW;                // [PD][32][6]
+    double *const CC = RING + s9::PD * 32 * 6;                 // corner coefficients [4][8]
     const int lane = threadIdx.x & 31;
     // wavefront geometry (warp 0): lane l owns rows A = 2l + 1 and B = 2l + 2 (local y) and at step
     // s updates column x = s - l + 1 of both; rows >= T1 do not exist
@@ -193,27 +219,39 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     const int sgx = sx ? -1 : 1;
     const int64_t iA = gidx(G, gxo(0), gyo(rAl), 0), iB = gidx(G, gxo(0), gyo(rBl), 0);
     const double *const fdg = (sx == sy) ? A.dd : A.da;
+    // per-lane source addresses of column 0 (W, S, SW coefficients of rows A and B); node x is
+    // sgx * x elements further
+    const double *const qWA = A.f0 ? A.f0 + iA + sx : nullptr, *const qWB = A.f0 ? A.f0 + iB + sx : nullptr;
+    const double *const qSA = A.f1 ? A.f1 + iA + sy * P0 : nullptr, *const qSB = A.f1 ? A.f1 + iB + sy * P0 : nullptr;
+    const double *const qDA = fdg + iA + sx + sy * P0, *const qDB = fdg + iB + sx + sy * P0;
+    // the coefficients of step s (node column x = s - l + 1 of rows A and B) into slot s % PD, one
+    // commit group per step (1.0 for unit faces)
     auto fetch = [&](int s) {
         const int x = s - lane + 1;
         if (threadIdx.x < 32 && onA && x >= 1 && x < T0) {
             double *dst = RING + ((s % s9::PD) * 32 + lane) * 6;
-            const int64_t ia = iA + sgx * x, ib = iB + sgx * x;
+            const int64_t o = sgx * x;
             auto cpa = [&](double *d, const double *src) {
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(src) : "memory");
             };
-            if (A.f0) cpa(dst + 0, A.f0 + ia + sx); else dst[0] = 1.0;
-            if (A.f1) cpa(dst + 1, A.f1 + ia + sy * P0); else dst[1] = 1.0;
-            cpa(dst + 2, fdg + ia + sx + sy * P0);
+            if (qWA) cpa(dst + 0, qWA + o); else dst[0] = 1.0;
+            if (qSA) cpa(dst + 1, qSA + o); else dst[1] = 1.0;
+            cpa(dst + 2, qDA + o);
             if (onB) {
-                if (A.f0) cpa(dst + 3, A.f0 + ib + sx); else dst[3] = 1.0;
-                if (A.f1) cpa(dst + 4, A.f1 + ib + sy * P0); else dst[4] = 1.0;
-                cpa(dst + 5, fdg + ib + sx + sy * P0);
+                if (qWB) cpa(dst + 3, qWB + o); else dst[3] = 1.0;
+                if (qSB) cpa(dst + 4, qSB + o); else dst[4] = 1.0;
+                cpa(dst + 5, qDB + o);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if (threadIdx.x < 32)
         for (int s = 0; s < s9::PD; ++s) fetch(s);
+    // the corner's coefficients (threads 32..63: member m = (-(m & 1), -(m >> 1)), neighbour k)
+    if (threadIdx.x >= 32 && threadIdx.x < 64 && (cx || cy)) {
+        const int m = (threadIdx.x - 32) >> 3, kk = threadIdx.x & 7;
+        CC[m * 8 + kk] = coef(kk, gxo(-(m & 1)), gyo(-(m >> 1)));
+    }
     int fl = 0;
     // ---- the chain data (threads 0..127, item (chain, k)): chain 0 = local row 0 (node (k, 0),
     // partner (k, -1) across the y start face), chain 1 = local column 0 (node (0, k), partner
@@ -263,6 +301,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     }
     // ---- the start corner (thread 0): the dense 4 x 4 set, a pair across the one coupled face,
     // or a single node without implicit neighbours in the domain (u = r0, nothing to do)
+    __syncthreads();                                          // CC
     if (threadIdx.x == 0 && (cx || cy)) {
         if (cx && cy) {
             constexpr int k = 4;
@@ -287,7 +326,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                     int qx, qy;
                     lnb(0, kk, qx, qy, px, py);
                     if (!implicit(px, py, qx, qy)) continue;
-                    const double m = al * coef(kk, gx, gy);
+                    const double m = al * CC[8 * (-px - 2 * py) + kk];
                     int in = -1;
                     for (int q = 0; q < k; ++q)
                         if (mx[q] == qx && my[q] == qy) in = q;
@@ -330,7 +369,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                     int qx, qy;
                     lnb(0, kk, qx, qy, px, py);
                     if (!implicit(px, py, qx, qy)) continue;
-                    const double m = al * coef(kk, gx, gy);
+                    const double m = al * CC[8 * (-px - 2 * py) + kk];
                     if (qx == ox && qy == oy) moff = -m;
                     else acc = fma(m, XN[wi(qx, qy)], acc);
                 }
@@ -377,6 +416,8 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
         }
         __syncwarp();
         SW_JITTER_POINT();
+        SW_TMARK(t_ch);
+        SW_TADD(4, t_cs, t_ch);
         // ---- the wavefront over local [1, T0) x [1, T1):
         //   u_A = fma(m_SW, SW_A, fma(m_S, S, fma(m_W, W_A, r0_A))),
         //   u_B = fma(m_SW, W_A, fma(m_S, u_A, fma(m_W, W_B, r0_B)))
@@ -388,26 +429,42 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
             const int NSTEP = (T0 - 1) + (nl - 1);
             double WA = XN[wi(0, rAl)], WB = XN[wi(0, rBl)], SWA = XN[wi(0, rAl - 1)];
             double uBp = 0.0;
+            // the operands of step s (ring coefficients, alpha, r0, row 0) are loaded during step s - 1,
+            // ahead of its dependent chain
+            auto ldv = [&](int s, double (&c)[6], double &aA, double &aB, double &r0A, double &r0B, double &row0) {
+                const int x = s - lane + 1;
+                const int xl = x < 1 ? 1 : (x >= T0 ? T0 - 1 : x);
+                const double *cr = RING + ((s % s9::PD) * 32 + lane) * 6;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) c[j] = cr[j];
+                aA = AW[ai(xl, rAl)];
+                aB = AW[ai(xl, rBl)];
+                r0A = XN[wi(xl, rAl)];
+                r0B = XN[wi(xl, rBl)];
+                row0 = XN[wi(xl, 0)];
+            };
+            double c6[6], aA, aB, r0A, r0B, row0;
+            asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 1) : "memory");   // group 0
+            ldv(0, c6, aA, aB, r0A, r0B, row0);
             for (int s = 0; s < NSTEP; ++s) {
                 const int x = s - lane + 1;
                 const bool act = onA && x >= 1 && x < T0;
                 const int xl = x < 1 ? 1 : (x >= T0 ? T0 - 1 : x);
-                asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 1) : "memory");
-                const double *cr = RING + ((s % s9::PD) * 32 + lane) * 6;
-                const double aA = AW[ai(xl, rAl)], aB = AW[ai(xl, rBl)];
-                const double mWA = aA * cr[0], mSA = aA * cr[1], mDA = aA * cr[2];
-                const double mWB = aB * cr[3], mSB = aB * cr[4], mDB = aB * cr[5];
-                const double r0A = XN[wi(xl, rAl)], r0B = XN[wi(xl, rBl)], row0 = XN[wi(xl, 0)];
-                const double S = sel_f64(lane == 0, row0, shfl_up1_f64(uBp));
-                const double uA = fma(mDA, SWA, fma(mSA, S, fma(mWA, WA, r0A)));
-                const double uB = fma(mDB, WA, fma(mSB, uA, fma(mWB, WB, r0B)));
+                const double mWA = aA * c6[0], mSA = aA * c6[1], mDA = aA * c6[2];
+                const double mWB = aB * c6[3], mSB = aB * c6[4], mDB = aB * c6[5];
+                const double cr0A = r0A, cr0B = r0B, crow0 = row0;
+                asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 2) : "memory");   // group s + 1
+                ldv(s + 1, c6, aA, aB, r0A, r0B, row0);
+                const double S = sel_f64(lane == 0, crow0, shfl_up1_f64(uBp));
+                const double uA = fma(mDA, SWA, fma(mSA, S, fma(mWA, WA, cr0A)));
+                const double uB = fma(mDB, WA, fma(mSB, uA, fma(mWB, WB, cr0B)));
                 st_shared_if(XN + wi(xl, rAl), uA, act);
                 st_shared_if(XN + wi(xl, rBl), uB, act && onB);
                 SWA = sel_f64(act, S, SWA);
                 WA = sel_f64(act, uA, WA);
                 WB = sel_f64(act, uB, WB);
                 uBp = uB;
-                fetch(s + s9::PD);                                     // this lane's slot is consumed
+                fetch(s + s9::PD);                                     // slot s % PD is consumed
             }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");

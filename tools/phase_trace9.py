@@ -39,7 +39,7 @@ def main():
     L.sw_debug_phase_times(out)
     c = max(out[5], 1)
     print(f"nine-point 4096^2: {ms:.4f} ms/sweep, {n * n / ms / 1e6:.2f} GLUP/s")
-    for i, nm in ((0, "stage-in"), (1, "alpha / r0"), (2, "set coefficients"), (3, "fronts")):
+    for i, nm in ((0, "stage-in"), (1, "alpha / r0"), (2, "set coefficients"), (3, "chains + wavefront"), (4, "  of which chains")):
         print(f"  {nm:18s} {out[i] / c:10.0f} cycles/CTA")
 
 
