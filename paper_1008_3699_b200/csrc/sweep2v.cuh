@@ -33,7 +33,10 @@ constexpr int T = 64, W = 68, WS = W * W;
 #endif
 constexpr int NW = SW_V2_NW;            // warps per box (8: the prologue streams 8 rows per warp)
 constexpr int ROWS = T / NW;            // prologue rows per warp
-constexpr int RING = 4;                 // rows in flight per warp
+#ifndef SW_V2_RING
+#define SW_V2_RING 2
+#endif
+constexpr int RING = SW_V2_RING;        // rows in flight per warp
 constexpr int NCOEF = T * T;            // m_W / m_S arrays, pitch 64 (window column order)
 constexpr int NCH = 6 * T + 4;          // chain partner couplings, chain pivots, diagonal couplings, 0, 1
 constexpr size_t SMEM = sizeof(double) * (WS + 2 * NCOEF + NCH);
@@ -45,6 +48,17 @@ constexpr size_t SMEM = sizeof(double) * (WS + 2 * NCOEF + NCH);
 //   aux (invd_mode, ILU) or omega / a_P (SSOR); couple = 0 drops the start-face coupling (the
 //   first phase of the transposed solve, run at the reversed corner).
 enum { MODE_SOR = 0, MODE_TRI = 1 };
+
+// Look-ahead (SW_V2_AHEAD boxes, 0 = off): once its own prologue is done, a box asks the L2 for the
+// tiles of the box that will take its place on the SM (x window, aux, F_x, F_y), so that box's
+// stage-in and prologue find their lines in L2 instead of waiting on HBM.
+#ifndef SW_V2_AHEAD
+#define SW_V2_AHEAD 222
+#endif
+struct Ahead2v {
+    const CUtensorMap *x, *b, *fx, *fy;
+    int tx, ty;        // tile coordinates of the box looked ahead to (tx < 0: none)
+};
 
 struct Sweep2vArgs {
     Geo G;
@@ -66,7 +80,7 @@ __device__ __forceinline__ void st_shared_v2_noalias(double *addr, double a, dou
 
 template <int MODE, bool FACES, int SX, int SY>
 __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, uint64_t *bar, int tx, int ty, bool cx,
-                                             bool cy) {
+                                             bool cy, const Ahead2v &AH) {
     constexpr bool SOR = (MODE == MODE_SOR);
     const bool invd = !SOR && A.invd_mode;      // alpha = 1/D~ from the aux array (ILU)
     const bool load_aux = SOR || invd;
@@ -290,6 +304,14 @@ __device__ __forceinline__ void sweep2v_tile(const Sweep2vArgs &A, double *sm, u
     }
     __syncthreads();
     SW_TMARK(t_prologue);
+    if (SW_V2_AHEAD > 0 && threadIdx.x == 64 && AH.tx >= 0) {
+        tma_prefetch_2d(AH.x, AH.tx * T, AH.ty * T);
+        if (load_aux) tma_prefetch_2d(AH.b, AH.tx * T + 2, AH.ty * T + 2);
+        if constexpr (FACES) {
+            tma_prefetch_2d(AH.fx, AH.tx * T + 2, AH.ty * T + 2);
+            tma_prefetch_2d(AH.fy, AH.tx * T + 2, AH.ty * T + 2);
+        }
+    }
 
     // ---------------------------------------------------------------- 3. corner and chains (warp 1)
     if (warp == 1 && lane == 0) {
@@ -495,11 +517,19 @@ __global__ void __launch_bounds__(v2::NW * 32, 2)
         }
     }
     __syncthreads();
+    Ahead2v AH{&tmx, &tmb, &tmfx, &tmfy, -1, 0};
+    if (SW_V2_AHEAD > 0) {
+        const int64_t nb = (int64_t)blockIdx.x + SW_V2_AHEAD;
+        if (nb < (int64_t)gridDim.x) {
+            AH.tx = (int)(nb % G.nt[0]);
+            AH.ty = (int)(nb / G.nt[0]);
+        }
+    }
     switch (sx | (sy << 1)) {
-        case 0: sweep2v_tile<MODE, FACES, 0, 0>(A, sm, &bar, tx, ty, cx, cy); break;
-        case 1: sweep2v_tile<MODE, FACES, 1, 0>(A, sm, &bar, tx, ty, cx, cy); break;
-        case 2: sweep2v_tile<MODE, FACES, 0, 1>(A, sm, &bar, tx, ty, cx, cy); break;
-        default: sweep2v_tile<MODE, FACES, 1, 1>(A, sm, &bar, tx, ty, cx, cy); break;
+        case 0: sweep2v_tile<MODE, FACES, 0, 0>(A, sm, &bar, tx, ty, cx, cy, AH); break;
+        case 1: sweep2v_tile<MODE, FACES, 1, 0>(A, sm, &bar, tx, ty, cx, cy, AH); break;
+        case 2: sweep2v_tile<MODE, FACES, 0, 1>(A, sm, &bar, tx, ty, cx, cy, AH); break;
+        default: sweep2v_tile<MODE, FACES, 1, 1>(A, sm, &bar, tx, ty, cx, cy, AH); break;
     }
 }
 

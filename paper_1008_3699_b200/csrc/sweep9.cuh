@@ -68,11 +68,14 @@ inline bool sweep9_supported(const Geo &G) {
     return G.dim == 2 && G.T[0] <= 64 && G.T[1] <= 64 && sweep9_smem(G) <= 227 * 1024;
 }
 
+// TC > 0: square boxes of TC nodes an axis, known at compile time (the index arithmetic of the
+// stage-in, the explicit parts and the write-back then needs no runtime division); TC = 0: any box.
+template <int TC>
 __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     extern __shared__ __align__(16) double s9m[];
     SW_JITTER_POINT();
     const Geo &G = A.G;
-    const int T0 = G.T[0], T1 = G.T[1], WX = T0 + 4, AX = T0 + 1;
+    const int T0 = TC ? TC : G.T[0], T1 = TC ? TC : G.T[1], WX = T0 + 4, AX = T0 + 1;
     double *const XO = s9m, *const XN = s9m + sweep9_r0(T0, T1), *const AW = XN + WX * (T1 + 4);
     const int tx = blockIdx.x % G.nt[0], ty = blockIdx.x / G.nt[0];
     const int64_t R0 = tx, R1 = ty + G.toff[1];
@@ -227,6 +230,9 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     // the coefficients of step s (node column x = s - l + 1 of rows A and B) into slot s % PD, one
     // commit group per step (1.0 for unit faces)
     auto fetch = [&](int s) {
+#ifdef SW_S9_NOFETCH   // timing experiment only (wrong results)
+        return;
+#endif
         const int x = s - lane + 1;
         if (threadIdx.x < 32 && onA && x >= 1 && x < T0) {
             double *dst = RING + ((s % s9::PD) * 32 + lane) * 6;
@@ -453,7 +459,9 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 const double mWA = aA * c6[0], mSA = aA * c6[1], mDA = aA * c6[2];
                 const double mWB = aB * c6[3], mSB = aB * c6[4], mDB = aB * c6[5];
                 const double cr0A = r0A, cr0B = r0B, crow0 = row0;
+#ifndef SW_S9_NOWAIT
                 asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 2) : "memory");   // group s + 1
+#endif
                 ldv(s + 1, c6, aA, aB, r0A, r0B, row0);
                 const double S = sel_f64(lane == 0, crow0, shfl_up1_f64(uBp));
                 const double uA = fma(mDA, SWA, fma(mSA, S, fma(mWA, WA, cr0A)));
@@ -484,11 +492,13 @@ inline cudaError_t launch_sweep9(const Sweep9Args &A, cudaStream_t s) {
     const size_t sm = sweep9_smem(A.G);
     static size_t attr = 0;
     if (sm > attr) {
-        cudaFuncSetAttribute(k_sweep9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_sweep9<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_sweep9<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = sm;
     }
     const unsigned tiles = (unsigned)((int64_t)A.G.nt[0] * A.G.nt[1]);
-    k_sweep9<<<tiles, s9::NT, sm, s>>>(A);
+    if (A.G.T[0] == 64 && A.G.T[1] == 64) k_sweep9<64><<<tiles, s9::NT, sm, s>>>(A);
+    else k_sweep9<0><<<tiles, s9::NT, sm, s>>>(A);
     return cudaGetLastError();
 }
 
