@@ -8,14 +8,17 @@
 // One CTA of 256 threads per box (T0, T1 <= 64).  All threads stage in the old values of the box and
 // its 2-node halo in LOCAL coordinates (local +a points away from the box's start corner; a node
 // outside the domain reads +inf) and the slowness of the active nodes (own and partner layers).
-// Warp 0 then: thread 0 solves the corner set; lanes 0 and 1 run the two start-face chains (row 0
-// with its partner row, column 0 with its partner column: pairs by ordered fixing, or plain updates
-// along an uncoupled face), branch-free with their window operands loaded a step ahead; then the
-// other own nodes as a register wavefront (lane l owns rows 2l+1 and 2l+2, the second one column
-// behind the first so that the two are independent; S by shfl.up, W from registers, E and N old
-// from the window).  Results go in place (the window then holds new values on every node's start
-// side and old values on its end side, exactly the split the method prescribes); write-back by all
-// threads.
+// Then the corner set (four lanes of warp 0, ordered fixing with shuffles), the two start-face chains
+// (lanes 0 and 1: row 0 with its partner row, column 0 with its partner column: pairs by ordered
+// fixing, or plain updates along an uncoupled face; branch-free, window operands loaded a step
+// ahead), then the other own nodes front by front (d = x + y; the first 64 threads, one column
+// each, a named barrier of the 64 per front): a node outside the coupled sets is updated in place
+// from the window, which holds new values on its start side and old values on its end side,
+// exactly the split the method prescribes.  Write-back by all threads.
+// (A register wavefront in one warp -- lane l owning rows 2l+1 and 2l+2, the second a column behind
+// the first -- was built and is bitwise correct, but has as many steps as there are fronts (126)
+// and pays the square root on every node: 0.87 instead of 0.70 ms per pass at 4096^2; not kept,
+// profiles/r02_eik_wavefront_experiment.txt.)
 #pragma once
 #include "common.cuh"
 #include "sweep2p.cuh"
@@ -72,6 +75,9 @@ inline bool eik2_supported(const Geo &G) {
     return G.dim == 2 && G.T[0] <= 64 && G.T[1] <= 64 && eik2_smem(G) <= 227 * 1024;
 }
 
+#ifndef SW_EK_AHEAD
+#define SW_EK_AHEAD 333
+#endif
 __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
     extern __shared__ __align__(16) double esm[];
     SW_JITTER_POINT();
@@ -139,6 +145,23 @@ __global__ void __launch_bounds__(ek::NT, 3) k_eik2(Eik2Args A) {
         return;
     }
     if (threadIdx.x >= ek::LT) {           // the other warps rejoin for the write-back
+#if SW_EK_AHEAD > 0
+        {   // look-ahead: the lines of the box SW_EK_AHEAD launches later (u window and slowness,
+            // clamped to the domain) into L2 while this box runs its chains and fronts
+            const int64_t nb = (int64_t)blockIdx.x + SW_EK_AHEAD;
+            if (nb < (int64_t)gridDim.x) {
+                const int64_t nX0 = (nb % G.nt[0]) * T0 - 2, nY0 = (nb / G.nt[0] + G.toff[1]) * T1 - 2;
+                const int NL = (T0 + 4 + 15) / 16 + 1;
+                for (int e = threadIdx.x - ek::LT; e < (T1 + 4) * NL * 2; e += ek::NT - ek::LT) {
+                    const int a = e & 1, q = e >> 1;
+                    int64_t gx = nX0 + 16 * (q % NL), gy = nY0 + q / NL;
+                    gx = gx < 0 ? 0 : (gx >= G.ng[0] ? G.ng[0] - 1 : gx);
+                    gy = gy < 0 ? 0 : (gy >= G.ng[1] ? G.ng[1] - 1 : gy);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"((a ? A.S : A.uo) + gidx(G, gx, gy, 0)));
+                }
+            }
+        }
+#endif
         __syncthreads();
         for (int e = threadIdx.x; e < T0 * T1; e += ek::NT) {
             const int lx = e % T0, ly = e / T0;

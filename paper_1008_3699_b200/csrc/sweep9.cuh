@@ -21,8 +21,9 @@
 //     start corner (the dense 4 x 4, or a pair);
 //  4. warp 0, lanes 0 / 1: the chains of 2 x 2 systems along local row 0 / column 0 (or the plain
 //     recurrence along a physical boundary), then the whole warp: the wavefront over [1, T)^2 as in
-//     k_sweep2p -- lane l owns rows 2l+1, 2l+2, S by shfl.up, W and SW from registers, the nodes'
-//     three implicit coefficients fetched 16 steps ahead by cp.async into a per-lane ring;
+//     k_sweep2p -- lane l owns rows 2l+1, 2l+2, S by shfl.up, W and SW from registers; the nodes'
+//     three implicit coefficients come from a shared-memory ring that warps 1..7 fill a chunk of
+//     8 steps ahead (coalesced row segments, one named barrier per chunk);
 //  5. write-back by all threads.
 #pragma once
 #include <type_traits>
@@ -36,6 +37,12 @@ namespace s9 {
 constexpr int NT = 256;   // threads per CTA
 constexpr int PD = 16;    // wavefront coefficient ring depth (steps ahead)
 constexpr int CDW = 8;    // doubles of chain data per chain step
+// ring element (slot, coefficient j, lane): slot * RSL + j * RJL + lane.  The wavefront reads one
+// (slot, j) for all lanes (consecutive words); a producer warp stores 8 consecutive slots x 4
+// coefficients of one lane: with RJL = 33, RSL = 198 (= 6 mod 16) a half-warp's 16 stores fall into
+// 16 different 8-byte banks.
+constexpr int RJL = 33, RSL = 6 * RJL;
+constexpr int NPROD = NT - 32;   // producer threads (warps 1..7)
 __constant__ int NBX[8] = {-1, 1, 0, 0, -1, 1, -1, 1};   // global neighbour order W, E, S, N, SW, SE, NW, NE
 __constant__ int NBY[8] = {0, 0, -1, 1, -1, -1, 1, 1};
 __host__ __device__ constexpr int nbx(int k) { return k == 0 ? -1 : (k == 1 ? 1 : (k < 4 ? 0 : ((k & 1) ? 1 : -1))); }
@@ -56,7 +63,7 @@ struct Sweep9Args {
 // [2][64][CDW], the wavefront's coefficient ring [PD][32][6] and the corner's 4 x 8 coefficients; then (r0, later the new values) over
 // local [-2, T + 2) and alpha over local [-1, T)
 __host__ __device__ inline int sweep9_r0(int T0, int T1) {
-    const int w = (T0 + 4) * (T1 + 4), c = 2 * 64 * s9::CDW + s9::PD * 32 * 6 + 32;
+    const int w = (T0 + 4) * (T1 + 4), c = 2 * 64 * s9::CDW + s9::PD * s9::RSL + 32;
     return w > c ? w : c;
 }
 inline size_t sweep9_smem(const Geo &G) {
@@ -70,6 +77,12 @@ inline bool sweep9_supported(const Geo &G) {
 
 // TC > 0: square boxes of TC nodes an axis, known at compile time (the index arithmetic of the
 // stage-in, the explicit parts and the write-back then needs no runtime division); TC = 0: any box.
+#ifndef SW_S9_AHEAD
+#define SW_S9_AHEAD 222
+#endif
+#ifndef SW_S9_AHEAD_AT
+#define SW_S9_AHEAD_AT 1      // the chunk after which the producers issue the look-ahead prefetches
+#endif
 template <int TC>
 __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     extern __shared__ __align__(16) double s9m[];
@@ -208,7 +221,7 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     // ---- region 0 is dead from here on: the chain data and the wavefront's coefficient ring
     double *const CD = XO;                                     // [2][64][CDW]
     double *const RING = XO + 2 * 64 * s9::CDW;                // [PD][32][6]
-    double *const CC = RING + s9::PD * 32 * 6;                 // corner coefficients [4][8]
+    double *const CC = RING + s9::PD * s9::RSL;                // corner coefficients [4][8]
     const int lane = threadIdx.x & 31;
     // wavefront geometry (warp 0): lane l owns rows A = 2l + 1 and B = 2l + 2 (local y) and at step
     // s updates column x = s - l + 1 of both; rows >= T1 do not exist
@@ -216,48 +229,25 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
     const bool onA = rA < T1, onB = rB < T1;
     const int rAl = onA ? rA : T1 - 1, rBl = onB ? rB : (T1 > 1 ? T1 - 1 : 0);
     // the implicit couplings of a wavefront node are local W, S, SW (global kW, kS, kSW: in the
-    // oracle's neighbour order always in this order); their coefficients arrive PD steps ahead by
-    // cp.async into a per-lane ring, one commit group per step
+    // oracle's neighbour order always in this order)
     const int64_t P0 = G.P0;
-    const int sgx = sx ? -1 : 1;
-    const int64_t iA = gidx(G, gxo(0), gyo(rAl), 0), iB = gidx(G, gxo(0), gyo(rBl), 0);
     const double *const fdg = (sx == sy) ? A.dd : A.da;
-    // per-lane source addresses of column 0 (W, S, SW coefficients of rows A and B); node x is
-    // sgx * x elements further
-    const double *const qWA = A.f0 ? A.f0 + iA + sx : nullptr, *const qWB = A.f0 ? A.f0 + iB + sx : nullptr;
-    const double *const qSA = A.f1 ? A.f1 + iA + sy * P0 : nullptr, *const qSB = A.f1 ? A.f1 + iB + sy * P0 : nullptr;
-    const double *const qDA = fdg + iA + sx + sy * P0, *const qDB = fdg + iB + sx + sy * P0;
-    // the coefficients of step s (node column x = s - l + 1 of rows A and B) into slot s % PD, one
-    // commit group per step (1.0 for unit faces)
-    auto fetch = [&](int s) {
-#ifdef SW_S9_NOFETCH   // timing experiment only (wrong results)
-        return;
-#endif
-        const int x = s - lane + 1;
-        if (threadIdx.x < 32 && onA && x >= 1 && x < T0) {
-            double *dst = RING + ((s % s9::PD) * 32 + lane) * 6;
-            const int64_t o = sgx * x;
-            auto cpa = [&](double *d, const double *src) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(src) : "memory");
-            };
-            if (qWA) cpa(dst + 0, qWA + o); else dst[0] = 1.0;
-            if (qSA) cpa(dst + 1, qSA + o); else dst[1] = 1.0;
-            cpa(dst + 2, qDA + o);
-            if (onB) {
-                if (qWB) cpa(dst + 3, qWB + o); else dst[3] = 1.0;
-                if (qSB) cpa(dst + 4, qSB + o); else dst[4] = 1.0;
-                cpa(dst + 5, qDB + o);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+    // The coefficients of step s (node column x = s - l + 1 of lane l's rows A and B: W, S, SW of A,
+    // then of B; 1.0 for unit faces) live in slot s % PD of the ring, PD = two chunks of CH steps.
+    // Warps 1..7 fill it a chunk ahead of the wavefront while warp 0 runs the chains and the fronts
+    // (one named barrier of the CTA per chunk): consecutive threads take consecutive columns of one
+    // row, so a chunk's 64-byte row segments are read whole instead of one node per lane and step.
+    constexpr int CH = s9::PD / 2;
+    // hand-off of ring half h (chunks c with c % 2 = h): named barriers FULL[h] = 1 + h (the producer
+    // warps arrive when a chunk is stored, the wavefront warp waits before it reads the chunk) and
+    // EMPTY[h] = 3 + h (the wavefront warp arrives when it has read the chunk, the producers wait
+    // before they overwrite the half)
+    auto bar_cnt = [](int) { return 32 + s9::NPROD; };
+    auto bar_wait = [&](int id, int cnt) {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+        SW_JITTER_POINT();
     };
-    if (threadIdx.x < 32)
-        for (int s = 0; s < s9::PD; ++s) fetch(s);
-    // the corner's coefficients (threads 32..63: member m = (-(m & 1), -(m >> 1)), neighbour k)
-    if (threadIdx.x >= 32 && threadIdx.x < 64 && (cx || cy)) {
-        const int m = (threadIdx.x - 32) >> 3, kk = threadIdx.x & 7;
-        CC[m * 8 + kk] = coef(kk, gxo(-(m & 1)), gyo(-(m >> 1)));
-    }
+    auto bar_arrive = [&](int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); };
     int fl = 0;
     // ---- the chain data (threads 0..127, item (chain, k)): chain 0 = local row 0 (node (k, 0),
     // partner (k, -1) across the y start face), chain 1 = local column 0 (node (0, k), partner
@@ -305,10 +295,16 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
             }
         }
     }
-    // ---- the start corner (thread 0): the dense 4 x 4 set, a pair across the one coupled face,
-    // or a single node without implicit neighbours in the domain (u = r0, nothing to do)
-    __syncthreads();                                          // CC
-    if (threadIdx.x == 0 && (cx || cy)) {
+    // ---- the start corner (warp 4, while warps 0..3 prepare the chain data): the dense 4 x 4 set,
+    // a pair across the one coupled face, or a single node without implicit neighbours in the
+    // domain (u = r0, nothing to do).  The lanes stage the members' coefficients (member
+    // m = (-(m & 1), -(m >> 1)), neighbour k), lane 0 solves.
+    if (threadIdx.x >= 128 && threadIdx.x < 160 && (cx || cy)) {
+        CC[lane] = coef(lane & 7, gxo(-((lane >> 3) & 1)), gyo(-(lane >> 4)));
+        __syncwarp();
+        SW_JITTER_POINT();
+    }
+    if (threadIdx.x == 128 && (cx || cy)) {
         if (cx && cy) {
             constexpr int k = 4;
             int mx[4] = {0, -1, 0, -1}, my[4] = {0, 0, -1, -1};
@@ -404,16 +400,29 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
             const int so = ch == 0 ? 1 : WX, sp = ch == 0 ? -WX : -1;   // window strides along / across
             double *const xc = XN + wi(0, 0);
             double u_op = xc[0], u_pp = cpl ? xc[sp] : 0.0;             // the corner's results
-            const double *cd = CD + ch * 64 * s9::CDW;
+            const double *const cd = CD + ch * 64 * s9::CDW;
+            // the operands of step k + 1 are loaded before the store of step k (off the dependent chain)
+            const int k1 = len > 1 ? 1 : 0;
+            double n_r0o = xc[k1 * so], n_r0p = cpl ? xc[k1 * so + sp] : 0.0, n_c[7];
+#pragma unroll
+            for (int j = 0; j < 7; ++j) n_c[j] = cd[k1 * s9::CDW + j];
+#pragma unroll 2
             for (int k = 1; k < len; ++k) {
-                cd += s9::CDW;
-                const double r0o = xc[k * so], r0p = cpl ? xc[k * so + sp] : 0.0;
-                const double in_o = fma(cd[0], u_op, r0o);
-                const double acc_o = fma(cd[1], u_pp, in_o);
-                const double acc_p = fma(cd[3], u_op, fma(cd[2], u_pp, r0p));
+                const double r0o = n_r0o, r0p = n_r0p;
+                double c[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) c[j] = n_c[j];
+                const int kn = k + 1 < len ? k + 1 : k;
+                n_r0o = xc[kn * so];
+                n_r0p = cpl ? xc[kn * so + sp] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 7; ++j) n_c[j] = cd[kn * s9::CDW + j];
+                const double in_o = fma(c[0], u_op, r0o);
+                const double acc_o = fma(c[1], u_pp, in_o);
+                const double acc_p = fma(c[3], u_op, fma(c[2], u_pp, r0p));
                 const double r0a = pfirst ? acc_p : acc_o, r0b = pfirst ? acc_o : acc_p;
-                const double ub = fma(-cd[5], r0a, r0b) * cd[6];
-                const double ua = fma(-cd[4], ub, r0a);
+                const double ub = fma(-c[5], r0a, r0b) * c[6];
+                const double ua = fma(-c[4], ub, r0a);
                 const double uo = cpl ? (pfirst ? ub : ua) : in_o;
                 u_pp = pfirst ? ua : ub;
                 u_op = uo;
@@ -440,9 +449,9 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
             auto ldv = [&](int s, double (&c)[6], double &aA, double &aB, double &r0A, double &r0B, double &row0) {
                 const int x = s - lane + 1;
                 const int xl = x < 1 ? 1 : (x >= T0 ? T0 - 1 : x);
-                const double *cr = RING + ((s % s9::PD) * 32 + lane) * 6;
+                const double *cr = RING + (s % s9::PD) * s9::RSL + lane;   // [slot][coefficient][lane]
 #pragma unroll
-                for (int j = 0; j < 6; ++j) c[j] = cr[j];
+                for (int j = 0; j < 6; ++j) c[j] = cr[j * s9::RJL];
                 aA = AW[ai(xl, rAl)];
                 aB = AW[ai(xl, rBl)];
                 r0A = XN[wi(xl, rAl)];
@@ -450,7 +459,8 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 row0 = XN[wi(xl, 0)];
             };
             double c6[6], aA, aB, r0A, r0B, row0;
-            asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 1) : "memory");   // group 0
+            const int NC = (NSTEP + CH) / CH;                         // chunks (step NSTEP is read ahead)
+            bar_wait(1, bar_cnt(0));                                  // chunk 0 is in the ring
             ldv(0, c6, aA, aB, r0A, r0B, row0);
             for (int s = 0; s < NSTEP; ++s) {
                 const int x = s - lane + 1;
@@ -459,9 +469,13 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 const double mWA = aA * c6[0], mSA = aA * c6[1], mDA = aA * c6[2];
                 const double mWB = aB * c6[3], mSB = aB * c6[4], mDB = aB * c6[5];
                 const double cr0A = r0A, cr0B = r0B, crow0 = row0;
-#ifndef SW_S9_NOWAIT
-                asm volatile("cp.async.wait_group %0;" ::"n"(s9::PD - 2) : "memory");   // group s + 1
-#endif
+                // step s + 1 opens chunk c + 1: the chunk c this step closes has been read (this step's
+                // operands are in registers), its half may be refilled; wait for chunk c + 1
+                if ((s + 1) % CH == 0) {
+                    const int c = (s + 1) / CH - 1;
+                    if (c + 2 < NC) bar_arrive(3 + (c & 1), bar_cnt(c & 1));
+                    bar_wait(1 + ((c + 1) & 1), bar_cnt((c + 1) & 1));
+                }
                 ldv(s + 1, c6, aA, aB, r0A, r0B, row0);
                 const double S = sel_f64(lane == 0, crow0, shfl_up1_f64(uBp));
                 const double uA = fma(mDA, SWA, fma(mSA, S, fma(mWA, WA, cr0A)));
@@ -472,10 +486,79 @@ __global__ void __launch_bounds__(s9::NT, 2) k_sweep9(Sweep9Args A) {
                 WA = sel_f64(act, uA, WA);
                 WB = sel_f64(act, uB, WB);
                 uBp = uB;
-                fetch(s + s9::PD);                                     // slot s % PD is consumed
             }
         }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else if (T0 > 1 && T1 > 1) {
+        const int pt = (int)threadIdx.x - 32;                                   // producer thread index
+        // ---- warps 1..7: the wavefront's coefficient ring; the loads of chunk c + 1 are in flight
+        //      while the producers wait for the half of chunk c to be free
+        const int nl = T1 / 2, NSTEP = (T0 - 1) + (nl - 1);
+        const int NC = (NSTEP + CH) / CH;
+        constexpr int NP = s9::NPROD, NE = 32 * 6 * CH, NI = (NE + NP - 1) / NP;     // producer threads, items per chunk
+        // item k of a producer thread: ring element e = pt + k NP = ((l * 6 + j) * CH + sl), i.e. step
+        // c CH + sl of lane l, coefficient j -- the same (l, j, sl) in every chunk, so the row's source
+        // pointer (at column x = 0), the column offset and the ring index are set up once
+        const double *psrc[NI];
+        int pxo[NI], pdst[NI];
+        {
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {
+                const int e = pt + k * NP;
+                const int sl = e % CH, lj = e / CH, j = lj % 6, l = lj / 6;
+                const int r = 2 * l + 1 + (j >= 3), a = j % 3;
+                const bool ok = e < NE && r < T1;
+                const int64_t i = gidx(G, gxo(0), gyo(ok ? r : 0), 0);
+                psrc[k] = !ok ? nullptr
+                              : (a == 0 ? (A.f0 ? A.f0 + i + sx : nullptr)
+                                        : (a == 1 ? (A.f1 ? A.f1 + i + sy * P0 : nullptr) : fdg + i + sx + sy * P0));
+                pxo[k] = ok ? sl - l + 1 : -(1 << 20);                     // x = c CH + pxo (never in range if !ok)
+                pdst[k] = sl * s9::RSL + j * s9::RJL + l;                  // + (c % 2) CH RSL
+            }
+        }
+        const int sgx = sx ? -1 : 1;
+        auto pload = [&](int c, double (&v)[NI]) {                         // chunk c into registers
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {
+                const int x = c * CH + pxo[k];
+                v[k] = (psrc[k] && x >= 1 && x < T0) ? __ldg(psrc[k] + sgx * x) : 1.0;
+            }
+        };
+        auto pstore = [&](int c, const double (&v)[NI]) {                  // registers into half c % 2
+            double *const half = RING + (c & 1) * (CH * s9::RSL);
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {
+                const int x = c * CH + pxo[k];
+                if (x >= 1 && x < T0) half[pdst[k]] = v[k];
+            }
+        };
+        double pv[NI];
+        pload(0, pv);
+        for (int c = 0; c < NC; ++c) {
+            if (c >= 2) bar_wait(3 + (c & 1), bar_cnt(c & 1));
+            pstore(c, pv);
+            bar_arrive(1 + (c & 1), bar_cnt(c & 1));
+            if (c + 1 < NC) pload(c + 1, pv);
+#if SW_S9_AHEAD > 0
+            if (c == SW_S9_AHEAD_AT) {
+                // look-ahead: the lines of the box SW_S9_AHEAD launches later (window of x_old, b and
+                // the coefficient arrays, clamped to the domain) into L2 while this box runs its fronts
+                const int64_t nb = (int64_t)blockIdx.x + SW_S9_AHEAD;
+                if (nb < (int64_t)gridDim.x) {
+                    const int64_t nX0 = (nb % G.nt[0]) * T0 - 2, nY0 = (nb / G.nt[0] + G.toff[1]) * T1 - 2;
+                    const int NL = (T0 + 4 + 15) / 16 + 1;
+                    for (int e = pt; e < (T1 + 4) * NL * 6; e += NP) {
+                        const int a = e % 6, q = e / 6;
+                        int64_t gx = nX0 + 16 * (q % NL), gy = nY0 + q / NL;
+                        gx = gx < 0 ? 0 : (gx >= G.ng[0] ? G.ng[0] - 1 : gx);
+                        gy = gy < 0 ? 0 : (gy >= G.ng[1] ? G.ng[1] - 1 : gy);
+                        const double *base =
+                            a == 0 ? A.xo : (a == 1 ? A.b : (a == 2 ? A.f0 : (a == 3 ? A.f1 : (a == 4 ? A.dd : A.da))));
+                        if (base) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + gidx(G, gx, gy, 0)));
+                    }
+                }
+            }
+#endif
+        }
     }
     if (fl) atomicOr(A.flag, 1);
     SW_TMARK(t_fronts);

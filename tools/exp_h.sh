@@ -1,10 +1,12 @@
 #!/bin/bash
-# k_sweep9 wavefront: what the per-lane cp.async coefficient ring costs (timing-only builds)
 set -u
-TAG=${1:-expc}
+TAG=${1:-exph}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 bld() { SW_TRACE=${2:-0} SW_DEFINES="$1" python -c "from paper_1008_3699_b200 import build as b; b.build(force=True, jitter=False)" > $OUT/build.log 2>&1 || { echo "BUILD FAILED $1"; tail -5 $OUT/build.log; }; }
-for d in "" "SW_S9_NOFETCH" "SW_S9_NOWAIT"; do
+for d in "SW_S9_PSTART=1" "SW_S9_PSTART=1 SW_S9_AHEAD_AT=0"; do
+echo "== [$d]"; bld "$d"
+timeout 300 python -m pytest tests/test_gpu_ninepoint.py -m gpu -q 2>&1 | tail -1
+timeout 200 python tools/time_next.py 2>&1 | head -1
 echo "== trace [$d]"; bld "$d" 1
-timeout 120 python tools/phase_trace9.py 2>&1 | tail -7
+timeout 120 python tools/phase_trace9.py 2>&1 | tail -6
 done
