@@ -1,5 +1,7 @@
 #!/bin/bash
-# Look-ahead L2 prefetch experiments (k_sweep2v: SW_V2_AHEAD, k_sweep2p: SW_P2_AHEAD) and 16 prologue warps.
+# Look-ahead L2 prefetch experiments (k_sweep2v: SW_V2_AHEAD) and 16 prologue warps.  The k_sweep2p switches
+# (SW_P2_AHEAD, SW_P2_SWAP) measured slower and were removed from the kernel (profiles/r02_ahead_experiments.txt);
+# the script is kept as the record of what was run.
 # usage (under gpurun): bash tools/exp_ahead.sh TAG
 set -u
 TAG=${1:-ahead}
