@@ -233,7 +233,11 @@ __global__ void __launch_bounds__(128, 4)
     const Lay3 Y = lay3(T1, T2, FACES, A.has_aux);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *const ring = sm;
-    double *const rng = sm + Y.ring;                          // the x-lines' compact rings
+    // the x-lines' compact rings, entry E = (r0, c0 | c1, c2) split into two arrays of 16-byte halves
+    // (rng[2E..] and rng[HB + 2E..]): the wavefront's 16-byte loads of one half then spread over all
+    // eight 16-byte bank groups instead of every other one
+    double *const rng = sm + Y.ring;
+    const int HB = Y.rings / 2;                               // doubles before the second halves
     double *const res = sm + Y.res;
     double *const XE = sm + Y.xf;                             // x-edge results: (u, across z, across y) per column
     double *const MX = sm + Y.mx;
@@ -491,9 +495,9 @@ __global__ void __launch_bounds__(128, 4)
                 if ((lane & 3) == 0 && li < NLn && (L & cb) == L) {
                     double r0, cc[3];
                     compact(c, j, k, L, colw(c), colw(c - 1), colw(c + 1), r0, cc);
-                    double *e = rng + 4 * ring_first(T1, j, k);
+                    double *e = rng + 2 * ring_first(T1, j, k);
                     sts2(e, r0, cc[0]);
-                    sts2(e + 2, cc[1], cc[2]);
+                    sts2(e + HB, cc[1], cc[2]);
                 }
             }
         };
@@ -529,11 +533,12 @@ __global__ void __launch_bounds__(128, 4)
                         r0 = A.rscale ? al * xo : A.coef * xo;
                     }
                     const double c1 = al * fi1, c2 = al * fi2;
-                    const uint32_t e = smem_u32(rng + q.rb + 4 * q.pos);
+                    const uint32_t e = smem_u32(rng + q.rb / 2 + 2 * q.pos);
                     const int on = q.on && cact;
                     asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n"
-                                 " @p st.shared.v2.f64 [%1], {%2, %3};\n @p st.shared.v2.f64 [%1+16], {%4, %5};\n}\n"
-                                 ::"r"(on), "r"(e), "d"(r0), "d"(al * fi0), "d"(q.cuty ? 0.0 : c1), "d"(q.cutz ? 0.0 : c2)
+                                 " @p st.shared.v2.f64 [%1], {%2, %3};\n @p st.shared.v2.f64 [%6], {%4, %5};\n}\n"
+                                 ::"r"(on), "r"(e), "d"(r0), "d"(al * fi0), "d"(q.cuty ? 0.0 : c1), "d"(q.cutz ? 0.0 : c2),
+                                 "r"(e + 8u * (uint32_t)HB)
                                  : "memory");
                     q.pos += 4;
                     if (q.pos >= q.D) q.pos -= q.D;
@@ -620,11 +625,11 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         const int S = r ^ mm, jj = -(S & 1), kk = -(S >> 1);
-                        const double *e = rng + 4 * (ring_first(T1, jj, kk) + pos);
+                        const double *e = rng + 2 * (ring_first(T1, jj, kk) + pos);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) M[r][q] = (r == q) ? 1.0 : 0.0;
-                        M[r][r ^ 1] = -e[2];                     // toward the partner across y
-                        M[r][r ^ 2] = -e[3];                     // across z
+                        M[r][r ^ 1] = -e[HB];                    // toward the partner across y
+                        M[r][r ^ 2] = -e[HB + 1];                // across z
                         fR[r] = e[0];
                         fX[r] = e[1];
                     }
@@ -704,8 +709,8 @@ __global__ void __launch_bounds__(128, 4)
         const int pj = pax == 1 ? -1 : j, pk = pax == 2 ? -1 : k;
         const int qf = pax < 0 ? 1 : (((sb >> pax) & 1) == 0);
         const int Do = ring_depth(j, k), Dp = ring_depth(pj, pk);
-        const double *const ro = rng + 4 * ring_first(T1, j, k);
-        const double *const rp_ = rng + 4 * ring_first(T1, pj, pk);
+        const double *const ro = rng + 2 * ring_first(T1, j, k);
+        const double *const rp_ = rng + 2 * ring_first(T1, pj, pk);
         const int rrow = ((sz ? T2 - 1 - k : k) * T1 + (sy ? T1 - 1 - j : j)) * 4;
         named_bar(1, 128);                                    // B_0
         S3T(t_cb0);
@@ -734,6 +739,7 @@ __global__ void __launch_bounds__(128, 4)
         double W = 0.0, Wq = 0.0, u = 0.0, sS = 0.0, sB = 0.0;
         // 32-bit shared addresses (no generic-to-shared conversion in the loop)
         const uint32_t ro_a = smem_u32(ro), rp_a = smem_u32(rp_), xe_a = smem_u32(XE);
+        const uint32_t hb_b = 8u * (uint32_t)HB;             // byte offset of the second halves
         const uint32_t res_a = smem_u32(res) + 8 * (rrow);
         // coefficients of the step's column, prepared a step ahead (off the wavefront's dependence
         // chain): the couplings without the pair axis, the pair couplings and 1 / (1 - m m')
@@ -743,10 +749,10 @@ __global__ void __launch_bounds__(128, 4)
         };
         auto prep = [&](Co &o) {
             double c1, c2, d1, d2;
-            lds2u(ro_a + 32 * po, o.r0, o.c0);
-            lds2u(ro_a + 32 * po + 16, c1, c2);
-            lds2u(rp_a + 32 * pp, o.q0, o.d0);
-            lds2u(rp_a + 32 * pp + 16, d1, d2);
+            lds2u(ro_a + 16 * po, o.r0, o.c0);
+            lds2u(ro_a + 16 * po + hb_b, c1, c2);
+            lds2u(rp_a + 16 * pp, o.q0, o.d0);
+            lds2u(rp_a + 16 * pp + hb_b, d1, d2);
             const double cpp = pax == 1 ? c1 : c2, cqp = pax == 1 ? d1 : d2;
             o.e1 = pax == 1 ? 0.0 : c1;
             o.e2 = pax == 2 ? 0.0 : c2;
